@@ -1,0 +1,281 @@
+/*
+ * probegrid_b200 — C ABI of the B200 (sm_100a) learned-hash-probing hot path.
+ *
+ * Drop-in boundary for the reference package `probegrid`
+ * (/root/reference/pkg).  The reference's only native seam is its compiled
+ * Cython core, bound through the backend protocol
+ * (src/probegrid/backends/__init__.py:12-50, cython_backend.py:24-89).  Each
+ * "protocol" entry point below replaces one of those bindings with the same
+ * argument meaning; the "fused" entry points replace the Python orchestration
+ * above them (encoding.py, mlp.py, trainer.py, model_io.py) with whole-path
+ * kernels.  A maintainer binds them with ctypes exactly as
+ * paper_2312_17241_b200/_lib.py does.
+ *
+ * Conventions
+ *  - Every array argument is a DEVICE pointer unless its name starts with h_.
+ *  - Shapes are C-contiguous row-major, as the reference's memoryviews require.
+ *  - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).
+ *  - Calls are asynchronous on `stream`; they return PG_OK or an error code,
+ *    with a message available from pg_last_error() (thread-local).
+ *  - The library never allocates device memory on these paths; callers own
+ *    every buffer, including workspaces sized by the *_workspace_bytes calls.
+ *  - Suffix _f32 / _f64 selects float / double storage and arithmetic.
+ */
+#ifndef PROBEGRID_B200_H
+#define PROBEGRID_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PG_OK 0
+#define PG_ERR_ARG 1      /* invalid argument (shape, limit, null pointer)     */
+#define PG_ERR_CUDA 2     /* CUDA launch / runtime failure                     */
+#define PG_ERR_DOMAIN 3   /* a coordinate lies outside [0,1]^d                 */
+
+#define PG_MAX_LEVELS 64    /* model file limit, model_io.py:207              */
+#define PG_MAX_FEATURE 16   /* compiled limit, cython_backend.py:9            */
+#define PG_MAX_PROBES 256   /* 8-bit baked storage, model.py:61-62            */
+#define PG_MAX_LAYERS 17    /* n_hidden_layers <= 16, model_io.py:213         */
+
+/* level kinds: indexing.py:26-41 + model.py:150 (probing iff hashed & conf) */
+#define PG_LEVEL_DENSE 0
+#define PG_LEVEL_HASHED 1
+#define PG_LEVEL_PROBED 2
+
+/* flags */
+#define PG_EXACT_MLP 1u   /* MLP in the reference's operation order, no FMA   */
+#define PG_SIGMOID 2u     /* logistic output (HyperParams.out_sigmoid)        */
+#define PG_SURROGATE 4u   /* softmax-mixture forward (encoding.py:45-47)      */
+#define PG_HALF_FEATS 8u  /* feature tables stored as IEEE binary16           */
+
+/* Geometry of one multiresolution grid (HyperParams + build_level_specs,
+ * model.py:35-87, indexing.py:93-101).  Feature tables of all levels are one
+ * buffer [n_levels][n_f][feature_dim]; probed levels additionally own slot
+ * `slot[l]` of conf [n_probed][n_c][n_p] and baked [n_probed][n_c]. */
+typedef struct pg_grid {
+    int32_t d;            /* 2 or 3                                          */
+    int32_t n_levels;
+    int32_t feature_dim;  /* F                                               */
+    int32_t n_f;          /* rows per feature table (power of two)           */
+    int32_t n_c;          /* rows per index/confidence table (power of two)  */
+    int32_t log2_np;      /* log2 of the probing range N_p                   */
+    int32_t res[PG_MAX_LEVELS];
+    int32_t kind[PG_MAX_LEVELS];
+    int32_t slot[PG_MAX_LEVELS];
+    uint32_t primary[3];  /* indexing.py:22 */
+    uint32_t aux[3];      /* indexing.py:23 */
+} pg_grid;
+
+/* Tiny MLP shape (mlp.py:16-52): weights (fan_in, fan_out) row-major; the
+ * parameter buffer is [W0 | b0 | W1 | b1 | ...] in that order. */
+typedef struct pg_mlp {
+    int32_t n_layers;
+    int32_t widths[PG_MAX_LAYERS + 1];
+} pg_mlp;
+
+const char *pg_last_error(void);
+const char *pg_version(void);
+int pg_device_sm_count(int device);
+
+/* ------------------------------------------------------------------------
+ * Protocol kernels: one level / one layer per call, numpy-backend semantics.
+ * ---------------------------------------------------------------------- */
+
+/* replaces _core.dense_fwd (_core.pyx:26-54) via cython_backend.dense_fwd
+ * (cython_backend.py:24-31).  out must be zero-initialised by the caller. */
+int pg_dense_fwd_f32(const float *xs, int64_t B, int d, int64_t res,
+                     const float *feats, int F, float *out, int32_t *idx,
+                     float *wgt, void *stream);
+int pg_dense_fwd_f64(const double *xs, int64_t B, int d, int64_t res,
+                     const double *feats, int F, double *out, int32_t *idx,
+                     double *wgt, void *stream);
+
+/* replaces _core.hashed_fwd (_core.pyx:57-84), cython_backend.py:34-42;
+ * primary points to d host uint32 primes. */
+int pg_hashed_fwd_f32(const float *xs, int64_t B, int d, int64_t res,
+                      uint32_t nf_mask, const float *feats, int F,
+                      const uint32_t *h_primary, float *out, int32_t *idx,
+                      float *wgt, void *stream);
+int pg_hashed_fwd_f64(const double *xs, int64_t B, int d, int64_t res,
+                      uint32_t nf_mask, const double *feats, int F,
+                      const uint32_t *h_primary, double *out, int32_t *idx,
+                      double *wgt, void *stream);
+
+/* replaces _core.probed_fwd (_core.pyx:87-122), cython_backend.py:45-55 */
+int pg_probed_fwd_f32(const float *xs, int64_t B, int d, int64_t res,
+                      uint32_t nf_mask, uint32_t nc_mask, int log2_np,
+                      const float *feats, int F, const uint8_t *baked,
+                      const uint32_t *h_primary, const uint32_t *h_aux,
+                      float *out, int32_t *base, int32_t *row, float *wgt,
+                      void *stream);
+int pg_probed_fwd_f64(const double *xs, int64_t B, int d, int64_t res,
+                      uint32_t nf_mask, uint32_t nc_mask, int log2_np,
+                      const double *feats, int F, const uint8_t *baked,
+                      const uint32_t *h_primary, const uint32_t *h_aux,
+                      double *out, int32_t *base, int32_t *row, double *wgt,
+                      void *stream);
+
+/* replaces _core.indexed_bwd (_core.pyx:125-137): gfeat[idx] += w*up */
+int pg_indexed_bwd_f32(const float *up, int64_t B, int F, const int32_t *idx,
+                       const float *wgt, int C, float *gfeat, void *stream);
+int pg_indexed_bwd_f64(const double *up, int64_t B, int F, const int32_t *idx,
+                       const double *wgt, int C, double *gfeat, void *stream);
+
+/* replaces _core.dedup_rows (_core.pyx:140-160): same first-encounter order.
+ * Workspace: pg_dedup_workspace_bytes(n, n_c).  *d_count receives U. */
+int64_t pg_dedup_workspace_bytes(int64_t n, int64_t n_c);
+int pg_dedup_rows(const int32_t *row, int64_t n, int64_t n_c, void *workspace,
+                  int32_t *rows_u, int32_t *inv, int32_t *d_count,
+                  void *stream);
+
+/* replaces _core.probed_bwd (_core.pyx:163-221) */
+int pg_probed_bwd_f32(const float *up, int64_t B, int F, const int32_t *base,
+                      const int32_t *inv, const float *wgt, int C,
+                      const float *smu, int n_p, const float *feats,
+                      float *gfeat, float *gconf_u, void *stream);
+int pg_probed_bwd_f64(const double *up, int64_t B, int F, const int32_t *base,
+                      const int32_t *inv, const double *wgt, int C,
+                      const double *smu, int n_p, const double *feats,
+                      double *gfeat, double *gconf_u, void *stream);
+
+/* replaces _core.adam_rebake_rows (_core.pyx:224-272); corr1/corr2 are
+ * 1-beta^t as cython_backend.py:73-77 passes them. */
+int pg_adam_rebake_rows_f32(float *conf, float *m, float *v, int n_p,
+                            uint8_t *baked, const int32_t *rows_u, int64_t U,
+                            const float *gconf_u, double corr1, double corr2,
+                            double lr, double beta1, double beta2, double eps,
+                            void *stream);
+int pg_adam_rebake_rows_f64(double *conf, double *m, double *v, int n_p,
+                            uint8_t *baked, const int32_t *rows_u, int64_t U,
+                            const double *gconf_u, double corr1, double corr2,
+                            double lr, double beta1, double beta2, double eps,
+                            void *stream);
+
+/* replaces cython_backend.mlp_infer_rows (cython_backend.py:80-89, i.e.
+ * _core.linear_rows/_core.sigmoid_rows, _core.pyx:275-298): row-wise, in the
+ * reference's operation order (bit-identical), any widths.  act_ws needs
+ * 2*B*max(widths) elements. */
+int pg_mlp_infer_rows_f32(const float *xs, int64_t B, const pg_mlp *mlp,
+                          const float *params, unsigned flags, float *act_ws,
+                          float *out, void *stream);
+int pg_mlp_infer_rows_f64(const double *xs, int64_t B, const pg_mlp *mlp,
+                          const double *params, unsigned flags,
+                          double *act_ws, double *out, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Fused B200 kernels (all levels / the whole MLP per launch).
+ * ---------------------------------------------------------------------- */
+
+/* encoding.encode_forward (encoding.py:42-86) for all levels at once:
+ * y (B, L*F).  flags: PG_SURROGATE (needs conf), PG_HALF_FEATS (feats is
+ * binary16).  *d_bad (optional) is set to 1 if any coordinate is outside
+ * [0,1] (encoding.py:33-39). */
+int pg_encode_fwd_f32(const pg_grid *grid, const float *xs, int64_t B,
+                      const void *feats, const uint8_t *baked,
+                      const float *conf, unsigned flags, float *y,
+                      int32_t *d_bad, void *stream);
+int pg_encode_fwd_f64(const pg_grid *grid, const double *xs, int64_t B,
+                      const void *feats, const uint8_t *baked,
+                      const double *conf, unsigned flags, double *y,
+                      int32_t *d_bad, void *stream);
+
+/* encoding.encode_backward (encoding.py:89-133) for all levels at once.
+ * Recomputes geometry from xs; accumulates into gfeat [L][n_f][F] and
+ * gconf [P][n_c][N_p]; marks every looked-up confidence row in
+ * touched [P][n_c] (uint8, set to 1), including zero-weight corners. */
+int pg_encode_bwd_f32(const pg_grid *grid, const float *xs, int64_t B,
+                      const float *dy, const float *feats, const float *conf,
+                      float *gfeat, float *gconf, uint8_t *touched,
+                      void *stream);
+int pg_encode_bwd_f64(const pg_grid *grid, const double *xs, int64_t B,
+                      const double *dy, const double *feats,
+                      const double *conf, double *gfeat, double *gconf,
+                      uint8_t *touched, void *stream);
+
+/* model_io.decode_pixels (model_io.py:292-311): fused encode + MLP forward
+ * per 128-query tile; out (B, out_dim).  Fast path for widths
+ * [L*F = 32, 64, 64, out_dim <= 4]; other shapes run the generic kernels
+ * (then ws must hold B*(L*F) + 2*B*max(widths) floats, else ws may be 0).
+ * PG_EXACT_MLP reproduces _core.linear_rows bit for bit. */
+int pg_decode_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
+                  int64_t B, const void *feats, const uint8_t *baked,
+                  const float *params, unsigned flags, float *ws, float *out,
+                  void *stream);
+
+/* End-to-end decode from HOST memory (pinned for overlap): chunks of
+ * `chunk` queries alternate between two streams, H2D copy -> fused decode ->
+ * D2H copy, so transfers overlap compute.  d_xs must hold 2*chunk*d floats,
+ * d_out 2*chunk*out_dim floats.  Returns after both streams drain. */
+int pg_decode_host_f32(const pg_grid *grid, const pg_mlp *mlp,
+                       const float *h_xs, int64_t B, const void *feats,
+                       const uint8_t *baked, const float *params,
+                       unsigned flags, int64_t chunk, float *d_xs,
+                       float *d_out, float *h_out, void *stream0,
+                       void *stream1);
+
+/* Training MLP pass (trainer.py:122-137 + mlp.py:55-85): forward, squared
+ * error loss (sum in fp64 into *loss_sum), dpred = diff*scale, backward.
+ * Accumulates parameter grads into gparams (same layout as params) and
+ * writes dy (B, widths[0]).  targets (B, out_dim).  flags: PG_SIGMOID.
+ * ws: pg_mlp_train_workspace_floats(B, mlp) floats (0 for the fast path). */
+int64_t pg_mlp_train_workspace_floats(int64_t B, const pg_mlp *mlp);
+int pg_mlp_train_f32(const pg_mlp *mlp, const float *y, const float *targets,
+                     int64_t B, const float *params, float scale,
+                     unsigned flags, float *gparams, float *dy,
+                     double *loss_sum, float *ws, void *stream);
+int pg_mlp_train_f64(const pg_mlp *mlp, const double *y, const double *targets,
+                     int64_t B, const double *params, double scale,
+                     unsigned flags, double *gparams, double *dy,
+                     double *loss_sum, double *ws, void *stream);
+
+/* Pixel batch for the image trainer (trainer.py:109-116): xs from pixel
+ * indices pix (host-drawn for reference parity, or drawn on device from
+ * (seed, step) when pix_in is NULL and pix_out receives them), targets
+ * gathered from the HxWxC image. */
+int pg_pixel_batch_f32(const int64_t *pix_in, int64_t B, int width,
+                       int height, const float *image, int channels,
+                       uint64_t seed, uint64_t step, int64_t *pix_out,
+                       float *xs, float *targets, void *stream);
+int pg_pixel_batch_f64(const int64_t *pix_in, int64_t B, int width,
+                       int height, const double *image, int channels,
+                       uint64_t seed, uint64_t step, int64_t *pix_out,
+                       double *xs, double *targets, void *stream);
+
+/* trainer.adam_update (trainer.py:73-84) over one flat buffer, reference
+ * rounding order; zeroes grad afterwards (trainer.py:157-161).
+ * d_guard (optional): when *d_guard is not finite (a diverged loss,
+ * trainer.py:130-132) the update is skipped and only the gradient cleared. */
+int pg_adam_f32(float *param, float *grad, float *m, float *v, int64_t n,
+                int64_t t, double lr, double beta1, double beta2, double eps,
+                const double *d_guard, void *stream);
+int pg_adam_f64(double *param, double *grad, double *m, double *v, int64_t n,
+                int64_t t, double lr, double beta1, double beta2, double eps,
+                const double *d_guard, void *stream);
+
+/* Lazy Adam + incremental re-bake over every confidence row whose touched
+ * flag is set (trainer.py:162-167 with _core.pyx:224-272 arithmetic), then
+ * clears that row's gradient and flag.  rows = n_probed*n_c. */
+int pg_lazy_adam_rebake_f32(float *conf, float *m, float *v, uint8_t *baked,
+                            float *gconf, uint8_t *touched, int64_t rows,
+                            int n_p, int64_t t, double lr, double beta1,
+                            double beta2, double eps, const double *d_guard,
+                            void *stream);
+int pg_lazy_adam_rebake_f64(double *conf, double *m, double *v,
+                            uint8_t *baked, double *gconf, uint8_t *touched,
+                            int64_t rows, int n_p, int64_t t, double lr,
+                            double beta1, double beta2, double eps,
+                            const double *d_guard, void *stream);
+
+/* touched flags as fp32 counts (for the data-parallel allreduce) and back */
+int pg_touched_to_f32(const uint8_t *touched, int64_t n, float *out,
+                      void *stream);
+int pg_touched_from_f32(const float *in, int64_t n, uint8_t *touched,
+                        void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PROBEGRID_B200_H */

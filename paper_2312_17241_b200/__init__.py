@@ -1,0 +1,41 @@
+"""B200-native learned-hash-probing hot path (arXiv 2312.17241).
+
+Drop-in for the reference package ``probegrid``'s encoder / model / trainer /
+decode entry points and its backend plugin protocol (``backend``), running
+hand-written sm_100a CUDA through the C ABI in include/probegrid_b200.h.
+Importing this package does not touch the GPU; the first kernel call loads
+libprobegrid_b200.so and fails loudly if it or a CUDA device is missing.
+"""
+
+__version__ = "0.1.0"
+
+from .errors import (DomainViolation, InvalidHyperparameter, ProbeGridError, ShapeMismatch,
+                     StaleTrace, TrainingDiverged, UnbakedModel)
+from .hyper import (AUX_PRIMES, PRIMARY_PRIMES, HyperParams, LevelMode, LevelSpec,
+                    build_level_specs, level_resolution)
+
+__all__ = [
+    "AUX_PRIMES", "PRIMARY_PRIMES", "HyperParams", "LevelMode", "LevelSpec", "build_level_specs",
+    "level_resolution", "ProbeGridError", "InvalidHyperparameter", "DomainViolation",
+    "ShapeMismatch", "StaleTrace", "TrainingDiverged", "UnbakedModel",
+    "init_model", "Model", "encode_forward", "encode_backward", "TrainConfig", "TrainState", "fit",
+    "to_inference", "decode_pixels", "decode_at", "decode_rect", "decode_image", "InferenceModel",
+]
+
+
+def __getattr__(name):
+    # lazy: these import torch-backed modules
+    if name in ("init_model", "Model"):
+        from . import grid_model
+        return getattr(grid_model, name)
+    if name in ("encode_forward", "encode_backward"):
+        from . import encoding
+        return getattr(encoding, name)
+    if name in ("TrainConfig", "TrainState", "fit", "adam_update"):
+        from . import train
+        return getattr(train, name)
+    if name in ("to_inference", "decode_pixels", "decode_at", "decode_rect", "decode_image",
+                "InferenceModel", "TouchCounter", "HostDecoder"):
+        from . import decode
+        return getattr(decode, name)
+    raise AttributeError(name)

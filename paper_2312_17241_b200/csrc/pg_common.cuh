@@ -1,0 +1,160 @@
+// Shared device helpers for the probegrid B200 kernels (sm_100a).
+//
+// Bit-exactness contract: wherever a result must equal the reference's
+// (/root/reference/pkg/src/probegrid/backends/_core.pyx, compiled without
+// FMA contraction — pkg/setup.py:27-33) the code uses the explicitly rounded
+// intrinsics below (Ar<T>::mul/add/...), which nvcc never contracts.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/probegrid_b200.h"
+
+namespace pg {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string &msg);
+int check_launch(const char *what);
+
+#define PG_REQUIRE(cond, msg)            \
+    do {                                 \
+        if (!(cond)) {                   \
+            ::pg::set_error(msg);        \
+            return PG_ERR_ARG;           \
+        }                                \
+    } while (0)
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int grid_for(int64_t n, int block, int64_t cap = (int64_t)1 << 30) {
+    int64_t g = (n + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (int)g;
+}
+
+// ------------------------------------------------- explicitly rounded math
+template <typename T> struct Ar;
+template <> struct Ar<float> {
+    static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+    static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+    static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+    static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
+    static __device__ __forceinline__ float sqrt(float a) { return __fsqrt_rn(a); }
+    static __device__ __forceinline__ float fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+    static __device__ __forceinline__ float exp(float a) { return expf(a); }
+};
+template <> struct Ar<double> {
+    static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+    static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+    static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+    static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+    static __device__ __forceinline__ double sqrt(double a) { return __dsqrt_rn(a); }
+    static __device__ __forceinline__ double fma(double a, double b, double c) { return __fma_rn(a, b, c); }
+    static __device__ __forceinline__ double exp(double a) { return ::exp(a); }
+};
+
+// ------------------------------------------------------------ geometry
+// _core.pyx:17-23 + 38-40: cell = clamp(floor((double)x * res), 0, res-1),
+// t = x*(T)res - (T)cell in T.
+//
+// float: x*res is exact in 48 bits, so floor((double)x*res) equals the floor
+// of the exact product.  We get it in fp32: p = RN(x*res), e = x*res - p
+// (exact via FMA); floor(exact) = floor(p) - [p integral and e < 0].  p cannot
+// jump over an integer because integers below 2^24 are representable.
+__device__ __forceinline__ int cell_coord(float x, int res, float &t) {
+    const float rf = (float)res;
+    const float p = __fmul_rn(x, rf);
+    const float e = __fmaf_rn(x, rf, -p);
+    float fl = floorf(p);
+    if (p == fl && e < 0.0f) fl -= 1.0f;
+    int c = (int)fl;
+    c = c > res - 1 ? res - 1 : c;
+    c = c < 0 ? 0 : c;
+    t = __fsub_rn(p, (float)c);
+    return c;
+}
+// double: the reference rounds the double product, then floors it.
+__device__ __forceinline__ int cell_coord(double x, int res, double &t) {
+    const double p = __dmul_rn(x, (double)res);
+    double fl = floor(p);
+    int c = (int)fl;
+    c = c > res - 1 ? res - 1 : c;
+    c = c < 0 ? 0 : c;
+    t = __dsub_rn(p, (double)c);
+    return c;
+}
+
+// corner k has offset bit (d-1-i) on axis i (numpy_backend.py:10, 37-41);
+// w = ((1*a_0)*a_1)*a_2 with a_i = t_i or 1-t_i (_core.pyx:44-47).
+template <typename T, int D>
+__device__ __forceinline__ T corner_weight(int k, const T (&t)[D], const T (&omt)[D]) {
+    T w = ((k >> (D - 1)) & 1) ? t[0] : omt[0];
+#pragma unroll
+    for (int i = 1; i < D; ++i) w = Ar<T>::mul(w, ((k >> (D - 1 - i)) & 1) ? t[i] : omt[i]);
+    return w;
+}
+
+template <int D>
+__device__ __forceinline__ uint32_t corner_hash(int k, const int (&c)[D], const uint32_t *pr) {
+    uint32_t h = 0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) h ^= (uint32_t)(c[i] + ((k >> (D - 1 - i)) & 1)) * pr[i];
+    return h;
+}
+
+// row-major dense vertex index v_0 + s*(v_1 + s*v_2), s = res+1 (_core.pyx:48-50)
+template <int D>
+__device__ __forceinline__ int corner_dense(int k, const int (&c)[D], int stride) {
+    int lin = 0;
+#pragma unroll
+    for (int i = D - 1; i >= 0; --i) lin = lin * stride + (c[i] + ((k >> (D - 1 - i)) & 1));
+    return lin;
+}
+
+// ------------------------------------------------- feature row loads
+template <typename FT> struct Feat;
+template <> struct Feat<float> {
+    static __device__ __forceinline__ float ld(const float *p) { return __ldg(p); }
+    static __device__ __forceinline__ float2 ld2(const float *p) {
+        return __ldg(reinterpret_cast<const float2 *>(p));
+    }
+};
+template <> struct Feat<double> {
+    static __device__ __forceinline__ double ld(const double *p) { return __ldg(p); }
+};
+template <> struct Feat<__half> {
+    static __device__ __forceinline__ float ld(const __half *p) { return __half2float(__ldg(p)); }
+    static __device__ __forceinline__ float2 ld2(const __half *p) {
+        return __half22float2(__ldg(reinterpret_cast<const __half2 *>(p)));
+    }
+};
+
+// ------------------------------------------------------ vector reductions
+// sm_90+ vector float reductions straight into L2 (REDG.E.ADD.F32x4).
+__device__ __forceinline__ void red_add_v4(float *p, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
+                 "f"(d)
+                 : "memory");
+}
+__device__ __forceinline__ void red_add_v2(float *p, float a, float b) {
+    asm volatile("red.global.add.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(a), "f"(b) : "memory");
+}
+__device__ __forceinline__ void red_add(float *p, float a) { atomicAdd(p, a); }
+__device__ __forceinline__ void red_add(double *p, double a) { atomicAdd(p, a); }
+
+// ------------------------------------------------------- level table
+struct LevelTab {
+    int res[PG_MAX_LEVELS];
+    int kind[PG_MAX_LEVELS];
+    int slot[PG_MAX_LEVELS];
+};
+
+int validate_grid(const pg_grid *g);
+
+}  // namespace pg

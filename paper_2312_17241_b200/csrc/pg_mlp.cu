@@ -1,0 +1,569 @@
+// The tiny decoder MLP on sm_100a (mlp.py:16-85, _core.pyx:275-298):
+//  * generic row-wise kernels for any widths (protocol mlp_infer_rows, and
+//    the training pass for shapes the fused kernels do not cover);
+//  * the fused decode kernel: all-level encode + [32,64,64,<=4] MLP per
+//    128-query tile, activations resident in shared memory.
+#include "pg_common.cuh"
+
+namespace pg {
+
+// =========================================================================
+// Generic row-wise linear layer in the reference's order: acc = b_j, then
+// acc += x_i * W_ij for i ascending (no FMA unless !exact), optional ReLU
+// (acc < 0 -> 0, so NaN/-0 pass like _core.pyx:287-288) and logistic
+// evaluated in double (_core.pyx:292-298).
+// =========================================================================
+template <typename T, bool EXACT>
+__global__ void linear_rows_kernel(const T *__restrict__ a, int64_t B, int fin,
+                                   const T *__restrict__ W, const T *__restrict__ bias, int fout,
+                                   T *__restrict__ out, int relu, int sigmoid) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B * fout) return;
+    const int64_t b = i / fout;
+    const int j = (int)(i - b * fout);
+    const T *ar = a + b * fin;
+    T acc = bias[j];
+    for (int k = 0; k < fin; ++k) {
+        if (EXACT)
+            acc = Ar<T>::add(acc, Ar<T>::mul(ar[k], W[(int64_t)k * fout + j]));
+        else
+            acc = Ar<T>::fma(ar[k], W[(int64_t)k * fout + j], acc);
+    }
+    if (relu && acc < T(0)) acc = T(0);
+    if (sigmoid) acc = (T)(1.0 / (1.0 + ::exp(-(double)acc)));
+    out[i] = acc;
+}
+
+static int64_t mlp_param_count(const pg_mlp *m) {
+    int64_t n = 0;
+    for (int l = 0; l < m->n_layers; ++l) n += (int64_t)m->widths[l] * m->widths[l + 1] + m->widths[l + 1];
+    return n;
+}
+static int mlp_max_width(const pg_mlp *m) {
+    int w = 0;
+    for (int l = 0; l <= m->n_layers; ++l) w = m->widths[l] > w ? m->widths[l] : w;
+    return w;
+}
+static int validate_mlp(const pg_mlp *m) {
+    PG_REQUIRE(m != nullptr, "null mlp");
+    PG_REQUIRE(m->n_layers >= 1 && m->n_layers <= PG_MAX_LAYERS, "mlp layer count out of range");
+    for (int l = 0; l <= m->n_layers; ++l) PG_REQUIRE(m->widths[l] >= 1, "mlp width must be positive");
+    return PG_OK;
+}
+
+template <typename T>
+static int mlp_infer_rows_generic(const T *xs, int64_t B, const pg_mlp *mlp, const T *params,
+                                  unsigned flags, T *act_ws, T *out, cudaStream_t s) {
+    if (int e = validate_mlp(mlp)) return e;
+    if (B == 0) return PG_OK;
+    PG_REQUIRE(act_ws != nullptr || mlp->n_layers == 1, "mlp_infer_rows needs activation workspace");
+    const int maxw = mlp_max_width(mlp);
+    const T *a = xs;
+    const T *p = params;
+    const bool exact = (flags & PG_EXACT_MLP) != 0;
+    for (int l = 0; l < mlp->n_layers; ++l) {
+        const int fin = mlp->widths[l], fout = mlp->widths[l + 1];
+        const bool last = l == mlp->n_layers - 1;
+        T *dst = last ? out : act_ws + (int64_t)(l & 1) * B * maxw;
+        const int relu = last ? 0 : 1;
+        const int sig = (last && (flags & PG_SIGMOID)) ? 1 : 0;
+        const int grd = grid_for(B * fout, 256);
+        if (exact)
+            linear_rows_kernel<T, true><<<grd, 256, 0, s>>>(a, B, fin, p, p + (int64_t)fin * fout, fout, dst, relu, sig);
+        else
+            linear_rows_kernel<T, false><<<grd, 256, 0, s>>>(a, B, fin, p, p + (int64_t)fin * fout, fout, dst, relu, sig);
+        p += (int64_t)fin * fout + fout;
+        a = dst;
+    }
+    return check_launch("mlp_infer_rows");
+}
+
+// =========================================================================
+// Fused decode: encode all 16 levels (F = 2) of a 128-query tile into
+// shared memory, then run the [32, 64, 64, out] MLP on it.
+//
+// Activation tiles are stored transposed, act[feature][query], 128 floats
+// per row with the 16-byte chunk index XOR-swizzled by (row >> 2) & 7, so
+//   - encode writes (32 consecutive queries of one feature) and
+//   - the MMA-style reads (one feature row, 4 chunks per warp) and
+//   - the epilogue writes (8 feature rows x 1 chunk per quarter-warp)
+// are all bank-conflict free.
+// Layer math: thread (og = tid % 16, pg = tid / 16) owns queries pg*8..+7 and
+// outputs og*4..+3 of a 128x64 layer tile (32 accumulators).
+// =========================================================================
+constexpr int kTP = 128;   // queries per tile
+constexpr int kIn = 32;    // L * F
+constexpr int kHid = 64;
+constexpr int kOutMax = 4;
+
+struct DecodeSmem {
+    float w0[kIn * kHid];
+    float w1[kHid * kHid];
+    float w2[kHid * kOutMax];
+    float b0[kHid];
+    float b1[kHid];
+    float b2[kOutMax];
+    float actA[kHid * kTP];  // y^T (rows 0..31) for layer 1, then h2^T for layer 3
+    float actB[kHid * kTP];  // h1^T
+    float outs[kTP * kOutMax];
+    float xs[kTP * 3];
+};
+
+__device__ __forceinline__ int swz(int row, int col) {
+    // element offset of act[row][col] in a swizzled 128-float row
+    const int chunk = (col >> 2) ^ ((row >> 2) & 7);
+    return row * kTP + (chunk << 2) + (col & 3);
+}
+
+template <bool EXACT>
+__device__ __forceinline__ float mac(float acc, float a, float w) {
+    return EXACT ? __fadd_rn(acc, __fmul_rn(a, w)) : __fmaf_rn(a, w, acc);
+}
+
+// 128 x 64 layer: out^T = act(in^T)^T W + b, K = fan_in.
+template <int K, bool EXACT>
+__device__ __forceinline__ void layer_tile(const float *__restrict__ in_t, const float *__restrict__ W,
+                                           const float *__restrict__ bias, float *__restrict__ out_t) {
+    const int og = threadIdx.x & 15, pg = threadIdx.x >> 4;
+    float acc[8][4];
+    const float4 bb = *reinterpret_cast<const float4 *>(bias + og * 4);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        acc[i][0] = bb.x;
+        acc[i][1] = bb.y;
+        acc[i][2] = bb.z;
+        acc[i][3] = bb.w;
+    }
+#pragma unroll 8
+    for (int k = 0; k < K; ++k) {
+        const float4 a0 = *reinterpret_cast<const float4 *>(in_t + swz(k, pg * 8));
+        const float4 a1 = *reinterpret_cast<const float4 *>(in_t + swz(k, pg * 8 + 4));
+        const float4 w = *reinterpret_cast<const float4 *>(W + k * kHid + og * 4);
+        const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            acc[i][0] = mac<EXACT>(acc[i][0], a[i], w.x);
+            acc[i][1] = mac<EXACT>(acc[i][1], a[i], w.y);
+            acc[i][2] = mac<EXACT>(acc[i][2], a[i], w.z);
+            acc[i][3] = mac<EXACT>(acc[i][3], a[i], w.w);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        float r[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r[i] = acc[i][j] < 0.0f ? 0.0f : acc[i][j];  // ReLU
+        const int row = og * 4 + j;
+        *reinterpret_cast<float4 *>(out_t + swz(row, pg * 8)) = make_float4(r[0], r[1], r[2], r[3]);
+        *reinterpret_cast<float4 *>(out_t + swz(row, pg * 8 + 4)) = make_float4(r[4], r[5], r[6], r[7]);
+    }
+}
+
+template <typename FT, int D, bool EXACT>
+__global__ void __launch_bounds__(256, 2)
+    decode_fused_kernel(const pg_grid g, const float *__restrict__ xs, int64_t B,
+                        const FT *__restrict__ feats, const uint8_t *__restrict__ baked,
+                        const float *__restrict__ params, int out_dim, int sigmoid,
+                        float *__restrict__ out, int32_t *__restrict__ bad) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    DecodeSmem &sm = *reinterpret_cast<DecodeSmem *>(smem_raw);
+    const int tid = threadIdx.x;
+    // ---- weights to shared memory once per CTA (params = [W0|b0|W1|b1|W2|b2]) ----
+    {
+        const float *p = params;
+        for (int i = tid; i < kIn * kHid; i += 256) sm.w0[i] = p[i];
+        p += kIn * kHid;
+        for (int i = tid; i < kHid; i += 256) sm.b0[i] = p[i];
+        p += kHid;
+        for (int i = tid; i < kHid * kHid; i += 256) sm.w1[i] = p[i];
+        p += kHid * kHid;
+        for (int i = tid; i < kHid; i += 256) sm.b1[i] = p[i];
+        p += kHid;
+        for (int i = tid; i < kHid * kOutMax; i += 256) {
+            const int k = i / kOutMax, j = i % kOutMax;
+            sm.w2[i] = j < out_dim ? p[k * out_dim + j] : 0.0f;
+        }
+        p += kHid * out_dim;
+        for (int i = tid; i < kOutMax; i += 256) sm.b2[i] = i < out_dim ? p[i] : 0.0f;
+    }
+    constexpr int C = 1 << D;
+    const uint32_t nf_mask = (uint32_t)g.n_f - 1u, nc_mask = (uint32_t)g.n_c - 1u;
+    const int64_t ntiles = (B + kTP - 1) / kTP;
+    const int pl = tid & (kTP - 1);
+    const int lhalf = tid >> 7;  // 0/1: which of the two levels per iteration
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t p0 = tile * kTP;
+        const int nvalid = (int)((B - p0) < kTP ? (B - p0) : kTP);
+        __syncthreads();  // previous tile's layer 3 finished reading actA / outs
+        for (int i = tid; i < kTP * D; i += 256) sm.xs[i] = i < nvalid * D ? xs[p0 * D + i] : 0.0f;
+        __syncthreads();
+        // ---------------- encode: thread = (query pl, levels lhalf, lhalf+2, ...) --------
+        float x[D];
+        bool oob = false;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            x[a] = sm.xs[pl * D + a];
+            oob |= !(x[a] >= 0.0f && x[a] <= 1.0f);
+        }
+        if (bad && oob && pl < nvalid && lhalf == 0) *bad = 1;
+#pragma unroll 2
+        for (int it = 0; it < 8; ++it) {
+            const int l = 2 * it + lhalf;  // warp-uniform
+            const int res = g.res[l], kind = g.kind[l];
+            int c[D];
+            float t[D], omt[D];
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                c[a] = cell_coord(x[a], res, t[a]);
+                omt[a] = __fsub_rn(1.0f, t[a]);
+            }
+            int idx[C];
+            float w[C];
+#pragma unroll
+            for (int k = 0; k < C; ++k) {
+                w[k] = corner_weight<float, D>(k, t, omt);
+                if (kind == PG_LEVEL_DENSE) {
+                    idx[k] = corner_dense<D>(k, c, res + 1);
+                } else {
+                    const uint32_t h = corner_hash<D>(k, c, g.primary);
+                    if (kind == PG_LEVEL_HASHED) {
+                        idx[k] = (int)(h & nf_mask);
+                    } else {
+                        const int r = (int)(corner_hash<D>(k, c, g.aux) & nc_mask);
+                        idx[k] = (int)((h << g.log2_np) & nf_mask) +
+                                 (int)__ldg(baked + (int64_t)g.slot[l] * g.n_c + r);
+                    }
+                }
+            }
+            const FT *tab = feats + (int64_t)l * g.n_f * 2;
+            float2 f[C];
+#pragma unroll
+            for (int k = 0; k < C; ++k) f[k] = Feat<FT>::ld2(tab + (int64_t)idx[k] * 2);
+            float y0 = 0.0f, y1 = 0.0f;  // _core.pyx:53-54 blend order, from zero
+#pragma unroll
+            for (int k = 0; k < C; ++k) {
+                y0 = __fadd_rn(y0, __fmul_rn(w[k], f[k].x));
+                y1 = __fadd_rn(y1, __fmul_rn(w[k], f[k].y));
+            }
+            sm.actA[swz(2 * l, pl)] = y0;
+            sm.actA[swz(2 * l + 1, pl)] = y1;
+        }
+        __syncthreads();
+        layer_tile<kIn, EXACT>(sm.actA, sm.w0, sm.b0, sm.actB);
+        __syncthreads();
+        layer_tile<kHid, EXACT>(sm.actB, sm.w1, sm.b1, sm.actA);
+        __syncthreads();
+        // ---------------- output layer: thread = (query, pair of outputs) -------------
+        {
+            const int q = tid & (kTP - 1);
+            const int j0 = (tid >> 7) * 2;
+            float acc0 = sm.b2[j0], acc1 = sm.b2[j0 + 1];
+#pragma unroll 16
+            for (int k = 0; k < kHid; ++k) {
+                const float a = sm.actA[swz(k, q)];
+                acc0 = mac<EXACT>(acc0, a, sm.w2[k * kOutMax + j0]);
+                acc1 = mac<EXACT>(acc1, a, sm.w2[k * kOutMax + j0 + 1]);
+            }
+            if (sigmoid) {
+                acc0 = (float)(1.0 / (1.0 + exp(-(double)acc0)));
+                acc1 = (float)(1.0 / (1.0 + exp(-(double)acc1)));
+            }
+            sm.outs[q * kOutMax + j0] = acc0;
+            sm.outs[q * kOutMax + j0 + 1] = acc1;
+        }
+        __syncthreads();
+        float *dst = out + p0 * out_dim;
+        for (int i = tid; i < nvalid * out_dim; i += 256) {
+            const int q = i / out_dim, j = i - q * out_dim;
+            dst[i] = sm.outs[q * kOutMax + j];
+        }
+    }
+}
+
+static bool decode_fast_ok(const pg_grid *g, const pg_mlp *m) {
+    return g->feature_dim == 2 && g->n_levels == 16 && m->n_layers == 3 && m->widths[0] == kIn &&
+           m->widths[1] == kHid && m->widths[2] == kHid && m->widths[3] >= 1 && m->widths[3] <= kOutMax;
+}
+
+static int sm_count() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+template <typename FT, int D, bool EXACT>
+static void launch_decode(const pg_grid *g, const float *xs, int64_t B, const void *feats,
+                          const uint8_t *baked, const float *params, int out_dim, int sig,
+                          float *out, int32_t *bad, cudaStream_t s) {
+    static bool configured = false;
+    const int smem = (int)sizeof(DecodeSmem);
+    if (!configured) {
+        cudaFuncSetAttribute(decode_fused_kernel<FT, D, EXACT>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        configured = true;
+    }
+    const int64_t ntiles = (B + kTP - 1) / kTP;
+    const int64_t cap = (int64_t)sm_count() * 2;
+    const int grd = (int)(ntiles < cap ? ntiles : cap);
+    decode_fused_kernel<FT, D, EXACT><<<grd, 256, smem, s>>>(*g, xs, B, (const FT *)feats, baked,
+                                                            params, out_dim, sig, out, bad);
+}
+
+int decode_device(const pg_grid *g, const pg_mlp *m, const float *xs, int64_t B,
+                  const void *feats, const uint8_t *baked, const float *params, unsigned flags,
+                  float *ws, float *out, int32_t *bad, cudaStream_t s) {
+    if (int e = validate_grid(g)) return e;
+    if (int e = validate_mlp(m)) return e;
+    PG_REQUIRE(m->widths[0] == g->n_levels * g->feature_dim, "MLP input width != L*F");
+    if (B == 0) return PG_OK;
+    const bool half = (flags & PG_HALF_FEATS) != 0;
+    const bool exact = (flags & PG_EXACT_MLP) != 0;
+    const int sig = (flags & PG_SIGMOID) ? 1 : 0;
+    if (decode_fast_ok(g, m)) {
+        const int od = m->widths[3];
+#define PG_DEC(FT_, D_)                                                                       \
+    (exact ? launch_decode<FT_, D_, true>(g, xs, B, feats, baked, params, od, sig, out, bad, s) \
+           : launch_decode<FT_, D_, false>(g, xs, B, feats, baked, params, od, sig, out, bad, s))
+        if (half) {
+            if (g->d == 2) PG_DEC(__half, 2); else PG_DEC(__half, 3);
+        } else {
+            if (g->d == 2) PG_DEC(float, 2); else PG_DEC(float, 3);
+        }
+#undef PG_DEC
+        return check_launch("decode_fused");
+    }
+    // generic shapes: fused encode, then row-wise MLP
+    PG_REQUIRE(ws != nullptr, "generic decode needs workspace");
+    float *y = ws;
+    if (int e = pg_encode_fwd_f32(g, xs, B, feats, baked, nullptr, flags & PG_HALF_FEATS, y, bad, s)) return e;
+    return mlp_infer_rows_generic<float>(y, B, m, params, flags, ws + B * g->n_levels * g->feature_dim,
+                                         out, s);
+}
+
+// =========================================================================
+// Generic training pass (any widths, float or double).  ws layout:
+//   z_l (pre-activations) for every layer: B * sum(widths[1:])
+//   two delta buffers:                     2 * B * max(widths)
+// =========================================================================
+template <typename T>
+__global__ void train_linear_fwd_kernel(const T *__restrict__ a, int relu_in, int64_t B, int fin,
+                                        const T *__restrict__ W, const T *__restrict__ bias,
+                                        int fout, T *__restrict__ z) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B * fout) return;
+    const int64_t b = i / fout;
+    const int j = (int)(i - b * fout);
+    T acc = bias[j];
+    for (int k = 0; k < fin; ++k) {
+        T v = a[b * fin + k];
+        if (relu_in && v < T(0)) v = T(0);
+        acc = Ar<T>::fma(v, W[(int64_t)k * fout + j], acc);
+    }
+    z[i] = acc;
+}
+
+template <typename T>
+__global__ void train_loss_kernel(const T *__restrict__ zout, const T *__restrict__ targets,
+                                  int64_t n, T scale, int sigmoid, T *__restrict__ delta,
+                                  double *__restrict__ loss_sum) {
+    __shared__ double red[32];
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double sq = 0.0;
+    if (i < n) {
+        const T o = zout[i];
+        const T pred = sigmoid ? T(1) / (T(1) + Ar<T>::exp(-o)) : o;
+        const T diff = pred - targets[i];
+        sq = (double)diff * (double)diff;
+        T dp = Ar<T>::mul(diff, scale);
+        if (sigmoid) dp = dp * (pred * (T(1) - pred));
+        delta[i] = dp;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0 && loss_sum) atomicAdd(loss_sum, v);
+    }
+}
+
+// dW[k][j] += sum_b a[b][k] * delta[b][j] (k == fin -> bias row), rows split
+// over blockIdx.y in chunks, partial sums added atomically.
+template <typename T>
+__global__ void train_wgrad_kernel(const T *__restrict__ a, int relu_in, int64_t B, int fin,
+                                   const T *__restrict__ delta, int fout, T *__restrict__ gW,
+                                   T *__restrict__ gb, int64_t rows_per_chunk) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)(fin + 1) * fout) return;
+    const int k = (int)(i / fout), j = (int)(i % fout);
+    const int64_t b0 = (int64_t)blockIdx.y * rows_per_chunk;
+    const int64_t b1 = b0 + rows_per_chunk < B ? b0 + rows_per_chunk : B;
+    T acc = T(0);
+    for (int64_t b = b0; b < b1; ++b) {
+        T v = T(1);
+        if (k < fin) {
+            v = a[b * fin + k];
+            if (relu_in && v < T(0)) v = T(0);
+        }
+        acc = Ar<T>::fma(v, delta[b * fout + j], acc);
+    }
+    if (k < fin) red_add(gW + (int64_t)k * fout + j, acc);
+    else red_add(gb + j, acc);
+}
+
+// out[b][k] = (sum_j delta[b][j] W[k][j]) * (mask ? z[b][k] > 0 : 1)
+template <typename T>
+__global__ void train_dgrad_kernel(const T *__restrict__ delta, int64_t B, int fout,
+                                   const T *__restrict__ W, int fin, const T *__restrict__ zmask,
+                                   T *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B * fin) return;
+    const int64_t b = i / fin;
+    const int k = (int)(i - b * fin);
+    T acc = T(0);
+    for (int j = 0; j < fout; ++j) acc = Ar<T>::fma(delta[b * fout + j], W[(int64_t)k * fout + j], acc);
+    if (zmask && !(zmask[i] > T(0))) acc = T(0);
+    out[i] = acc;
+}
+
+template <typename T>
+int mlp_train_generic(const pg_mlp *m, const T *y, const T *targets, int64_t B, const T *params,
+                      T scale, unsigned flags, T *gparams, T *dy, double *loss_sum, T *ws,
+                      cudaStream_t s) {
+    if (int e = validate_mlp(m)) return e;
+    if (B == 0) return PG_OK;
+    PG_REQUIRE(ws != nullptr, "mlp_train needs workspace");
+    const int nl = m->n_layers;
+    const int maxw = mlp_max_width(m);
+    const T *Wp[PG_MAX_LAYERS], *bp[PG_MAX_LAYERS];
+    T *gWp[PG_MAX_LAYERS], *gbp[PG_MAX_LAYERS], *z[PG_MAX_LAYERS];
+    {
+        int64_t off = 0, zoff = 0;
+        for (int l = 0; l < nl; ++l) {
+            const int fi = m->widths[l], fo = m->widths[l + 1];
+            Wp[l] = params + off;
+            gWp[l] = gparams + off;
+            off += (int64_t)fi * fo;
+            bp[l] = params + off;
+            gbp[l] = gparams + off;
+            off += fo;
+            z[l] = ws + zoff;
+            zoff += B * fo;
+        }
+        T *d0 = ws + zoff;
+        T *d1 = d0 + B * maxw;
+        // forward
+        for (int l = 0; l < nl; ++l) {
+            const int fi = m->widths[l], fo = m->widths[l + 1];
+            const T *a = l == 0 ? y : z[l - 1];
+            train_linear_fwd_kernel<T><<<grid_for(B * fo, 256), 256, 0, s>>>(a, l > 0, B, fi, Wp[l], bp[l], fo, z[l]);
+        }
+        const int od = m->widths[nl];
+        train_loss_kernel<T><<<grid_for(B * od, 256), 256, 0, s>>>(z[nl - 1], targets, B * od, scale,
+                                                                  (flags & PG_SIGMOID) ? 1 : 0, d0, loss_sum);
+        // backward
+        T *dcur = d0, *dnext = d1;
+        for (int l = nl - 1; l >= 0; --l) {
+            const int fi = m->widths[l], fo = m->widths[l + 1];
+            const T *a = l == 0 ? y : z[l - 1];
+            const int64_t chunk = 4096;
+            dim3 gg(grid_for((int64_t)(fi + 1) * fo, 128), (unsigned)((B + chunk - 1) / chunk));
+            train_wgrad_kernel<T><<<gg, 128, 0, s>>>(a, l > 0, B, fi, dcur, fo, gWp[l], gbp[l], chunk);
+            T *dst = l > 0 ? dnext : dy;
+            train_dgrad_kernel<T><<<grid_for(B * fi, 256), 256, 0, s>>>(dcur, B, fo, Wp[l], fi,
+                                                                       l > 0 ? z[l - 1] : nullptr, dst);
+            T *tmp = dcur;
+            dcur = dnext;
+            dnext = tmp;
+        }
+    }
+    return check_launch("mlp_train");
+}
+
+template int mlp_train_generic<float>(const pg_mlp *, const float *, const float *, int64_t,
+                                      const float *, float, unsigned, float *, float *, double *,
+                                      float *, cudaStream_t);
+template int mlp_train_generic<double>(const pg_mlp *, const double *, const double *, int64_t,
+                                       const double *, double, unsigned, double *, double *,
+                                       double *, double *, cudaStream_t);
+
+int64_t mlp_train_ws(int64_t B, const pg_mlp *m) {
+    int64_t zsum = 0;
+    for (int l = 0; l < m->n_layers; ++l) zsum += m->widths[l + 1];
+    return B * zsum + 2 * B * mlp_max_width(m);
+}
+int64_t mlp_params(const pg_mlp *m) { return mlp_param_count(m); }
+
+}  // namespace pg
+
+using namespace pg;
+
+extern "C" {
+
+int pg_mlp_infer_rows_f32(const float *xs, int64_t B, const pg_mlp *mlp, const float *params,
+                          unsigned flags, float *act_ws, float *out, void *stream) {
+    return mlp_infer_rows_generic<float>(xs, B, mlp, params, flags, act_ws, out, as_stream(stream));
+}
+int pg_mlp_infer_rows_f64(const double *xs, int64_t B, const pg_mlp *mlp, const double *params,
+                          unsigned flags, double *act_ws, double *out, void *stream) {
+    return mlp_infer_rows_generic<double>(xs, B, mlp, params, flags, act_ws, out, as_stream(stream));
+}
+
+int pg_decode_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs, int64_t B,
+                  const void *feats, const uint8_t *baked, const float *params, unsigned flags,
+                  float *ws, float *out, void *stream) {
+    return decode_device(grid, mlp, xs, B, feats, baked, params, flags, ws, out, nullptr,
+                         as_stream(stream));
+}
+
+int pg_decode_host_f32(const pg_grid *grid, const pg_mlp *mlp, const float *h_xs, int64_t B,
+                       const void *feats, const uint8_t *baked, const float *params,
+                       unsigned flags, int64_t chunk, float *d_xs, float *d_out, float *h_out,
+                       void *stream0, void *stream1) {
+    if (int e = validate_grid(grid)) return e;
+    if (int e = validate_mlp(mlp)) return e;
+    PG_REQUIRE(decode_fast_ok(grid, mlp), "host decode needs the fused [32,64,64,<=4] shape");
+    PG_REQUIRE(chunk >= 1, "chunk must be positive");
+    const int d = grid->d, od = mlp->widths[mlp->n_layers];
+    cudaStream_t st[2] = {as_stream(stream0), as_stream(stream1)};
+    int64_t c = 0;
+    for (int64_t off = 0; off < B; off += chunk, ++c) {
+        const int64_t n = (B - off) < chunk ? (B - off) : chunk;
+        const int slot = (int)(c & 1);
+        cudaStream_t s = st[slot];
+        float *dx = d_xs + (int64_t)slot * chunk * d;
+        float *dout = d_out + (int64_t)slot * chunk * od;
+        cudaMemcpyAsync(dx, h_xs + off * d, sizeof(float) * n * d, cudaMemcpyHostToDevice, s);
+        if (int e = decode_device(grid, mlp, dx, n, feats, baked, params, flags, nullptr, dout, nullptr, s))
+            return e;
+        cudaMemcpyAsync(h_out + off * od, dout, sizeof(float) * n * od, cudaMemcpyDeviceToHost, s);
+    }
+    cudaStreamSynchronize(st[0]);
+    cudaStreamSynchronize(st[1]);
+    return check_launch("decode_host");
+}
+
+int64_t pg_mlp_train_workspace_floats(int64_t B, const pg_mlp *mlp) { return mlp_train_ws(B, mlp); }
+
+int pg_mlp_train_f32(const pg_mlp *mlp, const float *y, const float *targets, int64_t B,
+                     const float *params, float scale, unsigned flags, float *gparams, float *dy,
+                     double *loss_sum, float *ws, void *stream) {
+    return mlp_train_generic<float>(mlp, y, targets, B, params, scale, flags, gparams, dy, loss_sum,
+                                    ws, as_stream(stream));
+}
+int pg_mlp_train_f64(const pg_mlp *mlp, const double *y, const double *targets, int64_t B,
+                     const double *params, double scale, unsigned flags, double *gparams,
+                     double *dy, double *loss_sum, double *ws, void *stream) {
+    return mlp_train_generic<double>(mlp, y, targets, B, params, scale, flags, gparams, dy,
+                                     loss_sum, ws, as_stream(stream));
+}
+
+}  // extern "C"

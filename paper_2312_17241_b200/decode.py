@@ -1,0 +1,193 @@
+"""Random-access decode on the GPU (model_io.py:92-147, 280-349 of the reference).
+
+``to_inference`` performs the reference's fp16 downcast of features and MLP
+(model_io.py:130-147).  The device keeps the feature tables IN binary16 (half
+the gather bytes of the fp32 twin) and widens them in registers — the widened
+values are exactly the reference twin's fp32 values (model_io.py:114-127).
+``decode_pixels`` runs ONE fused kernel per call: all-level encode + MLP per
+128-query tile.  With ``exact=True`` (the default for the reference-facing
+functions) the MLP uses the reference's operation order without FMA, so the
+output equals the reference's ``decode_pixels`` bit for bit; ``exact=False``
+uses FMA (within ~1e-6 relative).  Every output row depends only on its own
+input row either way (model_io.py:294-295), so any batching is bit-identical.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import DomainViolation, UnbakedModel
+from .grid_model import Model
+from .hyper import HyperParams, build_level_specs, grid_struct, mlp_struct
+
+
+@dataclass
+class TouchCounter:
+    """Rows touched by instrumented decode queries (model_io.py:280-289)."""
+
+    feature_rows: int = 0
+    index_rows: int = 0
+
+    @property
+    def total(self) -> int:
+        return self.feature_rows + self.index_rows
+
+
+class InferenceModel:
+    """Half-precision tables + fp16-rounded MLP resident on one GPU."""
+
+    def __init__(self, hyper: HyperParams, width: int, height: int, feats16: torch.Tensor,
+                 baked: torch.Tensor, probed: list, params: torch.Tensor, device=None):
+        self.hyper, self.width, self.height = hyper, width, height
+        self.device = torch.device(device or "cuda")
+        self.specs = build_level_specs(hyper.n_min, hyper.n_max, hyper.n_levels, hyper.n_f, hyper.d)
+        self.probed = list(probed)
+        self.grid = grid_struct(hyper, self.specs, self.probed)
+        self.widths = hyper.mlp_widths()
+        self.mlp_desc = mlp_struct(self.widths)
+        self.feats16 = feats16.to(self.device).contiguous()      # (L, n_f, F) float16
+        self.baked = baked.to(self.device).contiguous()          # (P, n_c) uint8
+        self.params = params.to(self.device).contiguous()        # fp32 of fp16-rounded MLP
+        self.fast = (hyper.feature_dim == 2 and hyper.n_levels == 16 and len(self.widths) == 4
+                     and self.widths[1] == 64 and self.widths[2] == 64 and hyper.out_dim <= 4)
+
+    @property
+    def out_dim(self) -> int:
+        return self.hyper.out_dim
+
+    @classmethod
+    def from_host(cls, hyper, feats16, baked, w16, b16, width=0, height=0, device=None):
+        """Build from the reference's InferenceModel payload (per-level fp16
+        tables, per-level baked entries or None, fp16 weights/biases)."""
+        probed = [i for i, b in enumerate(baked) if b is not None]
+        f = torch.from_numpy(np.stack([np.asarray(x, np.float16) for x in feats16]))
+        bk = torch.from_numpy(np.stack([np.asarray(baked[i], np.uint8) for i in probed])
+                              if probed else np.zeros((0, hyper.n_c), np.uint8))
+        flat = np.concatenate([np.concatenate([np.asarray(w, np.float16).astype(np.float32).ravel(),
+                                               np.asarray(b, np.float16).astype(np.float32).ravel()])
+                               for w, b in zip(w16, b16)])
+        return cls(hyper, width, height, f, bk, probed, torch.from_numpy(flat), device)
+
+
+def to_inference(model: Model, width: int = 0, height: int = 0) -> InferenceModel:
+    """Downcast a trained device model to its storable half-precision form."""
+    if model.probed and model.baked.numel() == 0:
+        raise UnbakedModel("probed levels have no baked indices")
+    feats16 = model.feats.to(torch.float16)                      # RNE, as numpy astype
+    params = model.mlp_params.to(torch.float16).to(torch.float32)
+    return InferenceModel(model.hyper, width, height, feats16, model.baked.clone(), model.probed,
+                          params, model.device)
+
+
+def _flags(inf: InferenceModel, exact: bool) -> int:
+    f = _lib.PG_HALF_FEATS
+    if exact:
+        f |= _lib.PG_EXACT_MLP
+    if inf.hyper.out_sigmoid:
+        f |= _lib.PG_SIGMOID
+    return f
+
+
+def decode_device(inf: InferenceModel, xs: torch.Tensor, out: torch.Tensor = None,
+                  exact: bool = True, stream=None) -> torch.Tensor:
+    """Fused encode + MLP on device-resident queries; returns (B, out_dim)."""
+    B = xs.shape[0]
+    if out is None:
+        out = torch.empty((B, inf.out_dim), dtype=torch.float32, device=inf.device)
+    ws = None
+    if not inf.fast:
+        n = B * inf.hyper.encoded_width + 2 * B * max(inf.widths)
+        ws = torch.empty(max(n, 1), dtype=torch.float32, device=inf.device)
+    _lib.call("pg_decode_f32", inf.grid, inf.mlp_desc, _lib.ptr(xs), B, _lib.ptr(inf.feats16),
+              _lib.ptr(inf.baked), _lib.ptr(inf.params), _flags(inf, exact), _lib.ptr(ws),
+              _lib.ptr(out), _lib.stream_ptr(stream))
+    return out
+
+
+def decode_pixels(inf: InferenceModel, xs, counter: TouchCounter | None = None,
+                  exact: bool = True):
+    """Decode arbitrary coordinates (numpy in -> numpy out, or CUDA tensor in
+    -> CUDA tensor out); model_io.py:292-311."""
+    d = inf.hyper.d
+    as_numpy = not isinstance(xs, torch.Tensor)
+    if as_numpy:
+        a = np.ascontiguousarray(np.asarray(xs, dtype=np.float32))
+        if a.ndim != 2 or a.shape[1] != d:
+            raise DomainViolation(f"expected (batch, {d}) coordinates, got {a.shape}")
+        if np.any(a < 0.0) or np.any(a > 1.0):
+            raise DomainViolation("coordinates outside the unit hypercube")
+        t = torch.from_numpy(a).to(inf.device)
+    else:
+        t = xs.to(device=inf.device, dtype=torch.float32).contiguous()
+    if counter is not None:
+        per = t.shape[0] * (1 << d)
+        counter.feature_rows += per * inf.hyper.n_levels
+        counter.index_rows += per * len(inf.probed)
+    out = decode_device(inf, t, exact=exact)
+    return out.cpu().numpy() if as_numpy else out
+
+
+def decode_at(inf: InferenceModel, x, counter: TouchCounter | None = None) -> np.ndarray:
+    """Random-access decode of one point (model_io.py:314-318)."""
+    return decode_pixels(inf, np.asarray(x, dtype=np.float32).reshape(1, -1), counter)[0]
+
+
+def grid_coords(width: int, height: int, x0: int, y0: int, x1: int, y1: int) -> np.ndarray:
+    """Pixel centres of a half-open rectangle (model_io.py:321-325)."""
+    cols, rows = np.meshgrid(np.arange(x0, x1), np.arange(y0, y1))
+    return np.stack([(cols.ravel() + 0.5) / width, (rows.ravel() + 0.5) / height],
+                    axis=1).astype(np.float32)
+
+
+def decode_rect(inf: InferenceModel, rect, width: int | None = None,
+                height: int | None = None) -> np.ndarray:
+    """Decode the half-open pixel rectangle (x0, y0, x1, y1) (model_io.py:327-339)."""
+    width = width or inf.width
+    height = height or inf.height
+    if width < 1 or height < 1:
+        raise DomainViolation("model stores no image dimensions; pass them")
+    x0, y0, x1, y1 = (int(v) for v in rect)
+    if not (0 <= x0 < x1 <= width and 0 <= y0 < y1 <= height):
+        raise DomainViolation(f"rect {rect} invalid for {width}x{height} image")
+    out = decode_pixels(inf, grid_coords(width, height, x0, y0, x1, y1))
+    return out.reshape(y1 - y0, x1 - x0, inf.out_dim)
+
+
+def decode_image(inf: InferenceModel, width: int | None = None,
+                 height: int | None = None) -> np.ndarray:
+    """Decode the full image (model_io.py:342-349)."""
+    width = width or inf.width
+    height = height or inf.height
+    if width < 1 or height < 1:
+        raise DomainViolation("model stores no image dimensions; pass them")
+    return decode_rect(inf, (0, 0, width, height), width, height)
+
+
+class HostDecoder:
+    """End-to-end decode from pinned host memory through the C ABI's
+    pg_decode_host_f32: H2D copy, fused kernel and D2H copy of successive
+    chunks alternate between two streams so transfers overlap compute."""
+
+    def __init__(self, inf: InferenceModel, chunk: int = 1 << 21, exact: bool = False):
+        if not inf.fast:
+            raise ValueError("host decode needs the fused [32,64,64,<=4] shape")
+        self.inf, self.chunk, self.exact = inf, chunk, exact
+        d, od = inf.hyper.d, inf.out_dim
+        self.d_xs = torch.empty(2 * chunk * d, dtype=torch.float32, device=inf.device)
+        self.d_out = torch.empty(2 * chunk * od, dtype=torch.float32, device=inf.device)
+        self.s0 = torch.cuda.Stream(device=inf.device)
+        self.s1 = torch.cuda.Stream(device=inf.device)
+
+    def __call__(self, h_xs: torch.Tensor, h_out: torch.Tensor) -> torch.Tensor:
+        inf = self.inf
+        assert h_xs.is_pinned() and h_out.is_pinned(), "host buffers must be pinned"
+        _lib.call("pg_decode_host_f32", inf.grid, inf.mlp_desc, _lib.ptr(h_xs), h_xs.shape[0],
+                  _lib.ptr(inf.feats16), _lib.ptr(inf.baked), _lib.ptr(inf.params),
+                  _flags(inf, self.exact), self.chunk, _lib.ptr(self.d_xs), _lib.ptr(self.d_out),
+                  _lib.ptr(h_out), _lib.ctypes.c_void_p(self.s0.cuda_stream),
+                  _lib.ctypes.c_void_p(self.s1.cuda_stream))
+        return h_out

@@ -1,0 +1,251 @@
+"""Device-resident training step (trainer.py:34-242 of the reference).
+
+One ``TrainState.step()`` on the GPU:
+
+    pixel batch -> fused encode fwd (all levels) -> MLP fwd + squared error
+    + MLP bwd -> fused encode bwd (straight-through scatter, touched rows)
+    -> dense Adam over [features | MLP] (one launch) -> lazy Adam + re-bake
+    over touched confidence rows (one launch)
+
+Batches come from the reference's own seeded stream on the host
+(``sampler="reference"``: identical pixels, hence comparable loss curves) or
+from a counter-based generator on the device (``sampler="device"``: no host
+work in the step).  The loss is the fp64 mean of squared errors
+(trainer.py:129-132); a non-finite loss leaves parameters untouched and raises
+TrainingDiverged, as the reference does.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .encoding import encode_backward_device, encode_forward_device
+from .errors import InvalidHyperparameter, TrainingDiverged
+from .grid_model import Model, init_model
+from .hyper import SEED_BATCH, HyperParams, seeded_rng
+
+
+@dataclass
+class TrainConfig:
+    steps: int = 10_000
+    batch_size: int = 8192
+    lr: float = 1e-2
+    beta1: float = 0.9
+    beta2: float = 0.99
+    eps: float = 1e-15
+    seed: int = 0
+    precision: str = "f32"      # "f32" | "f64"
+    metrics_path: str | None = None
+    debug_check_every: int = 0  # assert incremental bake == full bake every N steps
+
+    def validate(self) -> "TrainConfig":
+        if self.batch_size < 1:
+            raise InvalidHyperparameter("batch size must be at least 1")
+        if self.lr < 0:
+            raise InvalidHyperparameter("learning rate must be non-negative")
+        if self.steps < 0:
+            raise InvalidHyperparameter("step count must be non-negative")
+        if self.precision not in ("f32", "f64"):
+            raise InvalidHyperparameter(f"unknown precision {self.precision!r}")
+        return self
+
+    @property
+    def dtype(self):
+        return np.float64 if self.precision == "f64" else np.float32
+
+
+@dataclass
+class AdamSlot:
+    m: torch.Tensor
+    v: torch.Tensor
+
+    @classmethod
+    def like(cls, t: torch.Tensor) -> "AdamSlot":
+        return cls(torch.zeros_like(t), torch.zeros_like(t))
+
+
+def _sfx(t: torch.Tensor) -> str:
+    return "f64" if t.dtype == torch.float64 else "f32"
+
+
+def adam_update(param: torch.Tensor, grad: torch.Tensor, slot: AdamSlot, t: int, lr: float,
+                betas=(0.9, 0.99), eps: float = 1e-15) -> None:
+    """Standard Adam with bias correction, in place, the reference's rounding
+    order (trainer.py:73-84).  ``grad`` is left unchanged."""
+    g = grad.detach().clone().contiguous()
+    _lib.call(f"pg_adam_{_sfx(param)}", _lib.ptr(param), _lib.ptr(g), _lib.ptr(slot.m),
+              _lib.ptr(slot.v), param.numel(), int(t), float(lr), float(betas[0]), float(betas[1]),
+              float(eps), None, _lib.stream_ptr())
+
+
+class TrainState:
+    """Optimizer state bound to one device model; drives individual steps."""
+
+    def __init__(self, model: Model, image, cfg: TrainConfig, sampler: str = "reference"):
+        cfg.validate()
+        if sampler not in ("reference", "device"):
+            raise InvalidHyperparameter(f"unknown sampler {sampler!r}")
+        img = image if isinstance(image, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(image, dtype=model.dtype))
+        if img.ndim != 3 or img.shape[2] != model.hyper.out_dim:
+            raise InvalidHyperparameter(
+                f"image shape {tuple(img.shape)} does not match output dim {model.hyper.out_dim}")
+        if model.hyper.d != 2:
+            raise InvalidHyperparameter("the image trainer is 2-D (trainer.py:109-116)")
+        self.model, self.cfg, self.sampler = model, cfg, sampler
+        self.image = img.to(device=model.device, dtype=model.tdtype).contiguous()
+        self.height, self.width = int(img.shape[0]), int(img.shape[1])
+        self.rng = seeded_rng(cfg.seed, SEED_BATCH)
+        self.t = 0
+        dev, tdt = model.device, model.tdtype
+        self.dm = torch.zeros_like(model.dense)
+        self.dv = torch.zeros_like(model.dense)
+        self.cm = torch.zeros_like(model.conf)
+        self.cv = torch.zeros_like(model.conf)
+        B, h = cfg.batch_size, model.hyper
+        self.pix_host = torch.empty(B, dtype=torch.int64, pin_memory=True)
+        self.pix_copied = torch.cuda.Event()
+        self.pix = torch.empty(B, dtype=torch.int64, device=dev)
+        self.xs = torch.empty((B, 2), dtype=tdt, device=dev)
+        self.targets = torch.empty((B, h.out_dim), dtype=tdt, device=dev)
+        self.y = torch.empty((B, h.encoded_width), dtype=tdt, device=dev)
+        self.dy = torch.empty_like(self.y)
+        nws = int(_lib.lib().pg_mlp_train_workspace_floats(B, model.mlp_desc))
+        self.ws = torch.empty(max(nws, 1), dtype=tdt, device=dev)
+        self.loss_sum = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.loss_host = torch.zeros(1, dtype=torch.float64, pin_memory=True)
+        self.scale = 2.0 / (B * h.out_dim)   # trainer.py:134, cast to the model dtype
+
+    # ---------------------------------------------------------------- batch
+    def sample_batch(self):
+        """Draw the next batch; returns device (xs, targets)."""
+        m, B, s = self.model, self.cfg.batch_size, _lib.stream_ptr()
+        sfx = "f64" if m.tdtype == torch.float64 else "f32"
+        if self.sampler == "reference":
+            pix = self.rng.integers(0, self.width * self.height, size=B)   # trainer.py:110-111
+            self.pix_copied.synchronize()   # previous upload of pix_host has landed
+            self.pix_host.numpy()[:] = pix
+            self.pix.copy_(self.pix_host, non_blocking=True)
+            self.pix_copied.record()
+            _lib.call(f"pg_pixel_batch_{sfx}", _lib.ptr(self.pix), B, self.width, self.height,
+                      _lib.ptr(self.image), m.hyper.out_dim, 0, 0, None, _lib.ptr(self.xs),
+                      _lib.ptr(self.targets), s)
+        else:
+            _lib.call(f"pg_pixel_batch_{sfx}", None, B, self.width, self.height,
+                      _lib.ptr(self.image), m.hyper.out_dim, int(self.cfg.seed),
+                      int(self.t), _lib.ptr(self.pix), _lib.ptr(self.xs), _lib.ptr(self.targets), s)
+        return self.xs, self.targets
+
+    # ----------------------------------------------------------------- step
+    def launch_step(self) -> None:
+        """Enqueue one full step on the current stream (no host sync)."""
+        m, cfg = self.model, self.cfg
+        s = _lib.stream_ptr()
+        sfx = "f64" if m.tdtype == torch.float64 else "f32"
+        xs, targets = self.sample_batch()
+        encode_forward_device(m, xs, self.y)
+        self.loss_sum.zero_()
+        flags = _lib.PG_SIGMOID if m.hyper.out_sigmoid else 0
+        _lib.call(f"pg_mlp_train_{sfx}", m.mlp_desc, _lib.ptr(self.y), _lib.ptr(targets),
+                  cfg.batch_size, _lib.ptr(m.mlp_params), float(np.dtype(m.dtype).type(self.scale)),
+                  flags, _lib.ptr(m.gmlp), _lib.ptr(self.dy), _lib.ptr(self.loss_sum),
+                  _lib.ptr(self.ws), s)
+        encode_backward_device(m, xs, self.dy)
+        self.t += 1
+        self.apply_updates()
+
+    def apply_updates(self) -> None:
+        """Dense Adam over [features | MLP] and lazy Adam + re-bake over the
+        touched confidence rows; both skip the update if the loss diverged."""
+        m, cfg, s = self.model, self.cfg, _lib.stream_ptr()
+        sfx = "f64" if m.tdtype == torch.float64 else "f32"
+        _lib.call(f"pg_adam_{sfx}", _lib.ptr(m.dense), _lib.ptr(m.gdense), _lib.ptr(self.dm),
+                  _lib.ptr(self.dv), m.n_dense, self.t, cfg.lr, cfg.beta1, cfg.beta2, cfg.eps,
+                  _lib.ptr(self.loss_sum), s)
+        if m.probed:
+            _lib.call(f"pg_lazy_adam_rebake_{sfx}", _lib.ptr(m.conf), _lib.ptr(self.cm),
+                      _lib.ptr(self.cv), _lib.ptr(m.baked), _lib.ptr(m.gconf), _lib.ptr(m.touched),
+                      m.n_rows, m.hyper.n_p, self.t, cfg.lr, cfg.beta1, cfg.beta2, cfg.eps,
+                      _lib.ptr(self.loss_sum), s)
+
+    def loss_value(self) -> float:
+        self.loss_host.copy_(self.loss_sum, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return float(self.loss_host[0]) / (self.cfg.batch_size * self.model.hyper.out_dim)
+
+    def step(self) -> float:
+        self.launch_step()
+        loss = self.loss_value()
+        if not math.isfinite(loss):
+            self.t -= 1   # the reference raises before counting the step
+            raise TrainingDiverged(f"non-finite loss at step {self.t}")
+        if self.cfg.debug_check_every and self.t % self.cfg.debug_check_every == 0:
+            self.check_bake_consistency()
+        return loss
+
+    def check_bake_consistency(self) -> None:
+        m = self.model
+        if m.probed:
+            full = torch.argmax(m.conf, dim=-1).to(torch.uint8)
+            bad = (full != m.baked).any(dim=-1).nonzero()
+            if bad.numel():
+                raise TrainingDiverged(
+                    f"incremental bake diverged on level {m.probed[int(bad[0])]}")
+
+
+@dataclass
+class FitResult:
+    model: Model
+    inference: object
+    final_psnr: float
+    final_loss: float
+    steps: int
+    wall_time_s: float
+    ms_per_step: float
+    losses: list = field(default_factory=list, repr=False)
+
+
+def psnr(reference, test) -> float:
+    """20*log10(1/RMSE) over [0,1] values in fp64 (metrics.py:12-26)."""
+    a = np.asarray(reference, dtype=np.float64)
+    b = np.asarray(test, dtype=np.float64)
+    mse = float(np.mean((a - b) ** 2))
+    return float("inf") if mse == 0.0 else -10.0 * math.log10(mse)
+
+
+def fit(image, hyper: HyperParams, cfg: TrainConfig, force_probed: bool = False,
+        sampler: str = "reference") -> FitResult:
+    """Fit one image on the GPU (trainer.py:196-242)."""
+    from .decode import decode_image, to_inference
+    model = init_model(hyper, cfg.seed, cfg.dtype, force_probed=force_probed)
+    state = TrainState(model, image, cfg, sampler=sampler)
+    sink = open(cfg.metrics_path, "w") if cfg.metrics_path else None
+    losses, step_ms = [], []
+    t_start = time.perf_counter()
+    try:
+        for step in range(cfg.steps):
+            t0 = time.perf_counter()
+            loss = state.step()
+            ms = (time.perf_counter() - t0) * 1e3
+            losses.append(loss)
+            step_ms.append(ms)
+            if sink is not None:
+                bp = -10.0 * math.log10(loss) if loss > 0 else float("inf")
+                sink.write(json.dumps({"step": step, "loss": loss, "psnr": bp, "ms": ms}) + "\n")
+    finally:
+        if sink is not None:
+            sink.close()
+    wall = time.perf_counter() - t_start
+    inf = to_inference(model, width=state.width, height=state.height)
+    decoded = decode_image(inf)
+    img = image.cpu().numpy() if isinstance(image, torch.Tensor) else np.asarray(image)
+    final = psnr(img, np.clip(decoded, 0.0, 1.0))
+    return FitResult(model, inf, final, losses[-1] if losses else float("nan"), cfg.steps, wall,
+                     float(np.median(step_ms)) if step_ms else 0.0, losses)
