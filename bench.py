@@ -1,0 +1,436 @@
+#!/usr/bin/env python3
+"""Benchmark of the learned-hash-probing hot path on B200 (BASELINE.json metric:
+"encoded+MLP queries/sec and train samples/sec per GPU, % roofline").
+
+Headline (``value``): encoded+MLP inference queries/s, whole job, on the
+configs[1] workload (C2: 2-D gigapixel-style inference, 2^24 queries per GPU
+per step, log2 n_f = 16, n_c = 2^16, N_p = 4, n_max = 8192, 16 levels, F = 2,
+MLP [32, 64, 64, 3], fp16-stored tables).  A "step" = one fused decode of the
+batch; inputs are resident in HBM and larger than L2 (128 MiB of
+coordinates), tables stay L2-resident as in serving.  ``e2e`` = the same
+metric through the C ABI's host-buffer decode (pinned host coordinates in,
+pinned host outputs back, copies inside the timed region).  ``train`` = C1
+training samples/s (256x256 image, n_f = 2^12, n_c = 2^14, N_p = 4, 2^18
+samples per GPU per step, full step incl. both optimizers).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+N > 1 runs under torchrun, one rank per GPU: queries shard across ranks with
+no data-path collective (weak scaling); the training leg is data parallel
+with one NCCL all-reduce per step.  Timing: CUDA events on the launching
+stream, barrier + synchronize around the timed region, max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "encoded+MLP queries/sec and train samples/sec per GPU (1/2/4/8 B200), % roofline"
+C2 = dict(n_f=2**16, n_c=2**16, n_p=4, n_max=8192)
+C1 = dict(n_f=2**12, n_c=2**14, n_p=4)
+B_INFER = 1 << 24
+B_TRAIN = 1 << 18
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p.get("bf16_tflops", 1590.0)), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """SM clock + clock-event (throttle) reasons sampled every 20 ms through
+    NVML (the library nvidia-smi reads) while the timed region runs."""
+
+    def __init__(self, index):
+        self.index, self.sm, self.mask, self.max_mhz = index, [], 0, None
+        self._stop = threading.Event()
+        self.err = None
+
+    def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.index]) if vis else self.index
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.nv = pynvml
+        except Exception as e:  # pragma: no cover
+            self.err = f"nvml unavailable: {e}"
+            return
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
+
+    def _run(self):
+        nv = self.nv
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            try:
+                self.sm.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.mask |= int(get_reasons(self.h))
+            except Exception as e:  # pragma: no cover
+                self.err = str(e)
+            time.sleep(0.02)
+
+    def stop(self):
+        if self.err and not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [self.err]}
+        self._stop.set()
+        self.thread.join(timeout=2)
+        nv = self.nv
+        bits = {nv.nvmlClocksEventReasonSwPowerCap: "sw_power_cap",
+                nv.nvmlClocksEventReasonHwSlowdown: "hw_slowdown",
+                nv.nvmlClocksEventReasonSwThermalSlowdown: "sw_thermal_slowdown",
+                nv.nvmlClocksEventReasonHwThermalSlowdown: "hw_thermal_slowdown",
+                nv.nvmlClocksEventReasonHwPowerBrakeSlowdown: "hw_power_brake_slowdown"}
+        reasons = sorted(n for bit, n in bits.items() if self.mask & bit)
+        return {"sm_mhz": float(np.median(self.sm)) if self.sm else None,
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.sm)}
+
+
+# ------------------------------------------------------------------ models
+def inference_model(pg, hyper, seed=0):
+    """conf ~ N(0,1) then full bake (uniform probes), features
+    ~ 0.1 N(0,1), MLP from the reference init; fp16 downcast as to_inference."""
+    import torch
+    m = pg.init_model(hyper, seed=seed)
+    rng = np.random.default_rng(seed)
+    with torch.no_grad():
+        m.feats.copy_(torch.from_numpy((rng.standard_normal(tuple(m.feats.shape)) * 0.1).astype(np.float32)))
+        if m.probed:
+            m.conf.copy_(torch.from_numpy(rng.standard_normal(tuple(m.conf.shape)).astype(np.float32)))
+            m.rebake_all()
+    return m, pg.to_inference(m)
+
+
+def infer_bytes_per_query(hyper, n_probed, table_bytes_per_row):
+    """Algorithmic bytes per query: coordinates in, 2^d feature
+    rows per level, one baked byte per corner of each probed level, outputs."""
+    C = 1 << hyper.d
+    return (4 * hyper.d + hyper.n_levels * C * table_bytes_per_row + n_probed * C
+            + 4 * hyper.out_dim)
+
+
+def train_bytes_per_sample(hyper, n_probed):
+    """encode fwd + recompute-bwd bytes per training sample."""
+    C, L, F, d, n_p = 1 << hyper.d, hyper.n_levels, hyper.feature_dim, hyper.d, hyper.n_p
+    fwd = 4 * d + L * C * 4 * F + n_probed * C
+    bwd = (4 * L * F + 4 * d + n_probed * C * (4 * n_p + 4 * F * n_p + 8 * F * n_p + 8 * n_p)
+           + (L - n_probed) * C * 8 * F)
+    return fwd + bwd
+
+
+# ------------------------------------------------------------------ probes
+def measure_l2(lib_call, torch, table_mib=8):
+    """MEASURED L2 denominators: float4 streaming read over an L2-resident
+    buffer and random 8-byte gathers from a table of the config's size."""
+    from paper_2312_17241_b200 import _lib
+    buf = torch.ones(table_mib * (1 << 20) // 4, dtype=torch.float32, device="cuda")
+    sink = torch.zeros(1, device="cuda")
+    reps = 50
+    for _ in range(3):
+        _lib.call("pg_probe_stream_read", _lib.ptr(buf), buf.numel() * 4, 2, _lib.ptr(sink), _lib.stream_ptr())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    _lib.call("pg_probe_stream_read", _lib.ptr(buf), buf.numel() * 4, reps, _lib.ptr(sink), _lib.stream_ptr())
+    e1.record()
+    torch.cuda.synchronize()
+    stream_gbs = buf.numel() * 4 * reps / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    entries = (table_mib * (1 << 20)) // 8
+    nq = 1 << 26
+    _lib.call("pg_probe_gather", _lib.ptr(buf), entries, nq, 7, _lib.ptr(sink), _lib.stream_ptr())
+    e0.record()
+    _lib.call("pg_probe_gather", _lib.ptr(buf), entries, nq, 9, _lib.ptr(sink), _lib.stream_ptr())
+    e1.record()
+    torch.cuda.synchronize()
+    gather_gbs = nq * 8 / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    return stream_gbs, gather_gbs
+
+
+# ------------------------------------------------------------------ CPU arm
+def cpu_decode_baseline(hyper, budget_s=12.0, sample=1 << 20, threads=None):
+    """The reference's decode_pixels on the host: the reference's own compiled
+    Cython core (oracle/_ref) when it was built, else the C port, driven by the
+    oracle's restatement of model_io.decode_pixels; chunks of 16384 queries
+    (model_io.py:45) spread over all host threads (the kernels release the
+    GIL).  Bounded: stops after `budget_s` seconds or `sample` queries."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as O
+    ref = O.reference_core_backend()
+    kern, kind = (ref, "reference") if ref is not None else (O.CBackend, "port")
+    oh = O.Hyper(**hyper)
+    om = O.init_model(oh, seed=0)
+    rng = np.random.default_rng(0)
+    for L in om.levels:
+        L.feats[:] = (rng.standard_normal(L.feats.shape) * 0.1).astype(np.float32)
+    for L in om.levels:
+        if L.conf is not None:
+            L.conf[:] = rng.standard_normal(L.conf.shape).astype(np.float32)
+            L.baked[:] = np.argmax(L.conf, axis=1)
+    inf = O.to_inference(om)
+    xs = np.random.default_rng(1234).random((sample, 2), dtype=np.float32)
+    threads = threads or os.cpu_count() or 1
+    chunk = O.DECODE_CHUNK
+    done = 0
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        futs = []
+        for lo in range(0, sample, chunk):
+            futs.append(ex.submit(O.decode_pixels, inf, xs[lo:lo + chunk], kern))
+        for f in futs:
+            f.result()
+            done += chunk
+            if time.perf_counter() - t0 > budget_s:
+                for g in futs:
+                    g.cancel()
+                break
+    el = time.perf_counter() - t0
+    return {"value": done / el, "unit": "queries/s", "cores": threads, "kind": kind,
+            "sample": f"{done} of the same C2 queries (decode_pixels, {chunk}-query chunks, "
+                      f"{threads} threads, {el:.1f} s)"}
+
+
+def cpu_train_baseline(budget_s=8.0):
+    """Reference TrainState.step (C1, B=8192) on the host, median ms -> samples/s."""
+    from oracle import oracle as O
+    from tests.golden_util import smooth_image
+    ref = O.reference_core_backend()
+    kern, kind = (ref, "reference") if ref is not None else (O.CBackend, "port")
+    st = O.TrainState(O.init_model(O.Hyper(**C1), 0), smooth_image(256, 256),
+                      O.TrainCfg(batch_size=8192, seed=0), kern=kern)
+    for _ in range(3):
+        st.step()
+    times = []
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < budget_s and len(times) < 40:
+        a = time.perf_counter()
+        st.step()
+        times.append(time.perf_counter() - a)
+    ms = float(np.median(times)) * 1e3
+    return {"value": 8192 / (ms * 1e-3), "unit": "samples/s", "cores": 1, "kind": kind,
+            "sample": f"{len(times)} TrainState.step at C1 B=8192, median {ms:.2f} ms "
+                      "(encoding kernels single-threaded as shipped; BLAS threads for the MLP)"}
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_gpu(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2312_17241_b200 as pg
+    from paper_2312_17241_b200 import _lib
+    from paper_2312_17241_b200.decode import HostDecoder, decode_device
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    hbm_peak, tensor_peak, peak_src = peaks()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------- inference (headline) ----------------
+    hyper = pg.HyperParams(**C2)
+    _, inf = inference_model(pg, hyper, seed=0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    xs = torch.rand((B_INFER, 2), generator=g, device=dev)
+    out = torch.empty((B_INFER, hyper.out_dim), device=dev)
+    exact = args.exact
+    for _ in range(args.warmup):
+        decode_device(inf, xs, out, exact=exact)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        decode_device(inf, xs, out, exact=exact)
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    ms_total = max_over_ranks(e0.elapsed_time(e1))
+    clk = clocks.stop()
+    ms_step = ms_total / args.steps
+    qps = world * B_INFER / (ms_step * 1e-3)
+    n_probed = len(inf.probed)
+    bpq = infer_bytes_per_query(hyper, n_probed, table_bytes_per_row=2 * hyper.feature_dim)
+    achieved = B_INFER * bpq / (ms_step * 1e-3) / 1e9    # per GPU, per launch
+    l2_stream, l2_gather = measure_l2(None, torch, table_mib=8)
+    mlp_flops = 2 * sum(a * b for a, b in zip(inf.widths[:-1], inf.widths[1:]))
+
+    # ---------------- e2e through the C ABI host-buffer decode ----------------
+    hx = xs.cpu().pin_memory()
+    ho = torch.empty((B_INFER, hyper.out_dim)).pin_memory()
+    hd = HostDecoder(inf, chunk=1 << 21, exact=exact)
+    torch.cuda.synchronize()
+    for _ in range(max(1, args.warmup // 2)):
+        hd(hx, ho)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        hd(hx, ho)
+    el = max_over_ranks(time.perf_counter() - t0)
+    e2e_qps = world * B_INFER * args.steps / el
+    e2e_launches = args.steps * math.ceil(B_INFER / hd.chunk)
+
+    # ---------------- training (C1, data parallel) ----------------
+    train = run_train(args, pg, torch, dist, rank, world, dev, barrier, max_over_ranks)
+
+    line = {
+        "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 (fp16-stored tables, fp32 math)", "data": "synthetic",
+        "config": {"workload": "C2 inference: 2-D probed hash grid decode, fused encode+MLP",
+                   "queries_per_gpu_per_step": B_INFER, "log2_n_f": 16, "n_c": 2**16, "n_p": 4,
+                   "n_levels": 16, "feature_dim": 2, "n_min": 16, "n_max": 8192,
+                   "mlp": inf.widths, "probed_levels": n_probed,
+                   "mlp_mode": "exact (reference order, bit-identical)" if exact else "fma",
+                   "parallelism": f"query-sharded x{world}",
+                   "l2_policy": "inputs (128 MiB coords + 192 MiB outputs per GPU) larger than L2; tables L2-resident"},
+        "e2e": {"value": e2e_qps, "unit": "queries/s", "h2d_bytes_per_step": B_INFER * 2 * 4,
+                "d2h_bytes_per_step": B_INFER * hyper.out_dim * 4,
+                "path": "pg_decode_host_f32 (pinned host in/out, 2 streams, 2^21-query chunks)"},
+        "gpu_launches": args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None,
+                     "kernel": "decode_fused_kernel", "bytes_per_query": bpq,
+                     "peak_source": peak_src,
+                     "l2_stream_read_gbs": l2_stream, "l2_random_gather_8B_gbs": l2_gather,
+                     "frac_of_l2_stream": achieved / l2_stream,
+                     "mlp_tflops": qps / world * mlp_flops / 1e12,
+                     "note": "table gathers are L2-resident: bytes are algorithmic gather bytes; "
+                             "HBM streams only 20 B/query (coords + outputs)"},
+        "clocks": clk,
+        "train": train,
+    }
+    return line, e2e_launches
+
+
+def run_train(args, pg, torch, dist, rank, world, dev, barrier, max_over_ranks):
+    from tests.golden_util import smooth_image
+    hyper = pg.HyperParams(**C1)
+    model = pg.init_model(hyper, seed=0)
+    img = smooth_image(256, 256)
+    st = pg.TrainState(model, img, pg.TrainConfig(batch_size=B_TRAIN, seed=rank), sampler="device")
+    dp = None
+    if world > 1:
+        from paper_2312_17241_b200.dist import DataParallel
+        dp = DataParallel(st, dist)
+    step = dp.launch_step if dp else st.launch_step
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    loss = st.loss_value()
+    sps = world * B_TRAIN / (ms * 1e-3)
+    n_probed = len(model.probed)
+    bps = train_bytes_per_sample(hyper, n_probed)
+    return {"metric": "train samples/s", "value": sps, "unit": "samples/s", "ms_per_step": ms,
+            "config": {"workload": "C1 image fit step (fwd+bwd+dense Adam+lazy Adam/rebake)",
+                       "samples_per_gpu_per_step": B_TRAIN, "image": "256x256 synthetic smooth",
+                       "n_f": 2**12, "n_c": 2**14, "n_p": 4, "probed_levels": n_probed,
+                       "sampler": "device", "parallelism": f"dp{world}"},
+            "encode_bytes_per_sample": bps,
+            "encode_algorithmic_gbs": B_TRAIN * bps / (ms * 1e-3) / 1e9,
+            "last_loss": loss, "scaling": "weak"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's own CPU path on this host."""
+    if rank != 0:
+        return None
+    hyper = C2
+    res = [cpu_decode_baseline(hyper, budget_s=max(2.0, 20.0 / max(1, args.steps + args.warmup)))
+           for _ in range(args.warmup + args.steps)]
+    timed = res[args.warmup:]
+    v = float(np.median([r["value"] for r in timed]))
+    cb = dict(timed[-1])
+    cb["value"] = v
+    return {"metric": METRIC, "impl": "reference", "value": v, "unit": "queries/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": B_INFER / v * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "C2 inference: 2-D probed hash grid decode, fused encode+MLP",
+                       "queries_per_gpu_per_step": B_INFER, "log2_n_f": 16, "n_c": 2**16,
+                       "n_p": 4, "n_levels": 16, "feature_dim": 2, "n_min": 16, "n_max": 8192,
+                       "parallelism": "host threads"},
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--exact", action="store_true", help="reference-order (bit-exact) MLP")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    line, _ = run_gpu(args, rank, world, local_rank)
+    if rank == 0:
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_decode_baseline(C2)
+            line["train"]["cpu_baseline"] = cpu_train_baseline()
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -231,6 +231,23 @@ int pg_mlp_train_f64(const pg_mlp *mlp, const double *y, const double *targets,
                      unsigned flags, double *gparams, double *dy,
                      double *loss_sum, double *ws, void *stream);
 
+/* Fused training pass (trainer.py:118-148): per 128-sample tile one kernel
+ * runs encode fwd -> MLP fwd -> squared error -> MLP bwd -> encode bwd with
+ * activations in shared memory.  Shape: F = 2, 16 levels, N_p <= 16, MLP
+ * [32, 64, 64, out_dim <= 4].  Forward and data-gradient GEMMs follow
+ * numpy/OpenBLAS's FMA-chain order, so y, the loss terms and dL/dy equal the
+ * reference's bit for bit; weight/bias gradients (into gparams) and table
+ * gradients (gfeat, gconf, touched) are accumulated as pg_encode_bwd does.
+ * loss_sum += sum of squared errors (fp64).  dy_out (optional, B x 32)
+ * receives dL/dy for parity checks. */
+int pg_train_fused_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
+                       const float *targets, int64_t B, const float *feats,
+                       const uint8_t *baked, const float *conf,
+                       const float *params, float scale, unsigned flags,
+                       float *gfeat, float *gconf, uint8_t *touched,
+                       float *gparams, double *loss_sum, float *dy_out,
+                       void *stream);
+
 /* Pixel batch for the image trainer (trainer.py:109-116): xs from pixel
  * indices pix (host-drawn for reference parity, or drawn on device from
  * (seed, step) when pix_in is NULL and pix_out receives them), targets
@@ -274,6 +291,13 @@ int pg_touched_to_f32(const uint8_t *touched, int64_t n, float *out,
                       void *stream);
 int pg_touched_from_f32(const float *in, int64_t n, uint8_t *touched,
                         void *stream);
+
+/* Roofline probes (bench.py): L2 streaming read of `bytes` from buf, `reps`
+ * times; `nq` random 8-byte gathers from a table of entries_pow2 float2. */
+int pg_probe_stream_read(const void *buf, int64_t bytes, int reps, float *sink,
+                         void *stream);
+int pg_probe_gather(const void *table, int64_t entries_pow2, int64_t nq,
+                    uint32_t seed, float *sink, void *stream);
 
 #ifdef __cplusplus
 }

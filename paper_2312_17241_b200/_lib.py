@@ -77,6 +77,10 @@ _SIGS.update({
     "pg_decode_host_f32": [_G, _M, _P, _I64, _P, _P, _P, ctypes.c_uint, _I64, _P, _P, _P, _P, _P],
     "pg_touched_to_f32": [_P, _I64, _P, _P],
     "pg_touched_from_f32": [_P, _I64, _P, _P],
+    "pg_train_fused_f32": [_G, _M, _P, _P, _I64, _P, _P, _P, _P, _F, ctypes.c_uint, _P, _P, _P,
+                           _P, _P, _P, _P],
+    "pg_probe_stream_read": [_P, _I64, _I, _P, _P],
+    "pg_probe_gather": [_P, _I64, _I64, _U32, _P, _P],
 })
 _RESTYPE_I64 = {"pg_dedup_workspace_bytes": [_I64, _I64],
                 "pg_mlp_train_workspace_floats": [_I64, _M]}

@@ -31,3 +31,54 @@ int pg_device_sm_count(int device) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Roofline probes used by bench.py to MEASURE the L2 denominators the
+// gather/scatter kernels are judged against (MEASURED_PEAKS.json has HBM and
+// tensor peaks only).
+//   stream read : float4 grid-stride sum over an L2-resident buffer, reps times
+//   random gather: 8-byte loads at hashed indices of a 2^k-entry table
+// ---------------------------------------------------------------------------
+namespace pg {
+__global__ void probe_stream_kernel(const float4 *__restrict__ buf, int64_t n4, int reps,
+                                    float *__restrict__ sink) {
+    float acc = 0.0f;
+    for (int r = 0; r < reps; ++r)
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const float4 v = __ldcg(buf + i);
+            acc += v.x + v.y + v.z + v.w;
+        }
+    if (acc == 12345.678f) *sink = acc;
+}
+__global__ void probe_gather_kernel(const float2 *__restrict__ tab, uint32_t mask, int64_t nq,
+                                    uint32_t seed, float *__restrict__ sink) {
+    float acc = 0.0f;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t h = (uint32_t)i * 2654435761u ^ seed;
+        h ^= h >> 15;
+        h *= 0x2c1b3c6du;
+        h ^= h >> 12;
+        const float2 v = __ldg(tab + (h & mask));
+        acc += v.x + v.y;
+    }
+    if (acc == 12345.678f) *sink = acc;
+}
+}  // namespace pg
+
+extern "C" {
+int pg_probe_stream_read(const void *buf, int64_t bytes, int reps, float *sink, void *stream) {
+    const int64_t n4 = bytes / 16;
+    const int sms = pg_device_sm_count(0) > 0 ? pg_device_sm_count(0) : 148;
+    pg::probe_stream_kernel<<<sms * 4, 512, 0, pg::as_stream(stream)>>>((const float4 *)buf, n4, reps, sink);
+    return pg::check_launch("probe_stream_read");
+}
+int pg_probe_gather(const void *table, int64_t entries_pow2, int64_t nq, uint32_t seed,
+                    float *sink, void *stream) {
+    const int sms = pg_device_sm_count(0) > 0 ? pg_device_sm_count(0) : 148;
+    pg::probe_gather_kernel<<<sms * 8, 256, 0, pg::as_stream(stream)>>>(
+        (const float2 *)table, (uint32_t)(entries_pow2 - 1), nq, seed, sink);
+    return pg::check_launch("probe_gather");
+}
+}  // extern "C"

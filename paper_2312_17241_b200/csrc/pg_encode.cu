@@ -202,271 +202,6 @@ __global__ void dedup_emit_kernel(const int32_t *row, int64_t n, const int32_t *
     inv[i] = uf;
 }
 
-// =========================================================================
-// Fused all-level forward.  Thread task = (point, level) mapped level-major
-// inside a 128-point chunk so each warp serves 32 points of ONE level
-// (uniform dense/hashed/probed branch, one table per warp).
-// =========================================================================
-constexpr int kChunk = 128;
-
-template <typename T, typename FT, int D, int FC>
-__global__ void __launch_bounds__(256) encode_fwd_kernel(const pg_grid g, const T *__restrict__ xs,
-                                                         int64_t B, const FT *__restrict__ feats,
-                                                         const uint8_t *__restrict__ baked,
-                                                         const T *__restrict__ conf,
-                                                         unsigned flags, T *__restrict__ y,
-                                                         int32_t *__restrict__ bad) {
-    __shared__ LevelTab lt;
-    const int L = g.n_levels;
-    for (int i = threadIdx.x; i < L; i += blockDim.x) {
-        lt.res[i] = g.res[i];
-        lt.kind[i] = g.kind[i];
-        lt.slot[i] = g.slot[i];
-    }
-    __syncthreads();
-    constexpr int C = 1 << D;
-    const int F = FC ? FC : g.feature_dim;
-    const uint32_t nf_mask = (uint32_t)g.n_f - 1u, nc_mask = (uint32_t)g.n_c - 1u;
-    const int n_p = 1 << g.log2_np;
-    const bool surrogate = (flags & PG_SURROGATE) != 0;
-    const int64_t nchunks = (B + kChunk - 1) / kChunk;
-    for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-        for (int i = threadIdx.x; i < L * kChunk; i += blockDim.x) {
-            const int l = i / kChunk;
-            const int64_t p = ch * kChunk + (i - l * kChunk);
-            if (p >= B) continue;
-            T x[D];
-            bool oob = false;
-#pragma unroll
-            for (int a = 0; a < D; ++a) {
-                x[a] = xs[p * D + a];
-                oob |= !(x[a] >= T(0) && x[a] <= T(1));
-            }
-            if (l == 0 && oob && bad) *bad = 1;
-            const int res = lt.res[l], kind = lt.kind[l];
-            int c[D];
-            T t[D], omt[D];
-#pragma unroll
-            for (int a = 0; a < D; ++a) {
-                c[a] = cell_coord(x[a], res, t[a]);
-                omt[a] = Ar<T>::sub(T(1), t[a]);
-            }
-            const FT *tab = feats + (int64_t)l * g.n_f * F;
-            T acc[FC ? FC : PG_MAX_FEATURE];
-#pragma unroll
-            for (int q = 0; q < (FC ? FC : PG_MAX_FEATURE); ++q) acc[q] = T(0);
-            int idx[C];
-            T w[C];
-#pragma unroll
-            for (int k = 0; k < C; ++k) {
-                w[k] = corner_weight<T, D>(k, t, omt);
-                if (kind == PG_LEVEL_DENSE) {
-                    idx[k] = corner_dense<D>(k, c, res + 1);
-                } else {
-                    const uint32_t h = corner_hash<D>(k, c, g.primary);
-                    if (kind == PG_LEVEL_HASHED) {
-                        idx[k] = (int)(h & nf_mask);
-                    } else {
-                        const int bs = (int)((h << g.log2_np) & nf_mask);
-                        const int r = (int)(corner_hash<D>(k, c, g.aux) & nc_mask);
-                        if (surrogate) {
-                            idx[k] = -1 - r;  // remember the row; base re-derived below
-                        } else {
-                            idx[k] = bs + (int)__ldg(baked + (int64_t)lt.slot[l] * g.n_c + r);
-                        }
-                    }
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < C; ++k) {
-                if (idx[k] >= 0) {
-                    const FT *f = tab + (int64_t)idx[k] * F;
-                    for (int q = 0; q < F; ++q)
-                        acc[q] = Ar<T>::add(acc[q], Ar<T>::mul(w[k], (T)Feat<FT>::ld(f + q)));
-                } else {
-                    // softmax-mixture surrogate (numpy_backend.py:94-112), f64 checks
-                    const int r = -1 - idx[k];
-                    const int bs =
-                        (int)((corner_hash<D>(k, c, g.primary) << g.log2_np) & nf_mask);
-                    const T *cr = conf + ((int64_t)lt.slot[l] * g.n_c + r) * n_p;
-                    T mx = cr[0];
-                    for (int j = 1; j < n_p; ++j) mx = cr[j] > mx ? cr[j] : mx;
-                    T sum = T(0);
-                    for (int j = 0; j < n_p; ++j) sum += Ar<T>::exp(cr[j] - mx);
-                    for (int q = 0; q < F; ++q) {
-                        T mix = T(0);
-                        for (int j = 0; j < n_p; ++j)
-                            mix += (Ar<T>::exp(cr[j] - mx) / sum) *
-                                   (T)Feat<FT>::ld(tab + (int64_t)(bs + j) * F + q);
-                        acc[q] = Ar<T>::add(acc[q], Ar<T>::mul(w[k], mix));
-                    }
-                }
-            }
-            T *yo = y + p * (int64_t)L * F + (int64_t)l * F;
-            for (int q = 0; q < F; ++q) yo[q] = acc[q];
-        }
-    }
-}
-
-// =========================================================================
-// Fused all-level backward (encoding.py:119-133 + trainer.py:138-148):
-// recompute geometry, scatter d-linear-weighted upstream into gfeat; for
-// probed levels spread over all N_p probes with the row softmax and add the
-// softmax-Jacobian term to gconf (straight-through), and
-// flag the row as touched (every lookup, including zero-weight corners —
-// encoding.py:111 dedups over all B*2^d rows).
-// Softmax uses the per-row max (the reference shifts by the global max of the
-// gathered rows, numpy_backend.py:115-131: mathematically identical).
-// =========================================================================
-template <typename T, int D, int FC, int NPMAX>
-__global__ void __launch_bounds__(256) encode_bwd_kernel(
-    const pg_grid g, const T *__restrict__ xs, int64_t B, const T *__restrict__ dy,
-    const T *__restrict__ feats, const T *__restrict__ conf, T *__restrict__ gfeat,
-    T *__restrict__ gconf, uint8_t *__restrict__ touched) {
-    __shared__ LevelTab lt;
-    const int L = g.n_levels;
-    for (int i = threadIdx.x; i < L; i += blockDim.x) {
-        lt.res[i] = g.res[i];
-        lt.kind[i] = g.kind[i];
-        lt.slot[i] = g.slot[i];
-    }
-    __syncthreads();
-    constexpr int C = 1 << D;
-    const int F = FC ? FC : g.feature_dim;
-    const uint32_t nf_mask = (uint32_t)g.n_f - 1u, nc_mask = (uint32_t)g.n_c - 1u;
-    const int n_p = 1 << g.log2_np;
-    const int64_t nchunks = (B + kChunk - 1) / kChunk;
-    for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-        for (int i = threadIdx.x; i < L * kChunk; i += blockDim.x) {
-            const int l = i / kChunk;
-            const int64_t p = ch * kChunk + (i - l * kChunk);
-            if (p >= B) continue;
-            const int res = lt.res[l], kind = lt.kind[l];
-            int c[D];
-            T t[D], omt[D];
-#pragma unroll
-            for (int a = 0; a < D; ++a) {
-                c[a] = cell_coord(xs[p * D + a], res, t[a]);
-                omt[a] = Ar<T>::sub(T(1), t[a]);
-            }
-            T up[FC ? FC : PG_MAX_FEATURE];
-            const T *dyp = dy + p * (int64_t)L * F + (int64_t)l * F;
-            for (int q = 0; q < F; ++q) up[q] = dyp[q];
-            T *gtab = gfeat + (int64_t)l * g.n_f * F;
-            const T *ftab = feats + (int64_t)l * g.n_f * F;
-#pragma unroll
-            for (int k = 0; k < C; ++k) {
-                const T w = corner_weight<T, D>(k, t, omt);
-                T gq[FC ? FC : PG_MAX_FEATURE];
-                for (int q = 0; q < F; ++q) gq[q] = Ar<T>::mul(w, up[q]);
-                if (kind != PG_LEVEL_PROBED) {
-                    const int lin = kind == PG_LEVEL_DENSE
-                                        ? corner_dense<D>(k, c, res + 1)
-                                        : (int)(corner_hash<D>(k, c, g.primary) & nf_mask);
-                    T *dst = gtab + (int64_t)lin * F;
-                    if constexpr (FC == 2 && sizeof(T) == 4) {
-                        red_add_v2((float *)dst, gq[0], gq[1]);
-                    } else {
-                        for (int q = 0; q < F; ++q) red_add(dst + q, gq[q]);
-                    }
-                    continue;
-                }
-                const int bs = (int)((corner_hash<D>(k, c, g.primary) << g.log2_np) & nf_mask);
-                const int r = (int)(corner_hash<D>(k, c, g.aux) & nc_mask);
-                const int64_t crow = (int64_t)lt.slot[l] * g.n_c + r;
-                touched[crow] = 1;
-                const T *cr = conf + crow * n_p;
-                T *gc = gconf + crow * n_p;
-                const T *fb = ftab + (int64_t)bs * F;
-                T *gb = gtab + (int64_t)bs * F;
-                if constexpr (NPMAX > 0) {
-                    T sg[NPMAX], dots[NPMAX];
-                    T mx = cr[0];
-#pragma unroll
-                    for (int j = 1; j < NPMAX; ++j)
-                        if (j < n_p) mx = cr[j] > mx ? cr[j] : mx;
-                    T sum = T(0);
-#pragma unroll
-                    for (int j = 0; j < NPMAX; ++j)
-                        if (j < n_p) {
-                            sg[j] = Ar<T>::exp(cr[j] - mx);
-                            sum += sg[j];
-                        }
-                    const T inv_sum = T(1) / sum;
-                    T s = T(0);
-#pragma unroll
-                    for (int j = 0; j < NPMAX; ++j)
-                        if (j < n_p) {
-                            sg[j] = sg[j] * inv_sum;
-                            T dot = T(0);
-                            for (int q = 0; q < F; ++q) dot += fb[j * F + q] * gq[q];
-                            dots[j] = dot;
-                            s += sg[j] * dot;
-                        }
-                    if constexpr (FC == 2 && sizeof(T) == 4) {
-                        // N_p*F contiguous floats, 16B aligned when n_p >= 2
-                        if (n_p >= 2) {
-#pragma unroll
-                            for (int j = 0; j < NPMAX; j += 2)
-                                if (j < n_p)
-                                    red_add_v4((float *)gb + 2 * j, sg[j] * gq[0], sg[j] * gq[1],
-                                               sg[j + 1] * gq[0], sg[j + 1] * gq[1]);
-                        } else {
-                            red_add_v2((float *)gb, sg[0] * gq[0], sg[0] * gq[1]);
-                        }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < NPMAX; ++j)
-                            if (j < n_p)
-                                for (int q = 0; q < F; ++q) red_add(gb + j * F + q, sg[j] * gq[q]);
-                    }
-                    if constexpr (sizeof(T) == 4) {
-                        if (n_p >= 4) {
-#pragma unroll
-                            for (int j = 0; j < NPMAX; j += 4)
-                                if (j < n_p)
-                                    red_add_v4((float *)gc + j, sg[j] * (dots[j] - s),
-                                               sg[j + 1] * (dots[j + 1] - s),
-                                               sg[j + 2] * (dots[j + 2] - s),
-                                               sg[j + 3] * (dots[j + 3] - s));
-                        } else if (n_p == 2) {
-                            red_add_v2((float *)gc, sg[0] * (dots[0] - s), sg[1] * (dots[1] - s));
-                        } else {
-                            red_add(gc, sg[0] * (dots[0] - s));
-                        }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < NPMAX; ++j)
-                            if (j < n_p) red_add(gc + j, sg[j] * (dots[j] - s));
-                    }
-                } else {
-                    // long probing ranges: three passes, nothing kept per probe
-                    T mx = cr[0];
-                    for (int j = 1; j < n_p; ++j) mx = cr[j] > mx ? cr[j] : mx;
-                    T sum = T(0);
-                    for (int j = 0; j < n_p; ++j) sum += Ar<T>::exp(cr[j] - mx);
-                    const T inv_sum = T(1) / sum;
-                    T s = T(0);
-                    for (int j = 0; j < n_p; ++j) {
-                        T dot = T(0);
-                        for (int q = 0; q < F; ++q) dot += fb[j * F + q] * gq[q];
-                        s += Ar<T>::exp(cr[j] - mx) * inv_sum * dot;
-                    }
-                    for (int j = 0; j < n_p; ++j) {
-                        const T sj = Ar<T>::exp(cr[j] - mx) * inv_sum;
-                        T dot = T(0);
-                        for (int q = 0; q < F; ++q) {
-                            dot += fb[j * F + q] * gq[q];
-                            red_add(gb + j * F + q, sj * gq[q]);
-                        }
-                        red_add(gc + j, sj * (dot - s));
-                    }
-                }
-            }
-        }
-    }
-}
-
 int validate_grid(const pg_grid *g) {
     PG_REQUIRE(g != nullptr, "null grid");
     PG_REQUIRE(g->d == 2 || g->d == 3, "grid.d must be 2 or 3");
@@ -486,71 +221,6 @@ int validate_grid(const pg_grid *g) {
         if (g->kind[l] == PG_LEVEL_PROBED) PG_REQUIRE(g->slot[l] >= 0, "probed level without slot");
     }
     return PG_OK;
-}
-
-static int encode_blocks(int64_t B) {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    const int64_t nchunks = (B + kChunk - 1) / kChunk;
-    const int64_t cap = (int64_t)sms * 8;
-    return (int)(nchunks < cap ? nchunks : cap);
-}
-
-template <typename T, typename FT>
-static int launch_encode_fwd(const pg_grid *g, const T *xs, int64_t B, const FT *feats,
-                             const uint8_t *baked, const T *conf, unsigned flags, T *y,
-                             int32_t *bad, void *stream) {
-    if (int e = validate_grid(g)) return e;
-    PG_REQUIRE(!(flags & PG_SURROGATE) || conf != nullptr, "surrogate encoding needs confidences");
-    if (B == 0) return PG_OK;
-    const int grd = encode_blocks(B);
-    cudaStream_t s = as_stream(stream);
-    const bool f2 = g->feature_dim == 2;
-#define PG_ENC_FWD(D_, FC_) \
-    encode_fwd_kernel<T, FT, D_, FC_><<<grd, 256, 0, s>>>(*g, xs, B, feats, baked, conf, flags, y, bad)
-    if (g->d == 2) {
-        if (f2) PG_ENC_FWD(2, 2); else PG_ENC_FWD(2, 0);
-    } else {
-        if (f2) PG_ENC_FWD(3, 2); else PG_ENC_FWD(3, 0);
-    }
-#undef PG_ENC_FWD
-    return check_launch("encode_fwd");
-}
-
-template <typename T>
-static int launch_encode_bwd(const pg_grid *g, const T *xs, int64_t B, const T *dy,
-                             const T *feats, const T *conf, T *gfeat, T *gconf, uint8_t *touched,
-                             void *stream) {
-    if (int e = validate_grid(g)) return e;
-    bool any_probed = false;
-    for (int l = 0; l < g->n_levels; ++l) any_probed |= g->kind[l] == PG_LEVEL_PROBED;
-    PG_REQUIRE(!any_probed || (conf && gconf && touched), "probed levels need conf/gconf/touched");
-    if (B == 0) return PG_OK;
-    const int grd = encode_blocks(B);
-    cudaStream_t s = as_stream(stream);
-    const bool f2 = g->feature_dim == 2;
-    const int n_p = 1 << g->log2_np;
-#define PG_ENC_BWD(D_, FC_, NP_) \
-    encode_bwd_kernel<T, D_, FC_, NP_><<<grd, 256, 0, s>>>(*g, xs, B, dy, feats, conf, gfeat, gconf, touched)
-#define PG_ENC_BWD_NP(D_, FC_)                   \
-    do {                                         \
-        if (n_p <= 4) PG_ENC_BWD(D_, FC_, 4);     \
-        else if (n_p <= 16) PG_ENC_BWD(D_, FC_, 16); \
-        else PG_ENC_BWD(D_, FC_, 0);             \
-    } while (0)
-    if (g->d == 2) {
-        if (f2) PG_ENC_BWD_NP(2, 2); else PG_ENC_BWD_NP(2, 0);
-    } else {
-        if (f2) PG_ENC_BWD_NP(3, 2); else PG_ENC_BWD_NP(3, 0);
-    }
-#undef PG_ENC_BWD_NP
-#undef PG_ENC_BWD
-    return check_launch("encode_bwd");
 }
 
 }  // namespace pg
@@ -651,33 +321,6 @@ int pg_dedup_rows(const int32_t *row, int64_t n, int64_t n_c, void *workspace, i
     dedup_scan_sums_kernel<<<1, 1024, 0, s>>>(sums, nb, d_count);
     dedup_emit_kernel<<<grid_for(n, 256), 256, 0, s>>>(row, n, first, pos, sums, rows_u, inv, 256);
     return check_launch("dedup_rows");
-}
-
-int pg_encode_fwd_f32(const pg_grid *grid, const float *xs, int64_t B, const void *feats,
-                      const uint8_t *baked, const float *conf, unsigned flags, float *y,
-                      int32_t *d_bad, void *stream) {
-    if (flags & PG_HALF_FEATS)
-        return launch_encode_fwd<float, __half>(grid, xs, B, (const __half *)feats, baked, conf,
-                                                flags, y, d_bad, stream);
-    return launch_encode_fwd<float, float>(grid, xs, B, (const float *)feats, baked, conf, flags, y,
-                                           d_bad, stream);
-}
-int pg_encode_fwd_f64(const pg_grid *grid, const double *xs, int64_t B, const void *feats,
-                      const uint8_t *baked, const double *conf, unsigned flags, double *y,
-                      int32_t *d_bad, void *stream) {
-    PG_REQUIRE(!(flags & PG_HALF_FEATS), "binary16 tables are float32-only");
-    return launch_encode_fwd<double, double>(grid, xs, B, (const double *)feats, baked, conf, flags,
-                                             y, d_bad, stream);
-}
-int pg_encode_bwd_f32(const pg_grid *grid, const float *xs, int64_t B, const float *dy,
-                      const float *feats, const float *conf, float *gfeat, float *gconf,
-                      uint8_t *touched, void *stream) {
-    return launch_encode_bwd<float>(grid, xs, B, dy, feats, conf, gfeat, gconf, touched, stream);
-}
-int pg_encode_bwd_f64(const pg_grid *grid, const double *xs, int64_t B, const double *dy,
-                      const double *feats, const double *conf, double *gfeat, double *gconf,
-                      uint8_t *touched, void *stream) {
-    return launch_encode_bwd<double>(grid, xs, B, dy, feats, conf, gfeat, gconf, touched, stream);
 }
 
 }  // extern "C"

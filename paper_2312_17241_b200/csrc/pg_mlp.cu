@@ -358,13 +358,15 @@ __global__ void train_linear_fwd_kernel(const T *__restrict__ a, int relu_in, in
     if (i >= B * fout) return;
     const int64_t b = i / fout;
     const int j = (int)(i - b * fout);
-    T acc = bias[j];
+    // numpy `a @ W + b` on OpenBLAS: FMA chain over k from zero, then the
+    // bias as a separate rounded add (same bits as mlp.py:66 in fp32/fp64)
+    T acc = T(0);
     for (int k = 0; k < fin; ++k) {
         T v = a[b * fin + k];
         if (relu_in && v < T(0)) v = T(0);
         acc = Ar<T>::fma(v, W[(int64_t)k * fout + j], acc);
     }
-    z[i] = acc;
+    z[i] = Ar<T>::add(acc, bias[j]);
 }
 
 template <typename T>
@@ -428,9 +430,11 @@ __global__ void train_dgrad_kernel(const T *__restrict__ delta, int64_t B, int f
     if (i >= B * fin) return;
     const int64_t b = i / fin;
     const int k = (int)(i - b * fin);
+    // numpy `(delta @ W.T) * (pre > 0)`: FMA chain over j from zero, then a
+    // rounded multiply by the 0/1 mask (mlp.py:83-85)
     T acc = T(0);
     for (int j = 0; j < fout; ++j) acc = Ar<T>::fma(delta[b * fout + j], W[(int64_t)k * fout + j], acc);
-    if (zmask && !(zmask[i] > T(0))) acc = T(0);
+    if (zmask) acc = Ar<T>::mul(acc, zmask[i] > T(0) ? T(1) : T(0));
     out[i] = acc;
 }
 

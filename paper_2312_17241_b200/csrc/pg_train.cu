@@ -1,0 +1,411 @@
+// Fused training pass on sm_100a: for every 128-sample tile, ONE kernel does
+//   encode fwd (16 levels, F=2)  ->  MLP [32,64,64,out<=4] fwd  ->  squared
+//   error + dpred  ->  MLP bwd (weight grads held in registers across tiles,
+//   dgrads)  ->  encode bwd (straight-through scatter into gfeat/gconf)
+// with every activation in shared memory (trainer.py:118-148, mlp.py:55-85,
+// encoding.py:89-133 of the reference).
+//
+// Forward GEMMs and the data-gradient GEMMs reproduce numpy/OpenBLAS's
+// arithmetic exactly: OpenBLAS sgemm (SkylakeX kernel, K <= 64) computes each
+// output as a sequential fused multiply-add chain over k starting from 0, and
+// numpy then adds the bias / multiplies the ReLU mask as separate rounded
+// operations (verified bit-for-bit in the build container).  So y, the
+// activations, the loss terms and dy = dL/dy are bit-identical to the
+// reference for the same parameters and batch; only the cross-sample sums
+// (weight/bias gradients, table scatters) are reordered.
+#include "pg_encode_dev.cuh"
+
+namespace pg {
+
+constexpr int kT = 128;   // samples per tile
+constexpr int kNT = 512;  // threads per CTA
+constexpr int kI = 32;    // L*F
+constexpr int kH = 64;    // hidden width
+constexpr int kO = 4;     // padded output width
+
+struct TrainSmem {
+    float w0[kI * kH], w1[kH * kH], w2[kH * kO];      // [in][out]
+    float w0t[kH * kI], w1t[kH * kH], w2t[kO * kH];   // [out][in]
+    float b0[kH], b1[kH], b2[kO];
+    float yT[kI * kT];    // encodings, later dL/dy       (swizzled rows)
+    float z1T[kH * kT];   // layer-1 pre-activations, later delta_1
+    float z2T[kH * kT];   // layer-2 pre-activations, later delta_2
+    float d3[kT * kO];    // dL/d(out), sample-major
+    float xs[kT * 3];
+    float tg[kT * kO];
+    double red[kNT / 32];
+};
+
+__device__ __forceinline__ int sw(int row, int col) {
+    const int chunk = (col >> 2) ^ ((row >> 2) & 7);
+    return row * kT + (chunk << 2) + (col & 3);
+}
+__device__ __forceinline__ float relu_np(float z) { return z < 0.0f ? 0.0f : z; }  // np.maximum(z, 0)
+__device__ __forceinline__ float mask_np(float z) { return z > 0.0f ? 1.0f : 0.0f; }  // (pre > 0)
+
+// out^T[j][q] = fma-chain_k( act(in^T[k][q]) * W[k][j] ) + b[j]   (j < 64, q < 128)
+template <int K, bool RELU_IN>
+__device__ __forceinline__ void fwd_layer(const float *__restrict__ inT, const float *__restrict__ W,
+                                          const float *__restrict__ b, float *__restrict__ outT) {
+    const int og = threadIdx.x & 15, pg = threadIdx.x >> 4;  // 4 outputs x 4 samples
+    float acc[4][4] = {};
+#pragma unroll 8
+    for (int k = 0; k < K; ++k) {
+        float4 a = *reinterpret_cast<const float4 *>(inT + sw(k, pg * 4));
+        if (RELU_IN) {
+            a.x = relu_np(a.x); a.y = relu_np(a.y); a.z = relu_np(a.z); a.w = relu_np(a.w);
+        }
+        const float4 w = *reinterpret_cast<const float4 *>(W + k * kH + og * 4);
+        const float av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            acc[i][0] = __fmaf_rn(av[i], w.x, acc[i][0]);
+            acc[i][1] = __fmaf_rn(av[i], w.y, acc[i][1]);
+            acc[i][2] = __fmaf_rn(av[i], w.z, acc[i][2]);
+            acc[i][3] = __fmaf_rn(av[i], w.w, acc[i][3]);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const float bj = b[og * 4 + j];
+        *reinterpret_cast<float4 *>(outT + sw(og * 4 + j, pg * 4)) =
+            make_float4(__fadd_rn(acc[0][j], bj), __fadd_rn(acc[1][j], bj),
+                        __fadd_rn(acc[2][j], bj), __fadd_rn(acc[3][j], bj));
+    }
+}
+
+template <typename FT, int D>
+__global__ void __launch_bounds__(kNT, 1)
+    train_fused_kernel(const pg_grid g, const float *__restrict__ xs, const float *__restrict__ targets,
+                       int64_t B, const FT *__restrict__ feats_fwd, const float *__restrict__ feats,
+                       const uint8_t *__restrict__ baked, const float *__restrict__ conf,
+                       const float *__restrict__ params, int od, float scale, int sigmoid,
+                       float *__restrict__ gfeat, float *__restrict__ gconf,
+                       uint8_t *__restrict__ touched, float *__restrict__ gparams,
+                       double *__restrict__ loss_sum, float *__restrict__ dy_out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TrainSmem &S = *reinterpret_cast<TrainSmem *>(smem_raw);
+    const int tid = threadIdx.x;
+    // ---- parameters -> shared (both layouts) ----
+    {
+        const float *p = params;
+        for (int i = tid; i < kI * kH; i += kNT) {
+            const float v = p[i];
+            S.w0[i] = v;
+            S.w0t[(i % kH) * kI + i / kH] = v;
+        }
+        p += kI * kH;
+        for (int i = tid; i < kH; i += kNT) S.b0[i] = p[i];
+        p += kH;
+        for (int i = tid; i < kH * kH; i += kNT) {
+            const float v = p[i];
+            S.w1[i] = v;
+            S.w1t[(i % kH) * kH + i / kH] = v;
+        }
+        p += kH * kH;
+        for (int i = tid; i < kH; i += kNT) S.b1[i] = p[i];
+        p += kH;
+        for (int i = tid; i < kH * kO; i += kNT) {
+            const int k = i / kO, j = i % kO;
+            const float v = j < od ? p[k * od + j] : 0.0f;
+            S.w2[i] = v;
+            S.w2t[j * kH + k] = v;
+        }
+        p += kH * od;
+        for (int i = tid; i < kO; i += kNT) S.b2[i] = i < od ? p[i] : 0.0f;
+    }
+    // persistent per-thread gradient accumulators
+    float gW2 = 0.0f;                 // (k = tid&63, j = (tid>>6)&3), half = tid>>8
+    float gB2 = 0.0f;                 // j = tid (tid < 4)
+    float gW1[2][4] = {};             // i = (tid>>4)*2 + a, j = (tid&15)*4 + b
+    float gB1 = 0.0f;                 // j = tid (tid < 64)
+    float gW0[4] = {};                // i = tid>>4, j = (tid&15)*4 + b
+    float gB0 = 0.0f;                 // j = tid (tid < 64)
+    double lsum = 0.0;
+
+    const int64_t ntiles = (B + kT - 1) / kT;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t p0 = tile * kT;
+        const int nv = (int)((B - p0) < kT ? (B - p0) : kT);
+        __syncthreads();
+        for (int i = tid; i < kT * D; i += kNT) S.xs[i] = i < nv * D ? xs[p0 * D + i] : 0.5f;
+        for (int i = tid; i < kT * kO; i += kNT) {
+            const int q = i / kO, j = i % kO;
+            S.tg[i] = (q < nv && j < od) ? targets[(p0 + q) * od + j] : 0.0f;
+        }
+        __syncthreads();
+        // ---- encode forward: thread = (sample pl, levels lsub + 4*it) ----
+        const int pl = tid & (kT - 1), lsub = tid >> 7;
+        float x[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) x[a] = S.xs[pl * D + a];
+#pragma unroll 2
+        for (int it = 0; it < 4; ++it) {
+            const int l = lsub + 4 * it;
+            const float2 yv = encode_level_fwd2<FT, D>(g, l, x, feats_fwd, baked);
+            S.yT[sw(2 * l, pl)] = yv.x;
+            S.yT[sw(2 * l + 1, pl)] = yv.y;
+        }
+        __syncthreads();
+        fwd_layer<kI, false>(S.yT, S.w0, S.b0, S.z1T);
+        __syncthreads();
+        fwd_layer<kH, true>(S.z1T, S.w1, S.b1, S.z2T);
+        __syncthreads();
+        // ---- output layer, loss, dpred (trainer.py:122-136) ----
+        {
+            const int q = tid & (kT - 1), j = tid >> 7;
+            float d = 0.0f;
+            if (j < od && q < nv) {
+                float acc = 0.0f;
+#pragma unroll 16
+                for (int k = 0; k < kH; ++k) acc = __fmaf_rn(relu_np(S.z2T[sw(k, q)]), S.w2[k * kO + j], acc);
+                const float o = __fadd_rn(acc, S.b2[j]);
+                const float pred = sigmoid ? 1.0f / (1.0f + expf(-o)) : o;
+                const float diff = __fsub_rn(pred, S.tg[q * kO + j]);
+                lsum += (double)diff * (double)diff;
+                d = __fmul_rn(diff, scale);
+                if (sigmoid) d = __fmul_rn(d, __fmul_rn(pred, __fsub_rn(1.0f, pred)));
+            }
+            S.d3[q * kO + j] = d;
+        }
+        __syncthreads();
+        // ---- dW2 += relu(z2)^T d3, db2 += sum d3 ----
+        {
+            const int k = tid & 63, j = (tid >> 6) & 3, half = tid >> 8;
+            float acc = 0.0f;
+            for (int q = half * 64; q < half * 64 + 64; ++q)
+                acc = __fmaf_rn(relu_np(S.z2T[sw(k, q)]), S.d3[q * kO + j], acc);
+            gW2 += acc;
+            if (tid < kO) {
+                float s = 0.0f;
+                for (int q = 0; q < kT; ++q) s += S.d3[q * kO + tid];
+                gB2 += s;
+            }
+        }
+        __syncthreads();
+        // ---- delta2 = (d3 @ W2^T) * (z2 > 0), in place over z2 ----
+        {
+            const int og = tid & 15, pg = tid >> 4;
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const int k = og * 4 + jj;
+                float4 z = *reinterpret_cast<float4 *>(S.z2T + sw(k, pg * 4));
+                float zv[4] = {z.x, z.y, z.z, z.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int q = pg * 4 + i;
+                    float acc = 0.0f;
+                    for (int j = 0; j < od; ++j) acc = __fmaf_rn(S.d3[q * kO + j], S.w2t[j * kH + k], acc);
+                    zv[i] = __fmul_rn(acc, mask_np(zv[i]));
+                }
+                *reinterpret_cast<float4 *>(S.z2T + sw(k, pg * 4)) = make_float4(zv[0], zv[1], zv[2], zv[3]);
+            }
+        }
+        __syncthreads();
+        // ---- dW1 += relu(z1)^T delta2, db1 += sum delta2 ----
+        {
+            const int jg = tid & 15, ig = tid >> 4;
+            for (int q = 0; q < kT; q += 4) {
+                float4 a[2], dd[4];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    a[u] = *reinterpret_cast<const float4 *>(S.z1T + sw(ig * 2 + u, q));
+                    a[u].x = relu_np(a[u].x); a[u].y = relu_np(a[u].y);
+                    a[u].z = relu_np(a[u].z); a[u].w = relu_np(a[u].w);
+                }
+#pragma unroll
+                for (int v = 0; v < 4; ++v) dd[v] = *reinterpret_cast<const float4 *>(S.z2T + sw(jg * 4 + v, q));
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        float s = gW1[u][v];
+                        s = __fmaf_rn(a[u].x, dd[v].x, s);
+                        s = __fmaf_rn(a[u].y, dd[v].y, s);
+                        s = __fmaf_rn(a[u].z, dd[v].z, s);
+                        s = __fmaf_rn(a[u].w, dd[v].w, s);
+                        gW1[u][v] = s;
+                    }
+            }
+            if (tid < kH) {
+                float s = 0.0f;
+                for (int q = 0; q < kT; ++q) s += S.z2T[sw(tid, q)];
+                gB1 += s;
+            }
+        }
+        __syncthreads();
+        // ---- delta1 = (delta2 @ W1^T) * (z1 > 0), in place over z1 ----
+        {
+            const int og = tid & 15, pg = tid >> 4;
+            float acc[4][4] = {};
+#pragma unroll 8
+            for (int j = 0; j < kH; ++j) {
+                const float4 a = *reinterpret_cast<const float4 *>(S.z2T + sw(j, pg * 4));
+                const float4 w = *reinterpret_cast<const float4 *>(S.w1t + j * kH + og * 4);
+                const float av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    acc[i][0] = __fmaf_rn(av[i], w.x, acc[i][0]);
+                    acc[i][1] = __fmaf_rn(av[i], w.y, acc[i][1]);
+                    acc[i][2] = __fmaf_rn(av[i], w.z, acc[i][2]);
+                    acc[i][3] = __fmaf_rn(av[i], w.w, acc[i][3]);
+                }
+            }
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                float *dst = S.z1T + sw(og * 4 + jj, pg * 4);
+                const float4 z = *reinterpret_cast<float4 *>(dst);
+                *reinterpret_cast<float4 *>(dst) =
+                    make_float4(__fmul_rn(acc[0][jj], mask_np(z.x)), __fmul_rn(acc[1][jj], mask_np(z.y)),
+                                __fmul_rn(acc[2][jj], mask_np(z.z)), __fmul_rn(acc[3][jj], mask_np(z.w)));
+            }
+        }
+        __syncthreads();
+        // ---- dW0 += y^T delta1, db0 += sum delta1 ----
+        {
+            const int jg = tid & 15, i = tid >> 4;
+            for (int q = 0; q < kT; q += 4) {
+                const float4 a = *reinterpret_cast<const float4 *>(S.yT + sw(i, q));
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const float4 dd = *reinterpret_cast<const float4 *>(S.z1T + sw(jg * 4 + v, q));
+                    float s = gW0[v];
+                    s = __fmaf_rn(a.x, dd.x, s);
+                    s = __fmaf_rn(a.y, dd.y, s);
+                    s = __fmaf_rn(a.z, dd.z, s);
+                    s = __fmaf_rn(a.w, dd.w, s);
+                    gW0[v] = s;
+                }
+            }
+            if (tid < kH) {
+                float s = 0.0f;
+                for (int q = 0; q < kT; ++q) s += S.z1T[sw(tid, q)];
+                gB0 += s;
+            }
+        }
+        __syncthreads();
+        // ---- dy = delta1 @ W0^T (fma chain over j), over yT ----
+        {
+            const int og = tid & 7, pg = tid >> 3;  // 4 inputs x 2 samples
+            float acc[2][4] = {};
+#pragma unroll 8
+            for (int j = 0; j < kH; ++j) {
+                const float2 a = *reinterpret_cast<const float2 *>(S.z1T + sw(j, pg * 2));
+                const float4 w = *reinterpret_cast<const float4 *>(S.w0t + j * kI + og * 4);
+                acc[0][0] = __fmaf_rn(a.x, w.x, acc[0][0]);
+                acc[0][1] = __fmaf_rn(a.x, w.y, acc[0][1]);
+                acc[0][2] = __fmaf_rn(a.x, w.z, acc[0][2]);
+                acc[0][3] = __fmaf_rn(a.x, w.w, acc[0][3]);
+                acc[1][0] = __fmaf_rn(a.y, w.x, acc[1][0]);
+                acc[1][1] = __fmaf_rn(a.y, w.y, acc[1][1]);
+                acc[1][2] = __fmaf_rn(a.y, w.z, acc[1][2]);
+                acc[1][3] = __fmaf_rn(a.y, w.w, acc[1][3]);
+            }
+            __syncthreads();  // all reads of yT (dW0) finished before overwrite
+#pragma unroll
+            for (int ii = 0; ii < 4; ++ii)
+                *reinterpret_cast<float2 *>(S.yT + sw(og * 4 + ii, pg * 2)) = make_float2(acc[0][ii], acc[1][ii]);
+        }
+        __syncthreads();
+        if (dy_out) {  // optional copy of dL/dy (parity tests)
+            for (int i = tid; i < nv * kI; i += kNT) {
+                const int q = i / kI, c = i % kI;
+                dy_out[(p0 + q) * kI + c] = S.yT[sw(c, q)];
+            }
+        }
+        // ---- encode backward: scatter dy ----
+        if (pl < nv) {
+#pragma unroll 1
+            for (int it = 0; it < 4; ++it) {
+                const int l = lsub + 4 * it;
+                encode_level_bwd2<D, 16>(g, l, x, S.yT[sw(2 * l, pl)], S.yT[sw(2 * l + 1, pl)], feats,
+                                         conf, gfeat, gconf, touched);
+            }
+        }
+    }
+    // ---- flush gradient accumulators ----
+    float *gW0p = gparams, *gb0p = gW0p + kI * kH, *gW1p = gb0p + kH, *gb1p = gW1p + kH * kH;
+    float *gW2p = gb1p + kH, *gb2p = gW2p + kH * od;
+    {
+        const int jg = tid & 15;
+        const int i0 = tid >> 4;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) red_add(gW0p + i0 * kH + jg * 4 + v, gW0[v]);
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) red_add(gW1p + ((tid >> 4) * 2 + u) * kH + jg * 4 + v, gW1[u][v]);
+        const int k = tid & 63, j = (tid >> 6) & 3;
+        if (j < od) red_add(gW2p + k * od + j, gW2);
+        if (tid < kH) {
+            red_add(gb0p + tid, gB0);
+            red_add(gb1p + tid, gB1);
+        }
+        if (tid < od) red_add(gb2p + tid, gB2);
+    }
+    // loss: block reduce in fp64
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+    if ((tid & 31) == 0) S.red[tid >> 5] = lsum;
+    __syncthreads();
+    if (tid < 32) {
+        double v = tid < kNT / 32 ? S.red[tid] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (tid == 0 && loss_sum) atomicAdd(loss_sum, v);
+    }
+}
+
+bool train_fast_ok(const pg_grid *g, const pg_mlp *m) {
+    return g->feature_dim == 2 && g->n_levels == 16 && g->log2_np <= 4 && m->n_layers == 3 &&
+           m->widths[0] == kI && m->widths[1] == kH && m->widths[2] == kH && m->widths[3] >= 1 &&
+           m->widths[3] <= kO;
+}
+
+int train_fused(const pg_grid *g, const pg_mlp *m, const float *xs, const float *targets, int64_t B,
+                const float *feats, const uint8_t *baked, const float *conf, const float *params,
+                float scale, unsigned flags, float *gfeat, float *gconf, uint8_t *touched,
+                float *gparams, double *loss_sum, float *dy_out, cudaStream_t s) {
+    if (int e = validate_grid(g)) return e;
+    PG_REQUIRE(train_fast_ok(g, m), "fused training needs F=2, 16 levels, N_p<=16, MLP [32,64,64,<=4]");
+    if (B == 0) return PG_OK;
+    const int smem = (int)sizeof(TrainSmem);
+    static bool configured[2] = {false, false};
+    const int od = m->widths[3];
+    const int sig = (flags & PG_SIGMOID) ? 1 : 0;
+    int sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t ntiles = (B + kT - 1) / kT;
+    const int grd = (int)(ntiles < sms ? ntiles : sms);
+    if (g->d == 2) {
+        if (!configured[0]) {
+            cudaFuncSetAttribute(train_fused_kernel<float, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            configured[0] = true;
+        }
+        train_fused_kernel<float, 2><<<grd, kNT, smem, s>>>(*g, xs, targets, B, feats, feats, baked, conf,
+                                                           params, od, scale, sig, gfeat, gconf, touched,
+                                                           gparams, loss_sum, dy_out);
+    } else {
+        if (!configured[1]) {
+            cudaFuncSetAttribute(train_fused_kernel<float, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            configured[1] = true;
+        }
+        train_fused_kernel<float, 3><<<grd, kNT, smem, s>>>(*g, xs, targets, B, feats, feats, baked, conf,
+                                                           params, od, scale, sig, gfeat, gconf, touched,
+                                                           gparams, loss_sum, dy_out);
+    }
+    return check_launch("train_fused");
+}
+
+}  // namespace pg
+
+extern "C" int pg_train_fused_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
+                                  const float *targets, int64_t B, const float *feats,
+                                  const uint8_t *baked, const float *conf, const float *params,
+                                  float scale, unsigned flags, float *gfeat, float *gconf,
+                                  uint8_t *touched, float *gparams, double *loss_sum, float *dy_out,
+                                  void *stream) {
+    return pg::train_fused(grid, mlp, xs, targets, B, feats, baked, conf, params, scale, flags, gfeat,
+                           gconf, touched, gparams, loss_sum, dy_out, pg::as_stream(stream));
+}

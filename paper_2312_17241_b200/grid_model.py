@@ -5,7 +5,7 @@ HBM layout — one allocation per role so each optimizer pass is one launch and
 the data-parallel gradient exchange is one buffer:
 
     dense   [ feats (L, n_f, F) | mlp (W0, b0, W1, b1, ...) ]      float32/64
-    grads   [ gfeats | gmlp | gconf (P, n_c, N_p) | touched-as-float (P*n_c) ]
+    grads   [ gfeats | gmlp | pad | gconf (P, n_c, N_p) | pad | touched-as-float (P*n_c) ]
     conf    (P, n_c, N_p)  confidences of the P probed levels, slot order
     baked   (P, n_c)       uint8 argmax probe per row
     touched (P*n_c)        uint8 rows looked up since the last optimizer step
@@ -97,9 +97,13 @@ class Model:
         self.n_dense = self.n_feat + self.n_mlp
         self.n_conf = P * h.n_c * h.n_p
         self.n_rows = P * h.n_c
+        # section starts padded to 64 elements: the scatter kernels issue
+        # 16-byte vector reductions into gconf rows (red.global.add.v4.f32)
+        self.off_gconf = -(-self.n_dense // 64) * 64
+        self.off_touched = -(-(self.off_gconf + self.n_conf) // 64) * 64
         kw = dict(dtype=self.tdtype, device=self.device)
         self.dense = torch.zeros(self.n_dense, **kw)
-        self.grads = torch.zeros(self.n_dense + self.n_conf + self.n_rows, **kw)
+        self.grads = torch.zeros(self.off_touched + self.n_rows, **kw)
         self.conf = torch.zeros((P, h.n_c, h.n_p), **kw)
         self.baked = torch.zeros((P, h.n_c), dtype=torch.uint8, device=self.device)
         self.touched = torch.zeros(self.n_rows, dtype=torch.uint8, device=self.device)
@@ -132,11 +136,11 @@ class Model:
     @property
     def gconf(self):
         h = self.hyper
-        return self.grads[self.n_dense:self.n_dense + self.n_conf].view(len(self.probed), h.n_c, h.n_p)
+        return self.grads[self.off_gconf:self.off_gconf + self.n_conf].view(len(self.probed), h.n_c, h.n_p)
 
     @property
     def touched_f(self):
-        return self.grads[self.n_dense + self.n_conf:]
+        return self.grads[self.off_touched:]
 
     def _mlp_views(self, flat):
         out_w, out_b, off = [], [], 0

@@ -88,7 +88,8 @@ def adam_update(param: torch.Tensor, grad: torch.Tensor, slot: AdamSlot, t: int,
 class TrainState:
     """Optimizer state bound to one device model; drives individual steps."""
 
-    def __init__(self, model: Model, image, cfg: TrainConfig, sampler: str = "reference"):
+    def __init__(self, model: Model, image, cfg: TrainConfig, sampler: str = "reference",
+                 fused: bool | None = None):
         cfg.validate()
         if sampler not in ("reference", "device"):
             raise InvalidHyperparameter(f"unknown sampler {sampler!r}")
@@ -110,15 +111,22 @@ class TrainState:
         self.cm = torch.zeros_like(model.conf)
         self.cv = torch.zeros_like(model.conf)
         B, h = cfg.batch_size, model.hyper
+        w = model.widths
+        self.fused = (model.tdtype == torch.float32 and h.feature_dim == 2 and h.n_levels == 16
+                      and h.n_p <= 16 and len(w) == 4 and w[1] == 64 and w[2] == 64
+                      and w[3] <= 4)
         self.pix_host = torch.empty(B, dtype=torch.int64, pin_memory=True)
         self.pix_copied = torch.cuda.Event()
         self.pix = torch.empty(B, dtype=torch.int64, device=dev)
         self.xs = torch.empty((B, 2), dtype=tdt, device=dev)
         self.targets = torch.empty((B, h.out_dim), dtype=tdt, device=dev)
-        self.y = torch.empty((B, h.encoded_width), dtype=tdt, device=dev)
-        self.dy = torch.empty_like(self.y)
-        nws = int(_lib.lib().pg_mlp_train_workspace_floats(B, model.mlp_desc))
-        self.ws = torch.empty(max(nws, 1), dtype=tdt, device=dev)
+        if fused is not None:
+            self.fused = self.fused and bool(fused)
+        if not self.fused:
+            self.y = torch.empty((B, h.encoded_width), dtype=tdt, device=dev)
+            self.dy = torch.empty_like(self.y)
+            nws = int(_lib.lib().pg_mlp_train_workspace_floats(B, model.mlp_desc))
+            self.ws = torch.empty(max(nws, 1), dtype=tdt, device=dev)
         self.loss_sum = torch.zeros(1, dtype=torch.float64, device=dev)
         self.loss_host = torch.zeros(1, dtype=torch.float64, pin_memory=True)
         self.scale = 2.0 / (B * h.out_dim)   # trainer.py:134, cast to the model dtype
@@ -150,16 +158,33 @@ class TrainState:
         s = _lib.stream_ptr()
         sfx = "f64" if m.tdtype == torch.float64 else "f32"
         xs, targets = self.sample_batch()
-        encode_forward_device(m, xs, self.y)
         self.loss_sum.zero_()
-        flags = _lib.PG_SIGMOID if m.hyper.out_sigmoid else 0
-        _lib.call(f"pg_mlp_train_{sfx}", m.mlp_desc, _lib.ptr(self.y), _lib.ptr(targets),
-                  cfg.batch_size, _lib.ptr(m.mlp_params), float(np.dtype(m.dtype).type(self.scale)),
-                  flags, _lib.ptr(m.gmlp), _lib.ptr(self.dy), _lib.ptr(self.loss_sum),
-                  _lib.ptr(self.ws), s)
-        encode_backward_device(m, xs, self.dy)
+        self.compute_grads(xs, targets)
         self.t += 1
         self.apply_updates()
+
+    def compute_grads(self, xs, targets, dy_out=None) -> None:
+        """Forward + backward of one batch into model.grads / touched /
+        loss_sum: the fused single-kernel path when the shape allows it, else
+        fused encode kernels around the generic MLP kernels."""
+        m, cfg, s = self.model, self.cfg, _lib.stream_ptr()
+        flags = _lib.PG_SIGMOID if m.hyper.out_sigmoid else 0
+        scale = float(np.dtype(m.dtype).type(self.scale))
+        if self.fused:
+            _lib.call("pg_train_fused_f32", m.grid, m.mlp_desc, _lib.ptr(xs), _lib.ptr(targets),
+                      xs.shape[0], _lib.ptr(m.feats), _lib.ptr(m.baked), _lib.ptr(m.conf),
+                      _lib.ptr(m.mlp_params), scale, flags, _lib.ptr(m.gfeats), _lib.ptr(m.gconf),
+                      _lib.ptr(m.touched), _lib.ptr(m.gmlp), _lib.ptr(self.loss_sum),
+                      _lib.ptr(dy_out), s)
+            return
+        sfx = "f64" if m.tdtype == torch.float64 else "f32"
+        encode_forward_device(m, xs, self.y)
+        _lib.call(f"pg_mlp_train_{sfx}", m.mlp_desc, _lib.ptr(self.y), _lib.ptr(targets),
+                  xs.shape[0], _lib.ptr(m.mlp_params), scale, flags, _lib.ptr(m.gmlp),
+                  _lib.ptr(self.dy), _lib.ptr(self.loss_sum), _lib.ptr(self.ws), s)
+        if dy_out is not None:
+            dy_out.copy_(self.dy)
+        encode_backward_device(m, xs, self.dy)
 
     def apply_updates(self) -> None:
         """Dense Adam over [features | MLP] and lazy Adam + re-bake over the
