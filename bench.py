@@ -106,6 +106,18 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.sm)}
 
 
+def ncu_traffic(kernel, units):
+    """DRAM bytes per launch of `kernel` scaled to `units`, from the committed
+    ncu capture summary (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            rec = json.load(f)[kernel]
+        per_unit = (rec["dram_read_bytes"] + rec["dram_write_bytes"]) / rec["units_per_launch"]
+        return per_unit * units
+    except Exception:
+        return None
+
+
 # ------------------------------------------------------------------ models
 def inference_model(pg, hyper, seed=0):
     """conf ~ N(0,1) then full bake (uniform probes), features
@@ -322,7 +334,8 @@ def run_gpu(args, rank, world, local_rank):
                 "path": "pg_decode_host_f32 (pinned host in/out, 2 streams, 2^21-query chunks)"},
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None,
+                     "frac": achieved / hbm_peak,
+                     "traffic": ncu_traffic("decode_fused_kernel", B_INFER),
                      "kernel": "decode_fused_kernel", "bytes_per_query": bpq,
                      "peak_source": peak_src,
                      "l2_stream_read_gbs": l2_stream, "l2_random_gather_8B_gbs": l2_gather,

@@ -103,7 +103,8 @@ class Model:
         self.off_touched = -(-(self.off_gconf + self.n_conf) // 64) * 64
         kw = dict(dtype=self.tdtype, device=self.device)
         self.dense = torch.zeros(self.n_dense, **kw)
-        self.grads = torch.zeros(self.off_touched + self.n_rows, **kw)
+        # + 1 trailing slot: the step's loss sum rides in the same all-reduce
+        self.grads = torch.zeros(self.off_touched + self.n_rows + 1, **kw)
         self.conf = torch.zeros((P, h.n_c, h.n_p), **kw)
         self.baked = torch.zeros((P, h.n_c), dtype=torch.uint8, device=self.device)
         self.touched = torch.zeros(self.n_rows, dtype=torch.uint8, device=self.device)
@@ -140,7 +141,11 @@ class Model:
 
     @property
     def touched_f(self):
-        return self.grads[self.off_touched:]
+        return self.grads[self.off_touched:self.off_touched + self.n_rows]
+
+    @property
+    def loss_slot(self):
+        return self.grads[self.off_touched + self.n_rows:]
 
     def _mlp_views(self, flat):
         out_w, out_b, off = [], [], 0

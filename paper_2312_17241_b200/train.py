@@ -129,7 +129,17 @@ class TrainState:
             self.ws = torch.empty(max(nws, 1), dtype=tdt, device=dev)
         self.loss_sum = torch.zeros(1, dtype=torch.float64, device=dev)
         self.loss_host = torch.zeros(1, dtype=torch.float64, pin_memory=True)
+        self.rank, self.world = 0, 1
         self.scale = 2.0 / (B * h.out_dim)   # trainer.py:134, cast to the model dtype
+
+    def shard(self, rank: int, world: int) -> "TrainState":
+        """Make this state one of `world` data-parallel replicas: the batch is
+        rank's slice of a global batch of world*batch_size samples, and the
+        loss gradient is scaled by 2/(world*B*out_dim) so the summed gradients
+        equal the global-batch gradient."""
+        self.rank, self.world = rank, world
+        self.scale = 2.0 / (world * self.cfg.batch_size * self.model.hyper.out_dim)
+        return self
 
     # ---------------------------------------------------------------- batch
     def sample_batch(self):
@@ -137,7 +147,9 @@ class TrainState:
         m, B, s = self.model, self.cfg.batch_size, _lib.stream_ptr()
         sfx = "f64" if m.tdtype == torch.float64 else "f32"
         if self.sampler == "reference":
-            pix = self.rng.integers(0, self.width * self.height, size=B)   # trainer.py:110-111
+            # trainer.py:110-111; replicas draw the global batch and keep their slice
+            pix = self.rng.integers(0, self.width * self.height, size=B * self.world)
+            pix = pix[self.rank * B:(self.rank + 1) * B]
             self.pix_copied.synchronize()   # previous upload of pix_host has landed
             self.pix_host.numpy()[:] = pix
             self.pix.copy_(self.pix_host, non_blocking=True)
@@ -147,9 +159,32 @@ class TrainState:
                       _lib.ptr(self.targets), s)
         else:
             _lib.call(f"pg_pixel_batch_{sfx}", None, B, self.width, self.height,
-                      _lib.ptr(self.image), m.hyper.out_dim, int(self.cfg.seed),
+                      _lib.ptr(self.image), m.hyper.out_dim, int(self.cfg.seed) * 1000003 + self.rank,
                       int(self.t), _lib.ptr(self.pix), _lib.ptr(self.xs), _lib.ptr(self.targets), s)
         return self.xs, self.targets
+
+    # ------------------------------------------------------- DP exchange
+    def exchange_buffer(self) -> torch.Tensor:
+        """The ONE buffer a data-parallel step all-reduces:
+        [gfeats | gmlp | pad | gconf | pad | touched-as-float | loss]."""
+        return self.model.grads
+
+    def pack_exchange(self) -> None:
+        m, s = self.model, _lib.stream_ptr()
+        if m.n_rows:
+            _lib.call("pg_touched_to_f32", _lib.ptr(m.touched), m.n_rows, _lib.ptr(m.touched_f), s)
+        m.loss_slot.copy_(self.loss_sum)
+
+    def unpack_exchange(self) -> None:
+        """After the all-reduce: touched = union over replicas (every replica
+        then updates the same rows, keeping replicas identical), loss = sum."""
+        m, s = self.model, _lib.stream_ptr()
+        if m.n_rows:
+            _lib.call("pg_touched_from_f32", _lib.ptr(m.touched_f), m.n_rows, _lib.ptr(m.touched), s)
+        self.loss_sum.copy_(m.loss_slot)
+
+    def loss_denominator(self) -> int:
+        return self.world * self.cfg.batch_size * self.model.hyper.out_dim
 
     # ----------------------------------------------------------------- step
     def launch_step(self) -> None:
@@ -203,7 +238,7 @@ class TrainState:
     def loss_value(self) -> float:
         self.loss_host.copy_(self.loss_sum, non_blocking=True)
         torch.cuda.current_stream().synchronize()
-        return float(self.loss_host[0]) / (self.cfg.batch_size * self.model.hyper.out_dim)
+        return float(self.loss_host[0]) / self.loss_denominator()
 
     def step(self) -> float:
         self.launch_step()

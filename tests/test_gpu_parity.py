@@ -253,7 +253,9 @@ def test_train_step_parity_c1():
     #           OpenBLAS and Adam amplifies that on ~zero-gradient weights ->
     #           the reference's own cross-backend spread is the bar.
     lr = 1e-2
-    for t, (conf_bar, baked_bar) in enumerate([(0.01, 0.002), (0.15, 0.05), (0.15, 0.05)], 1):
+    # measured (B200): step 1 <= 0.01% of confidences outside 1e-5, 0 baked
+    # differences; step 3 up to ~15% of confidences, baked <= 0.01%.
+    for t, (conf_bar, baked_bar) in enumerate([(0.002, 0.0005), (0.2, 0.002), (0.2, 0.002)], 1):
         loss, oloss = st.step(), ost.step()
         assert abs(loss - oloss) <= 1e-5 * oloss
         feats = st.model.feats.cpu().numpy()
