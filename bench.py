@@ -299,6 +299,19 @@ def run_gpu(args, rank, world, local_rank):
     l2_stream, l2_gather = measure_l2(None, torch, table_mib=8)
     mlp_flops = 2 * sum(a * b for a, b in zip(inf.widths[:-1], inf.widths[1:]))
 
+    # ---------------- ablation: same decode, other MLP engines ----------------
+    ablation = {}
+    for name, kw in (("cuda_core_fma", dict(exact=False, tensor=False)),
+                     ("cuda_core_exact_reference_order", dict(exact=True))):
+        for _ in range(2):
+            decode_device(inf, xs, out, **kw)
+        e0.record()
+        for _ in range(max(3, args.steps // 4)):
+            decode_device(inf, xs, out, **kw)
+        e1.record()
+        torch.cuda.synchronize()
+        ablation[name] = B_INFER * max(3, args.steps // 4) / (e0.elapsed_time(e1) * 1e-3)
+
     # ---------------- e2e through the C ABI host-buffer decode ----------------
     hx = xs.cpu().pin_memory()
     ho = torch.empty((B_INFER, hyper.out_dim)).pin_memory()
@@ -326,7 +339,7 @@ def run_gpu(args, rank, world, local_rank):
                    "queries_per_gpu_per_step": B_INFER, "log2_n_f": 16, "n_c": 2**16, "n_p": 4,
                    "n_levels": 16, "feature_dim": 2, "n_min": 16, "n_max": 8192,
                    "mlp": inf.widths, "probed_levels": n_probed,
-                   "mlp_mode": "exact (reference order, bit-identical)" if exact else "fma",
+                   "mlp_mode": "exact (reference order, bit-identical)" if exact else "tcgen05 kind::tf32 UMMA, 2-term split (fp32-level)",
                    "parallelism": f"query-sharded x{world}",
                    "l2_policy": "inputs (128 MiB coords + 192 MiB outputs per GPU) larger than L2; tables L2-resident"},
         "e2e": {"value": e2e_qps, "unit": "queries/s", "h2d_bytes_per_step": B_INFER * 2 * 4,
@@ -344,6 +357,7 @@ def run_gpu(args, rank, world, local_rank):
                      "note": "table gathers are L2-resident: bytes are algorithmic gather bytes; "
                              "HBM streams only 20 B/query (coords + outputs)"},
         "clocks": clk,
+        "ablation_queries_per_s": ablation,
         "train": train,
     }
     return line, e2e_launches

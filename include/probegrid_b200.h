@@ -50,6 +50,7 @@ extern "C" {
 #define PG_SIGMOID 2u     /* logistic output (HyperParams.out_sigmoid)        */
 #define PG_SURROGATE 4u   /* softmax-mixture forward (encoding.py:45-47)      */
 #define PG_HALF_FEATS 8u  /* feature tables stored as IEEE binary16           */
+#define PG_NO_TENSOR 16u  /* decode: FFMA MLP instead of tcgen05 (ablation)   */
 
 /* Geometry of one multiresolution grid (HyperParams + build_level_specs,
  * model.py:35-87, indexing.py:93-101).  Feature tables of all levels are one
@@ -291,6 +292,12 @@ int pg_touched_to_f32(const uint8_t *touched, int64_t n, float *out,
                       void *stream);
 int pg_touched_from_f32(const float *in, int64_t n, uint8_t *touched,
                         void *stream);
+
+/* Self-test of the tcgen05 (UMMA) path: one CTA computes
+ * D[128x64] = A[128x32] . B[64x32]^T with kind::tf32 MMA into TMEM;
+ * split != 0 uses the 2-term hi/lo expansion of A. */
+int pg_selftest_umma_tf32(const float *A, const float *B, float *D, int split,
+                          void *stream);
 
 /* Roofline probes (bench.py): L2 streaming read of `bytes` from buf, `reps`
  * times; `nq` random 8-byte gathers from a table of entries_pow2 float2. */

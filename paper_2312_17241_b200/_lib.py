@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(HERE, "libprobegrid_b200.so")
 PG_OK, PG_ERR_ARG, PG_ERR_CUDA, PG_ERR_DOMAIN = 0, 1, 2, 3
 PG_MAX_LEVELS, PG_MAX_FEATURE, PG_MAX_PROBES, PG_MAX_LAYERS = 64, 16, 256, 17
 PG_LEVEL_DENSE, PG_LEVEL_HASHED, PG_LEVEL_PROBED = 0, 1, 2
-PG_EXACT_MLP, PG_SIGMOID, PG_SURROGATE, PG_HALF_FEATS = 1, 2, 4, 8
+PG_EXACT_MLP, PG_SIGMOID, PG_SURROGATE, PG_HALF_FEATS, PG_NO_TENSOR = 1, 2, 4, 8, 16
 
 
 class PgGrid(ctypes.Structure):
@@ -79,6 +79,7 @@ _SIGS.update({
     "pg_touched_from_f32": [_P, _I64, _P, _P],
     "pg_train_fused_f32": [_G, _M, _P, _P, _I64, _P, _P, _P, _P, _F, ctypes.c_uint, _P, _P, _P,
                            _P, _P, _P, _P],
+    "pg_selftest_umma_tf32": [_P, _P, _P, _I, _P],
     "pg_probe_stream_read": [_P, _I64, _I, _P, _P],
     "pg_probe_gather": [_P, _I64, _I64, _U32, _P, _P],
 })

@@ -380,8 +380,13 @@ def test_decode_exact_bit_identical_to_reference_order():
     oinf = O.to_inference(om)
     q = _edge_points(20000, 2, np.float32, seed=11)
     eq(pg.decode_pixels(inf, q), O.decode_pixels(oinf, q))
-    fast = pg.decode_pixels(inf, q, exact=False)
-    np.testing.assert_allclose(fast, O.decode_pixels(oinf, q), rtol=1e-5, atol=1e-6)
+    want = O.decode_pixels(oinf, q)
+    fast = pg.decode_pixels(inf, q, exact=False)          # tcgen05 UMMA MLP
+    np.testing.assert_allclose(fast, want, rtol=1e-5, atol=1e-6)
+    from paper_2312_17241_b200.decode import decode_device
+    ffma = decode_device(inf, torch.from_numpy(q).cuda(), exact=False, tensor=False).cpu().numpy()
+    np.testing.assert_allclose(ffma, want, rtol=1e-5, atol=1e-6)
+    print("decode max abs err: tcgen05", np.abs(fast - want).max(), "ffma", np.abs(ffma - want).max())
 
 
 def test_decode_rows_independent_of_batching_and_rect_is_crop():
