@@ -296,7 +296,7 @@ def run_gpu(args, rank, world, local_rank):
     n_probed = len(inf.probed)
     bpq = infer_bytes_per_query(hyper, n_probed, table_bytes_per_row=2 * hyper.feature_dim)
     achieved = B_INFER * bpq / (ms_step * 1e-3) / 1e9    # per GPU, per launch
-    l2_stream, l2_gather = measure_l2(None, torch, table_mib=8)
+    l2_stream, l2_gather = measure_l2(None, torch, table_mib=32)
     mlp_flops = 2 * sum(a * b for a, b in zip(inf.widths[:-1], inf.widths[1:]))
 
     # ---------------- ablation: same decode, other MLP engines ----------------

@@ -42,12 +42,15 @@ int pg_device_sm_count(int device) {
 namespace pg {
 __global__ void probe_stream_kernel(const float4 *__restrict__ buf, int64_t n4, int reps,
                                     float *__restrict__ sink) {
+    // 4 independent 16-byte L2 loads in flight per thread per iteration
     float acc = 0.0f;
+    // (n4 must be a multiple of 4: bytes a multiple of 64)
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
     for (int r = 0; r < reps; ++r)
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
-             i += (int64_t)gridDim.x * blockDim.x) {
-            const float4 v = __ldcg(buf + i);
-            acc += v.x + v.y + v.z + v.w;
+        for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < n4; i += stride) {
+            const float4 a = __ldcg(buf + i), b = __ldcg(buf + i + 1);
+            const float4 c = __ldcg(buf + i + 2), d = __ldcg(buf + i + 3);
+            acc += (a.x + b.y) + (c.z + d.w);
         }
     if (acc == 12345.678f) *sink = acc;
 }

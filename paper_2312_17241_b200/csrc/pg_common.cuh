@@ -136,14 +136,17 @@ template <> struct Feat<__half> {
 };
 
 // ------------------------------------------------------ vector reductions
-// sm_90+ vector float reductions straight into L2 (REDG.E.ADD.F32x4).
+// sm_90+ vector float reductions straight into L2 (REDG.E.ADD.F32x4).  No
+// "memory" clobber on purpose: the gradient buffers they target are never
+// read by the issuing kernels, so loads may be scheduled across them (a
+// clobber would serialise every corner's L2 round trip behind the previous
+// corner's reductions).  Kernel boundaries order them for later readers.
 __device__ __forceinline__ void red_add_v4(float *p, float a, float b, float c, float d) {
     asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
-                 "f"(d)
-                 : "memory");
+                 "f"(d));
 }
 __device__ __forceinline__ void red_add_v2(float *p, float a, float b) {
-    asm volatile("red.global.add.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(a), "f"(b) : "memory");
+    asm volatile("red.global.add.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(a), "f"(b));
 }
 __device__ __forceinline__ void red_add(float *p, float a) { atomicAdd(p, a); }
 __device__ __forceinline__ void red_add(double *p, double a) { atomicAdd(p, a); }

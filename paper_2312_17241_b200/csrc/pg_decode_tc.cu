@@ -105,16 +105,22 @@ __global__ void __launch_bounds__(tc::kThreads, 2)
             float x[D];
 #pragma unroll
             for (int a = 0; a < D; ++a) x[a] = S.xs[q * D + a];
+            // a thread encodes level PAIRS (2P, 2P+1): their 4 features fill one
+            // 16-byte K-chunk, so the operand stores are float4 and a warp's
+            // 32 queries hit 4 full wavefronts (no bank conflicts)
 #pragma unroll 2
-            for (int it = 0; it < 8; ++it) {
-                const int l = lsub + 2 * it;  // warp-uniform
-                const float2 y = encode_level_fwd2<FT, D>(g, l, x, feats, baked);
-                float h0, l0, h1, l1;
-                umma::split_tf32(y.x, h0, l0);
-                umma::split_tf32(y.y, h1, l1);
-                const uint32_t off = umma::kmaj_off(q, 2 * l, kTP);
-                *reinterpret_cast<float2 *>(opA + off) = make_float2(h0, h1);
-                *reinterpret_cast<float2 *>(opA + kTP * kIn * 4 + off) = make_float2(l0, l1);
+            for (int it = 0; it < 4; ++it) {
+                const int P = lsub + 2 * it;  // warp-uniform
+                const float2 ya = encode_level_fwd2<FT, D>(g, 2 * P, x, feats, baked);
+                const float2 yb = encode_level_fwd2<FT, D>(g, 2 * P + 1, x, feats, baked);
+                float h[4], lo[4];
+                umma::split_tf32(ya.x, h[0], lo[0]);
+                umma::split_tf32(ya.y, h[1], lo[1]);
+                umma::split_tf32(yb.x, h[2], lo[2]);
+                umma::split_tf32(yb.y, h[3], lo[3]);
+                const uint32_t off = umma::kmaj_off(q, 4 * P, kTP);
+                *reinterpret_cast<float4 *>(opA + off) = make_float4(h[0], h[1], h[2], h[3]);
+                *reinterpret_cast<float4 *>(opA + kTP * kIn * 4 + off) = make_float4(lo[0], lo[1], lo[2], lo[3]);
             }
         }
         umma::fence_async_smem();

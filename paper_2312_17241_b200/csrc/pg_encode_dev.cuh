@@ -61,6 +61,10 @@ __device__ __forceinline__ float2 encode_level_fwd2(const pg_grid &g, int l, con
 // Backward for one (point, level), F = 2, fp32: scatter w*up into the
 // feature-gradient table (all N_p probes, softmax-weighted, for probed
 // levels), the softmax-Jacobian term into gconf, and flag the row touched.
+template <int NPMAX>
+__device__ __forceinline__ void encode_probe_reds(float *gb, float *gc, int n_p, const float (&sg)[NPMAX],
+                                                  const float (&dots)[NPMAX], float s, float g0, float g1);
+
 template <int D, int NPMAX>
 __device__ __forceinline__ void encode_level_bwd2(const pg_grid &g, int l, const float (&x)[D],
                                                   float up0, float up1,
@@ -82,46 +86,94 @@ __device__ __forceinline__ void encode_level_bwd2(const pg_grid &g, int l, const
     }
     float *gtab = gfeat + (int64_t)l * g.n_f * 2;
     const float *ftab = feats + (int64_t)l * g.n_f * 2;
+    float wk[C];
 #pragma unroll
-    for (int k = 0; k < C; ++k) {
-        const float w = corner_weight<float, D>(k, t, omt);
-        const float g0 = __fmul_rn(w, up0), g1 = __fmul_rn(w, up1);
-        if (kind != PG_LEVEL_PROBED) {
+    for (int k = 0; k < C; ++k) wk[k] = corner_weight<float, D>(k, t, omt);
+    if (kind != PG_LEVEL_PROBED) {
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
             const int lin = kind == PG_LEVEL_DENSE ? corner_dense<D>(k, c, res + 1)
                                                    : (int)(corner_hash<D>(k, c, g.primary) & nf_mask);
-            red_add_v2(gtab + (int64_t)lin * 2, g0, g1);
-            continue;
+            red_add_v2(gtab + (int64_t)lin * 2, __fmul_rn(wk[k], up0), __fmul_rn(wk[k], up1));
         }
-        const int bs = (int)((corner_hash<D>(k, c, g.primary) << g.log2_np) & nf_mask);
-        const int r = (int)(corner_hash<D>(k, c, g.aux) & nc_mask);
-        const int64_t crow = (int64_t)g.slot[l] * g.n_c + r;
-        touched[crow] = 1;
-        const float *cr = conf + crow * n_p;
-        float *gc = gconf + crow * n_p;
-        const float *fb = ftab + (int64_t)bs * 2;
-        float *gb = gtab + (int64_t)bs * 2;
-        float sg[NPMAX], dots[NPMAX];
-        float mx = cr[0];
+        return;
+    }
+    // Probed: resolve every corner's probing range and confidence row first
+    // and issue ALL their loads before any arithmetic or reduction, so the
+    // 2^d corners' L2 round trips overlap instead of serialising.
+    constexpr int PF = NPMAX <= 4 ? 2 : 1;  // corners prefetched together
+    int bs[C];
+    int64_t crow[C];
 #pragma unroll
-        for (int j = 1; j < NPMAX; ++j)
-            if (j < n_p) mx = fmaxf(mx, cr[j]);
-        float sum = 0.0f;
+    for (int k = 0; k < C; ++k) {
+        bs[k] = (int)((corner_hash<D>(k, c, g.primary) << g.log2_np) & nf_mask);
+        crow[k] = (int64_t)g.slot[l] * g.n_c + (int)(corner_hash<D>(k, c, g.aux) & nc_mask);
+    }
 #pragma unroll
-        for (int j = 0; j < NPMAX; ++j)
-            if (j < n_p) {
-                sg[j] = expf(cr[j] - mx);
-                sum += sg[j];
+    for (int k0 = 0; k0 < C; k0 += PF) {
+        float cv[PF][NPMAX], fv[PF][NPMAX][2];
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+            const float *cr = conf + crow[k0 + u] * n_p;
+            const float2 *fb = reinterpret_cast<const float2 *>(ftab + (int64_t)bs[k0 + u] * 2);
+            if (NPMAX == 4 && n_p == 4) {
+                const float4 c4 = __ldg(reinterpret_cast<const float4 *>(cr));
+                const float4 f01 = __ldg(reinterpret_cast<const float4 *>(fb));
+                const float4 f23 = __ldg(reinterpret_cast<const float4 *>(fb) + 1);
+                cv[u][0] = c4.x; cv[u][1 % NPMAX] = c4.y; cv[u][2 % NPMAX] = c4.z; cv[u][3 % NPMAX] = c4.w;
+                fv[u][0][0] = f01.x; fv[u][0][1] = f01.y; fv[u][1 % NPMAX][0] = f01.z; fv[u][1 % NPMAX][1] = f01.w;
+                fv[u][2 % NPMAX][0] = f23.x; fv[u][2 % NPMAX][1] = f23.y;
+                fv[u][3 % NPMAX][0] = f23.z; fv[u][3 % NPMAX][1] = f23.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < NPMAX; ++j)
+                    if (j < n_p) {
+                        cv[u][j] = __ldg(cr + j);
+                        const float2 f = __ldg(fb + j);
+                        fv[u][j][0] = f.x;
+                        fv[u][j][1] = f.y;
+                    }
             }
-        const float inv = 1.0f / sum;
-        float s = 0.0f;
+        }
 #pragma unroll
-        for (int j = 0; j < NPMAX; ++j)
-            if (j < n_p) {
-                sg[j] *= inv;
-                const float2 f = __ldg(reinterpret_cast<const float2 *>(fb) + j);
-                dots[j] = f.x * g0 + f.y * g1;
-                s += sg[j] * dots[j];
-            }
+        for (int u = 0; u < PF; ++u) {
+            const int k = k0 + u;
+            touched[crow[k]] = 1;
+            const float g0 = __fmul_rn(wk[k], up0), g1 = __fmul_rn(wk[k], up1);
+            float *gc = gconf + crow[k] * n_p;
+            float *gb = gtab + (int64_t)bs[k] * 2;
+            float sg[NPMAX], dots[NPMAX];
+            float mx = cv[u][0];
+#pragma unroll
+            for (int j = 1; j < NPMAX; ++j)
+                if (j < n_p) mx = fmaxf(mx, cv[u][j]);
+            float sum = 0.0f;
+#pragma unroll
+            for (int j = 0; j < NPMAX; ++j)
+                if (j < n_p) {
+                    sg[j] = expf(cv[u][j] - mx);
+                    sum += sg[j];
+                }
+            const float inv = 1.0f / sum;
+            float s = 0.0f;
+#pragma unroll
+            for (int j = 0; j < NPMAX; ++j)
+                if (j < n_p) {
+                    sg[j] *= inv;
+                    dots[j] = fv[u][j][0] * g0 + fv[u][j][1] * g1;
+                    s += sg[j] * dots[j];
+                }
+            encode_probe_reds<NPMAX>(gb, gc, n_p, sg, dots, s, g0, g1);
+        }
+    }
+}
+
+// scatter of one probed corner: softmax-weighted feature grads over the
+// probing range (16-byte vector reductions) + confidence-row gradient
+template <int NPMAX>
+__device__ __forceinline__ void encode_probe_reds(float *gb, float *gc, int n_p, const float (&sg)[NPMAX],
+                                                  const float (&dots)[NPMAX], float s, float g0, float g1) {
+    {
         if (n_p >= 2) {
 #pragma unroll
             for (int j = 0; j < NPMAX; j += 2)

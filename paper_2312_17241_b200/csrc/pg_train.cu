@@ -74,7 +74,7 @@ __device__ __forceinline__ void fwd_layer(const float *__restrict__ inT, const f
     }
 }
 
-template <typename FT, int D>
+template <typename FT, int D, int NPM>
 __global__ void __launch_bounds__(kNT, 1)
     train_fused_kernel(const pg_grid g, const float *__restrict__ xs, const float *__restrict__ targets,
                        int64_t B, const FT *__restrict__ feats_fwd, const float *__restrict__ feats,
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(kNT, 1)
 #pragma unroll 1
             for (int it = 0; it < 4; ++it) {
                 const int l = lsub + 4 * it;
-                encode_level_bwd2<D, 16>(g, l, x, S.yT[sw(2 * l, pl)], S.yT[sw(2 * l + 1, pl)], feats,
+                encode_level_bwd2<D, NPM>(g, l, x, S.yT[sw(2 * l, pl)], S.yT[sw(2 * l + 1, pl)], feats,
                                          conf, gfeat, gconf, touched);
             }
         }
@@ -370,7 +370,7 @@ int train_fused(const pg_grid *g, const pg_mlp *m, const float *xs, const float 
     PG_REQUIRE(train_fast_ok(g, m), "fused training needs F=2, 16 levels, N_p<=16, MLP [32,64,64,<=4]");
     if (B == 0) return PG_OK;
     const int smem = (int)sizeof(TrainSmem);
-    static bool configured[2] = {false, false};
+    static bool configured[4] = {false, false, false, false};
     const int od = m->widths[3];
     const int sig = (flags & PG_SIGMOID) ? 1 : 0;
     int sms = 0, dev = 0;
@@ -378,23 +378,25 @@ int train_fused(const pg_grid *g, const pg_mlp *m, const float *xs, const float 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t ntiles = (B + kT - 1) / kT;
     const int grd = (int)(ntiles < sms ? ntiles : sms);
+    const bool np4 = g->log2_np <= 2;
+#define PG_TRAIN_LAUNCH(D_, NP_, IDX)                                                                 \
+    do {                                                                                              \
+        if (!configured[IDX]) {                                                                       \
+            cudaFuncSetAttribute(train_fused_kernel<float, D_, NP_>,                                  \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                 \
+            configured[IDX] = true;                                                                   \
+        }                                                                                             \
+        train_fused_kernel<float, D_, NP_><<<grd, kNT, smem, s>>>(*g, xs, targets, B, feats, feats,  \
+                                                                 baked, conf, params, od, scale, sig, \
+                                                                 gfeat, gconf, touched, gparams,      \
+                                                                 loss_sum, dy_out);                   \
+    } while (0)
     if (g->d == 2) {
-        if (!configured[0]) {
-            cudaFuncSetAttribute(train_fused_kernel<float, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            configured[0] = true;
-        }
-        train_fused_kernel<float, 2><<<grd, kNT, smem, s>>>(*g, xs, targets, B, feats, feats, baked, conf,
-                                                           params, od, scale, sig, gfeat, gconf, touched,
-                                                           gparams, loss_sum, dy_out);
+        if (np4) PG_TRAIN_LAUNCH(2, 4, 0); else PG_TRAIN_LAUNCH(2, 16, 1);
     } else {
-        if (!configured[1]) {
-            cudaFuncSetAttribute(train_fused_kernel<float, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            configured[1] = true;
-        }
-        train_fused_kernel<float, 3><<<grd, kNT, smem, s>>>(*g, xs, targets, B, feats, feats, baked, conf,
-                                                           params, od, scale, sig, gfeat, gconf, touched,
-                                                           gparams, loss_sum, dy_out);
+        if (np4) PG_TRAIN_LAUNCH(3, 4, 2); else PG_TRAIN_LAUNCH(3, 16, 3);
     }
+#undef PG_TRAIN_LAUNCH
     return check_launch("train_fused");
 }
 
