@@ -249,6 +249,35 @@ int pg_train_fused_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
                        float *gparams, double *loss_sum, float *dy_out,
                        void *stream);
 
+/* Deterministic mode.  Same passes as pg_encode_bwd_f32 / pg_mlp_train_f32 /
+ * pg_train_fused_f32, but every cross-thread sum (table scatters, weight
+ * gradients, the loss) is accumulated in 64-bit fixed point (2^-56 for
+ * gradients, range +-128; 2^-32 for the loss), which is order-independent:
+ * results are bit-identical run to run, and identical contributions give
+ * identical sums (the reference's N_p=1 probed == plain-hash equivalence,
+ * test_trainer.py:131-141).  Accumulators (uint64, zeroed by the caller the
+ * first time) use the float buffers' element layout; pg_fx_accumulate_f32
+ * adds them into the float gradients and clears them, pg_fx_loss converts
+ * the loss accumulator. */
+int pg_encode_bwd_det_f32(const pg_grid *grid, const float *xs, int64_t B,
+                          const float *dy, const float *feats,
+                          const float *conf, uint64_t *gfeat_fx,
+                          uint64_t *gconf_fx, uint8_t *touched, void *stream);
+int pg_mlp_train_det_f32(const pg_mlp *mlp, const float *y,
+                         const float *targets, int64_t B, const float *params,
+                         float scale, unsigned flags, uint64_t *gparams_fx,
+                         float *dy, uint64_t *loss_fx, float *ws, void *stream);
+int pg_train_fused_det_f32(const pg_grid *grid, const pg_mlp *mlp,
+                           const float *xs, const float *targets, int64_t B,
+                           const float *feats, const uint8_t *baked,
+                           const float *conf, const float *params, float scale,
+                           unsigned flags, uint64_t *gfeat_fx,
+                           uint64_t *gconf_fx, uint8_t *touched,
+                           uint64_t *gparams_fx, uint64_t *loss_fx,
+                           float *dy_out, void *stream);
+int pg_fx_accumulate_f32(uint64_t *fx, int64_t n, float *dst, void *stream);
+int pg_fx_loss(uint64_t *fx, double *loss_sum, void *stream);
+
 /* Pixel batch for the image trainer (trainer.py:109-116): xs from pixel
  * indices pix (host-drawn for reference parity, or drawn on device from
  * (seed, step) when pix_in is NULL and pix_out receives them), targets

@@ -79,6 +79,12 @@ _SIGS.update({
     "pg_touched_from_f32": [_P, _I64, _P, _P],
     "pg_train_fused_f32": [_G, _M, _P, _P, _I64, _P, _P, _P, _P, _F, ctypes.c_uint, _P, _P, _P,
                            _P, _P, _P, _P],
+    "pg_encode_bwd_det_f32": [_G, _P, _I64, _P, _P, _P, _P, _P, _P, _P],
+    "pg_mlp_train_det_f32": [_M, _P, _P, _I64, _P, _F, ctypes.c_uint, _P, _P, _P, _P, _P],
+    "pg_train_fused_det_f32": [_G, _M, _P, _P, _I64, _P, _P, _P, _P, _F, ctypes.c_uint, _P, _P,
+                               _P, _P, _P, _P, _P],
+    "pg_fx_accumulate_f32": [_P, _I64, _P, _P],
+    "pg_fx_loss": [_P, _P, _P],
     "pg_selftest_umma_tf32": [_P, _P, _P, _I, _P],
     "pg_probe_stream_read": [_P, _I64, _I, _P, _P],
     "pg_probe_gather": [_P, _I64, _I64, _U32, _P, _P],

@@ -151,6 +151,36 @@ __device__ __forceinline__ void red_add_v2(float *p, float a, float b) {
 __device__ __forceinline__ void red_add(float *p, float a) { atomicAdd(p, a); }
 __device__ __forceinline__ void red_add(double *p, double a) { atomicAdd(p, a); }
 
+// ------------------------------------------------ deterministic accumulation
+// Deterministic mode (PG_DETERMINISTIC) accumulates every cross-thread sum in
+// 64-bit fixed point: integer addition is associative, so the result does not
+// depend on the order the GPU happens to schedule the adds.  Gradients use
+// 2^-56 resolution (range +-128), loss sums 2^-32 (range +-2^31).
+typedef unsigned long long fx_t;
+#define PG_FX_SHIFT 56
+#define PG_FX_LOSS_SHIFT 32
+__device__ __forceinline__ fx_t to_fx(double v, int shift) {
+    return (fx_t)__double2ll_rn(ldexp(v, shift));
+}
+__device__ __forceinline__ void red_add(fx_t *p, float a) {
+    atomicAdd(p, to_fx((double)a, PG_FX_SHIFT));
+}
+__device__ __forceinline__ void red_add(fx_t *p, double a) {
+    atomicAdd(p, to_fx(a, PG_FX_SHIFT));
+}
+__device__ __forceinline__ void red_add_v4(fx_t *p, float a, float b, float c, float d) {
+    red_add(p, a);
+    red_add(p + 1, b);
+    red_add(p + 2, c);
+    red_add(p + 3, d);
+}
+__device__ __forceinline__ void red_add_v2(fx_t *p, float a, float b) {
+    red_add(p, a);
+    red_add(p + 1, b);
+}
+__device__ __forceinline__ void loss_add(double *p, double v) { atomicAdd(p, v); }
+__device__ __forceinline__ void loss_add(fx_t *p, double v) { atomicAdd(p, to_fx(v, PG_FX_LOSS_SHIFT)); }
+
 // ------------------------------------------------------- level table
 struct LevelTab {
     int res[PG_MAX_LEVELS];

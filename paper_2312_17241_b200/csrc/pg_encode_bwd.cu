@@ -15,11 +15,11 @@ constexpr int kChunk = 128;
 // Softmax uses the per-row max (the reference shifts by the global max of the
 // gathered rows, numpy_backend.py:115-131: mathematically identical).
 // =========================================================================
-template <typename T, int D, int FC, int NPMAX>
+template <typename T, int D, int FC, int NPMAX, typename ACC>
 __global__ void __launch_bounds__(256) encode_bwd_kernel(
     const pg_grid g, const T *__restrict__ xs, int64_t B, const T *__restrict__ dy,
-    const T *__restrict__ feats, const T *__restrict__ conf, T *__restrict__ gfeat,
-    T *__restrict__ gconf, uint8_t *__restrict__ touched) {
+    const T *__restrict__ feats, const T *__restrict__ conf, ACC *__restrict__ gfeat,
+    ACC *__restrict__ gconf, uint8_t *__restrict__ touched) {
     __shared__ LevelTab lt;
     const int L = g.n_levels;
     for (int i = threadIdx.x; i < L; i += blockDim.x) {
@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(256) encode_bwd_kernel(
             T up[FC ? FC : PG_MAX_FEATURE];
             const T *dyp = dy + p * (int64_t)L * F + (int64_t)l * F;
             for (int q = 0; q < F; ++q) up[q] = dyp[q];
-            T *gtab = gfeat + (int64_t)l * g.n_f * F;
+            ACC *gtab = gfeat + (int64_t)l * g.n_f * F;
             const T *ftab = feats + (int64_t)l * g.n_f * F;
 #pragma unroll(FC == 2 && NPMAX > 0 ? C : 1)
             for (int k = 0; k < C; ++k) {
@@ -60,9 +60,9 @@ __global__ void __launch_bounds__(256) encode_bwd_kernel(
                     const int lin = kind == PG_LEVEL_DENSE
                                         ? corner_dense<D>(k, c, res + 1)
                                         : (int)(corner_hash<D>(k, c, g.primary) & nf_mask);
-                    T *dst = gtab + (int64_t)lin * F;
+                    ACC *dst = gtab + (int64_t)lin * F;
                     if constexpr (FC == 2 && sizeof(T) == 4) {
-                        red_add_v2((float *)dst, gq[0], gq[1]);
+                        red_add_v2((ACC *)dst, gq[0], gq[1]);
                     } else {
                         for (int q = 0; q < F; ++q) red_add(dst + q, gq[q]);
                     }
@@ -73,9 +73,9 @@ __global__ void __launch_bounds__(256) encode_bwd_kernel(
                 const int64_t crow = (int64_t)lt.slot[l] * g.n_c + r;
                 touched[crow] = 1;
                 const T *cr = conf + crow * n_p;
-                T *gc = gconf + crow * n_p;
+                ACC *gc = gconf + crow * n_p;
                 const T *fb = ftab + (int64_t)bs * F;
-                T *gb = gtab + (int64_t)bs * F;
+                ACC *gb = gtab + (int64_t)bs * F;
                 if constexpr (NPMAX > 0) {
                     T sg[NPMAX], dots[NPMAX];
                     T mx = cr[0];
@@ -106,10 +106,10 @@ __global__ void __launch_bounds__(256) encode_bwd_kernel(
 #pragma unroll
                             for (int j = 0; j < NPMAX; j += 2)
                                 if (j < n_p)
-                                    red_add_v4((float *)gb + 2 * j, sg[j] * gq[0], sg[j] * gq[1],
+                                    red_add_v4((ACC *)gb + 2 * j, sg[j] * gq[0], sg[j] * gq[1],
                                                sg[j + 1] * gq[0], sg[j + 1] * gq[1]);
                         } else {
-                            red_add_v2((float *)gb, sg[0] * gq[0], sg[0] * gq[1]);
+                            red_add_v2((ACC *)gb, sg[0] * gq[0], sg[0] * gq[1]);
                         }
                     } else {
 #pragma unroll
@@ -122,12 +122,12 @@ __global__ void __launch_bounds__(256) encode_bwd_kernel(
 #pragma unroll
                             for (int j = 0; j < NPMAX; j += 4)
                                 if (j < n_p)
-                                    red_add_v4((float *)gc + j, sg[j] * (dots[j] - s),
+                                    red_add_v4((ACC *)gc + j, sg[j] * (dots[j] - s),
                                                sg[j + 1] * (dots[j + 1] - s),
                                                sg[j + 2] * (dots[j + 2] - s),
                                                sg[j + 3] * (dots[j + 3] - s));
                         } else if (n_p == 2) {
-                            red_add_v2((float *)gc, sg[0] * (dots[0] - s), sg[1] * (dots[1] - s));
+                            red_add_v2((ACC *)gc, sg[0] * (dots[0] - s), sg[1] * (dots[1] - s));
                         } else {
                             red_add(gc, sg[0] * (dots[0] - s));
                         }
@@ -179,9 +179,9 @@ static int encode_blocks(int64_t B) {
 }
 
 
-template <typename T>
+template <typename T, typename ACC = T>
 static int launch_encode_bwd(const pg_grid *g, const T *xs, int64_t B, const T *dy,
-                             const T *feats, const T *conf, T *gfeat, T *gconf, uint8_t *touched,
+                             const T *feats, const T *conf, ACC *gfeat, ACC *gconf, uint8_t *touched,
                              void *stream) {
     if (int e = validate_grid(g)) return e;
     bool any_probed = false;
@@ -193,7 +193,7 @@ static int launch_encode_bwd(const pg_grid *g, const T *xs, int64_t B, const T *
     const bool f2 = g->feature_dim == 2;
     const int n_p = 1 << g->log2_np;
 #define PG_ENC_BWD(D_, FC_, NP_) \
-    encode_bwd_kernel<T, D_, FC_, NP_><<<grd, 256, 0, s>>>(*g, xs, B, dy, feats, conf, gfeat, gconf, touched)
+    encode_bwd_kernel<T, D_, FC_, NP_, ACC><<<grd, 256, 0, s>>>(*g, xs, B, dy, feats, conf, gfeat, gconf, touched)
 #define PG_ENC_BWD_NP(D_, FC_)                   \
     do {                                         \
         if (FC_ == 0) PG_ENC_BWD(D_, 0, 0);       \
@@ -227,6 +227,12 @@ int pg_encode_bwd_f64(const pg_grid *grid, const double *xs, int64_t B, const do
                       const double *feats, const double *conf, double *gfeat, double *gconf,
                       uint8_t *touched, void *stream) {
     return launch_encode_bwd<double>(grid, xs, B, dy, feats, conf, gfeat, gconf, touched, stream);
+}
+int pg_encode_bwd_det_f32(const pg_grid *grid, const float *xs, int64_t B, const float *dy,
+                          const float *feats, const float *conf, uint64_t *gfeat_fx,
+                          uint64_t *gconf_fx, uint8_t *touched, void *stream) {
+    return launch_encode_bwd<float, fx_t>(grid, xs, B, dy, feats, conf, (fx_t *)gfeat_fx,
+                                          (fx_t *)gconf_fx, touched, stream);
 }
 
 }  // extern "C"

@@ -61,17 +61,18 @@ __device__ __forceinline__ float2 encode_level_fwd2(const pg_grid &g, int l, con
 // Backward for one (point, level), F = 2, fp32: scatter w*up into the
 // feature-gradient table (all N_p probes, softmax-weighted, for probed
 // levels), the softmax-Jacobian term into gconf, and flag the row touched.
-template <int NPMAX>
-__device__ __forceinline__ void encode_probe_reds(float *gb, float *gc, int n_p, const float (&sg)[NPMAX],
+// ACC = float (vector reductions into L2) or fx_t (deterministic fixed point).
+template <int NPMAX, typename ACC>
+__device__ __forceinline__ void encode_probe_reds(ACC *gb, ACC *gc, int n_p, const float (&sg)[NPMAX],
                                                   const float (&dots)[NPMAX], float s, float g0, float g1);
 
-template <int D, int NPMAX>
+template <int D, int NPMAX, typename ACC = float>
 __device__ __forceinline__ void encode_level_bwd2(const pg_grid &g, int l, const float (&x)[D],
                                                   float up0, float up1,
                                                   const float *__restrict__ feats,
                                                   const float *__restrict__ conf,
-                                                  float *__restrict__ gfeat,
-                                                  float *__restrict__ gconf,
+                                                  ACC *__restrict__ gfeat,
+                                                  ACC *__restrict__ gconf,
                                                   uint8_t *__restrict__ touched) {
     constexpr int C = 1 << D;
     const uint32_t nf_mask = (uint32_t)g.n_f - 1u, nc_mask = (uint32_t)g.n_c - 1u;
@@ -84,7 +85,7 @@ __device__ __forceinline__ void encode_level_bwd2(const pg_grid &g, int l, const
         c[a] = cell_coord(x[a], res, t[a]);
         omt[a] = __fsub_rn(1.0f, t[a]);
     }
-    float *gtab = gfeat + (int64_t)l * g.n_f * 2;
+    ACC *gtab = gfeat + (int64_t)l * g.n_f * 2;
     const float *ftab = feats + (int64_t)l * g.n_f * 2;
     float wk[C];
 #pragma unroll
@@ -140,8 +141,8 @@ __device__ __forceinline__ void encode_level_bwd2(const pg_grid &g, int l, const
             const int k = k0 + u;
             touched[crow[k]] = 1;
             const float g0 = __fmul_rn(wk[k], up0), g1 = __fmul_rn(wk[k], up1);
-            float *gc = gconf + crow[k] * n_p;
-            float *gb = gtab + (int64_t)bs[k] * 2;
+            ACC *gc = gconf + crow[k] * n_p;
+            ACC *gb = gtab + (int64_t)bs[k] * 2;
             float sg[NPMAX], dots[NPMAX];
             float mx = cv[u][0];
 #pragma unroll
@@ -163,15 +164,15 @@ __device__ __forceinline__ void encode_level_bwd2(const pg_grid &g, int l, const
                     dots[j] = fv[u][j][0] * g0 + fv[u][j][1] * g1;
                     s += sg[j] * dots[j];
                 }
-            encode_probe_reds<NPMAX>(gb, gc, n_p, sg, dots, s, g0, g1);
+            encode_probe_reds<NPMAX, ACC>(gb, gc, n_p, sg, dots, s, g0, g1);
         }
     }
 }
 
 // scatter of one probed corner: softmax-weighted feature grads over the
 // probing range (16-byte vector reductions) + confidence-row gradient
-template <int NPMAX>
-__device__ __forceinline__ void encode_probe_reds(float *gb, float *gc, int n_p, const float (&sg)[NPMAX],
+template <int NPMAX, typename ACC>
+__device__ __forceinline__ void encode_probe_reds(ACC *gb, ACC *gc, int n_p, const float (&sg)[NPMAX],
                                                   const float (&dots)[NPMAX], float s, float g0, float g1) {
     {
         if (n_p >= 2) {

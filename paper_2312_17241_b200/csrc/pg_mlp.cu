@@ -374,10 +374,10 @@ __global__ void train_linear_fwd_kernel(const T *__restrict__ a, int relu_in, in
     z[i] = Ar<T>::add(acc, bias[j]);
 }
 
-template <typename T>
+template <typename T, typename LACC>
 __global__ void train_loss_kernel(const T *__restrict__ zout, const T *__restrict__ targets,
                                   int64_t n, T scale, int sigmoid, T *__restrict__ delta,
-                                  double *__restrict__ loss_sum) {
+                                  LACC *__restrict__ loss_sum) {
     __shared__ double red[32];
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     double sq = 0.0;
@@ -398,16 +398,17 @@ __global__ void train_loss_kernel(const T *__restrict__ zout, const T *__restric
         double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (threadIdx.x == 0 && loss_sum) atomicAdd(loss_sum, v);
+        if (threadIdx.x == 0 && loss_sum) loss_add(loss_sum, v);
     }
 }
 
 // dW[k][j] += sum_b a[b][k] * delta[b][j] (k == fin -> bias row), rows split
-// over blockIdx.y in chunks, partial sums added atomically.
-template <typename T>
+// over blockIdx.y in chunks, partial sums added atomically (fixed point in
+// deterministic mode).
+template <typename T, typename ACC>
 __global__ void train_wgrad_kernel(const T *__restrict__ a, int relu_in, int64_t B, int fin,
-                                   const T *__restrict__ delta, int fout, T *__restrict__ gW,
-                                   T *__restrict__ gb, int64_t rows_per_chunk) {
+                                   const T *__restrict__ delta, int fout, ACC *__restrict__ gW,
+                                   ACC *__restrict__ gb, int64_t rows_per_chunk) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (int64_t)(fin + 1) * fout) return;
     const int k = (int)(i / fout), j = (int)(i % fout);
@@ -443,9 +444,9 @@ __global__ void train_dgrad_kernel(const T *__restrict__ delta, int64_t B, int f
     out[i] = acc;
 }
 
-template <typename T>
+template <typename T, typename ACC = T, typename LACC = double>
 int mlp_train_generic(const pg_mlp *m, const T *y, const T *targets, int64_t B, const T *params,
-                      T scale, unsigned flags, T *gparams, T *dy, double *loss_sum, T *ws,
+                      T scale, unsigned flags, ACC *gparams, T *dy, LACC *loss_sum, T *ws,
                       cudaStream_t s) {
     if (int e = validate_mlp(m)) return e;
     if (B == 0) return PG_OK;
@@ -453,7 +454,8 @@ int mlp_train_generic(const pg_mlp *m, const T *y, const T *targets, int64_t B, 
     const int nl = m->n_layers;
     const int maxw = mlp_max_width(m);
     const T *Wp[PG_MAX_LAYERS], *bp[PG_MAX_LAYERS];
-    T *gWp[PG_MAX_LAYERS], *gbp[PG_MAX_LAYERS], *z[PG_MAX_LAYERS];
+    ACC *gWp[PG_MAX_LAYERS], *gbp[PG_MAX_LAYERS];
+    T *z[PG_MAX_LAYERS];
     {
         int64_t off = 0, zoff = 0;
         for (int l = 0; l < nl; ++l) {
@@ -476,8 +478,8 @@ int mlp_train_generic(const pg_mlp *m, const T *y, const T *targets, int64_t B, 
             train_linear_fwd_kernel<T><<<grid_for(B * fo, 256), 256, 0, s>>>(a, l > 0, B, fi, Wp[l], bp[l], fo, z[l]);
         }
         const int od = m->widths[nl];
-        train_loss_kernel<T><<<grid_for(B * od, 256), 256, 0, s>>>(z[nl - 1], targets, B * od, scale,
-                                                                  (flags & PG_SIGMOID) ? 1 : 0, d0, loss_sum);
+        train_loss_kernel<T, LACC><<<grid_for(B * od, 256), 256, 0, s>>>(
+            z[nl - 1], targets, B * od, scale, (flags & PG_SIGMOID) ? 1 : 0, d0, loss_sum);
         // backward
         T *dcur = d0, *dnext = d1;
         for (int l = nl - 1; l >= 0; --l) {
@@ -485,7 +487,7 @@ int mlp_train_generic(const pg_mlp *m, const T *y, const T *targets, int64_t B, 
             const T *a = l == 0 ? y : z[l - 1];
             const int64_t chunk = 4096;
             dim3 gg(grid_for((int64_t)(fi + 1) * fo, 128), (unsigned)((B + chunk - 1) / chunk));
-            train_wgrad_kernel<T><<<gg, 128, 0, s>>>(a, l > 0, B, fi, dcur, fo, gWp[l], gbp[l], chunk);
+            train_wgrad_kernel<T, ACC><<<gg, 128, 0, s>>>(a, l > 0, B, fi, dcur, fo, gWp[l], gbp[l], chunk);
             T *dst = l > 0 ? dnext : dy;
             train_dgrad_kernel<T><<<grid_for(B * fi, 256), 256, 0, s>>>(dcur, B, fo, Wp[l], fi,
                                                                        l > 0 ? z[l - 1] : nullptr, dst);
@@ -497,12 +499,6 @@ int mlp_train_generic(const pg_mlp *m, const T *y, const T *targets, int64_t B, 
     return check_launch("mlp_train");
 }
 
-template int mlp_train_generic<float>(const pg_mlp *, const float *, const float *, int64_t,
-                                      const float *, float, unsigned, float *, float *, double *,
-                                      float *, cudaStream_t);
-template int mlp_train_generic<double>(const pg_mlp *, const double *, const double *, int64_t,
-                                       const double *, double, unsigned, double *, double *,
-                                       double *, double *, cudaStream_t);
 
 int64_t mlp_train_ws(int64_t B, const pg_mlp *m) {
     int64_t zsum = 0;
@@ -567,6 +563,13 @@ int pg_mlp_train_f32(const pg_mlp *mlp, const float *y, const float *targets, in
                      double *loss_sum, float *ws, void *stream) {
     return mlp_train_generic<float>(mlp, y, targets, B, params, scale, flags, gparams, dy, loss_sum,
                                     ws, as_stream(stream));
+}
+int pg_mlp_train_det_f32(const pg_mlp *mlp, const float *y, const float *targets, int64_t B,
+                         const float *params, float scale, unsigned flags, uint64_t *gparams_fx,
+                         float *dy, uint64_t *loss_fx, float *ws, void *stream) {
+    return mlp_train_generic<float, fx_t, fx_t>(mlp, y, targets, B, params, scale, flags,
+                                                (fx_t *)gparams_fx, dy, (fx_t *)loss_fx, ws,
+                                                as_stream(stream));
 }
 int pg_mlp_train_f64(const pg_mlp *mlp, const double *y, const double *targets, int64_t B,
                      const double *params, double scale, unsigned flags, double *gparams,

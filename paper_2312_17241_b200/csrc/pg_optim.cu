@@ -84,6 +84,23 @@ __global__ void lazy_adam_rebake_kernel(T *conf, T *m, T *v, uint8_t *baked, T *
     }
 }
 
+// deterministic mode: fixed-point accumulators -> float gradients (added),
+// accumulators cleared for the next step
+__global__ void fx_accumulate_kernel(fx_t *fx, int64_t n, float *dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const long long v = (long long)fx[i];
+        if (v != 0) {
+            dst[i] = __fadd_rn(dst[i], (float)ldexp((double)v, -PG_FX_SHIFT));
+            fx[i] = 0;
+        }
+    }
+}
+__global__ void fx_loss_kernel(fx_t *fx, double *loss) {
+    loss[0] = ldexp((double)(long long)fx[0], -PG_FX_LOSS_SHIFT);
+    fx[0] = 0;
+}
+
 __global__ void touched_to_f32_kernel(const uint8_t *t, int64_t n, float *o) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) o[i] = (float)t[i];
@@ -223,6 +240,15 @@ int pg_adam_rebake_rows_f64(double *conf, double *m, double *v, int n_p, uint8_t
                             void *stream) {
     return launch_rows<double>(conf, m, v, n_p, baked, rows_u, U, gconf_u, corr1, corr2, lr, b1, b2,
                                eps, stream);
+}
+int pg_fx_accumulate_f32(uint64_t *fx, int64_t n, float *dst, void *stream) {
+    if (n == 0) return PG_OK;
+    fx_accumulate_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, as_stream(stream)>>>((fx_t *)fx, n, dst);
+    return check_launch("fx_accumulate");
+}
+int pg_fx_loss(uint64_t *fx, double *loss_sum, void *stream) {
+    fx_loss_kernel<<<1, 1, 0, as_stream(stream)>>>((fx_t *)fx, loss_sum);
+    return check_launch("fx_loss");
 }
 int pg_touched_to_f32(const uint8_t *touched, int64_t n, float *out, void *stream) {
     if (n == 0) return PG_OK;

@@ -74,15 +74,15 @@ __device__ __forceinline__ void fwd_layer(const float *__restrict__ inT, const f
     }
 }
 
-template <typename FT, int D, int NPM>
+template <typename FT, int D, int NPM, typename ACC, typename LACC>
 __global__ void __launch_bounds__(kNT, 1)
     train_fused_kernel(const pg_grid g, const float *__restrict__ xs, const float *__restrict__ targets,
                        int64_t B, const FT *__restrict__ feats_fwd, const float *__restrict__ feats,
                        const uint8_t *__restrict__ baked, const float *__restrict__ conf,
                        const float *__restrict__ params, int od, float scale, int sigmoid,
-                       float *__restrict__ gfeat, float *__restrict__ gconf,
-                       uint8_t *__restrict__ touched, float *__restrict__ gparams,
-                       double *__restrict__ loss_sum, float *__restrict__ dy_out) {
+                       ACC *__restrict__ gfeat, ACC *__restrict__ gconf,
+                       uint8_t *__restrict__ touched, ACC *__restrict__ gparams,
+                       LACC *__restrict__ loss_sum, float *__restrict__ dy_out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TrainSmem &S = *reinterpret_cast<TrainSmem *>(smem_raw);
     const int tid = threadIdx.x;
@@ -318,14 +318,14 @@ __global__ void __launch_bounds__(kNT, 1)
 #pragma unroll 1
             for (int it = 0; it < 4; ++it) {
                 const int l = lsub + 4 * it;
-                encode_level_bwd2<D, NPM>(g, l, x, S.yT[sw(2 * l, pl)], S.yT[sw(2 * l + 1, pl)], feats,
+                encode_level_bwd2<D, NPM, ACC>(g, l, x, S.yT[sw(2 * l, pl)], S.yT[sw(2 * l + 1, pl)], feats,
                                          conf, gfeat, gconf, touched);
             }
         }
     }
     // ---- flush gradient accumulators ----
-    float *gW0p = gparams, *gb0p = gW0p + kI * kH, *gW1p = gb0p + kH, *gb1p = gW1p + kH * kH;
-    float *gW2p = gb1p + kH, *gb2p = gW2p + kH * od;
+    ACC *gW0p = gparams, *gb0p = gW0p + kI * kH, *gW1p = gb0p + kH, *gb1p = gW1p + kH * kH;
+    ACC *gW2p = gb1p + kH, *gb2p = gW2p + kH * od;
     {
         const int jg = tid & 15;
         const int i0 = tid >> 4;
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(kNT, 1)
         double v = tid < kNT / 32 ? S.red[tid] : 0.0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (tid == 0 && loss_sum) atomicAdd(loss_sum, v);
+        if (tid == 0 && loss_sum) loss_add(loss_sum, v);
     }
 }
 
@@ -362,10 +362,11 @@ bool train_fast_ok(const pg_grid *g, const pg_mlp *m) {
            m->widths[3] <= kO;
 }
 
+template <typename ACC, typename LACC>
 int train_fused(const pg_grid *g, const pg_mlp *m, const float *xs, const float *targets, int64_t B,
                 const float *feats, const uint8_t *baked, const float *conf, const float *params,
-                float scale, unsigned flags, float *gfeat, float *gconf, uint8_t *touched,
-                float *gparams, double *loss_sum, float *dy_out, cudaStream_t s) {
+                float scale, unsigned flags, ACC *gfeat, ACC *gconf, uint8_t *touched,
+                ACC *gparams, LACC *loss_sum, float *dy_out, cudaStream_t s) {
     if (int e = validate_grid(g)) return e;
     PG_REQUIRE(train_fast_ok(g, m), "fused training needs F=2, 16 levels, N_p<=16, MLP [32,64,64,<=4]");
     if (B == 0) return PG_OK;
@@ -381,15 +382,13 @@ int train_fused(const pg_grid *g, const pg_mlp *m, const float *xs, const float 
     const bool np4 = g->log2_np <= 2;
 #define PG_TRAIN_LAUNCH(D_, NP_, IDX)                                                                 \
     do {                                                                                              \
+        auto kern = train_fused_kernel<float, D_, NP_, ACC, LACC>;                                    \
         if (!configured[IDX]) {                                                                       \
-            cudaFuncSetAttribute(train_fused_kernel<float, D_, NP_>,                                  \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                 \
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);            \
             configured[IDX] = true;                                                                   \
         }                                                                                             \
-        train_fused_kernel<float, D_, NP_><<<grd, kNT, smem, s>>>(*g, xs, targets, B, feats, feats,  \
-                                                                 baked, conf, params, od, scale, sig, \
-                                                                 gfeat, gconf, touched, gparams,      \
-                                                                 loss_sum, dy_out);                   \
+        kern<<<grd, kNT, smem, s>>>(*g, xs, targets, B, feats, feats, baked, conf, params, od, scale,  \
+                                    sig, gfeat, gconf, touched, gparams, loss_sum, dy_out);           \
     } while (0)
     if (g->d == 2) {
         if (np4) PG_TRAIN_LAUNCH(2, 4, 0); else PG_TRAIN_LAUNCH(2, 16, 1);
@@ -408,6 +407,20 @@ extern "C" int pg_train_fused_f32(const pg_grid *grid, const pg_mlp *mlp, const 
                                   float scale, unsigned flags, float *gfeat, float *gconf,
                                   uint8_t *touched, float *gparams, double *loss_sum, float *dy_out,
                                   void *stream) {
-    return pg::train_fused(grid, mlp, xs, targets, B, feats, baked, conf, params, scale, flags, gfeat,
-                           gconf, touched, gparams, loss_sum, dy_out, pg::as_stream(stream));
+    return pg::train_fused<float, double>(grid, mlp, xs, targets, B, feats, baked, conf, params, scale,
+                                          flags, gfeat, gconf, touched, gparams, loss_sum, dy_out,
+                                          pg::as_stream(stream));
+}
+
+extern "C" int pg_train_fused_det_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
+                                      const float *targets, int64_t B, const float *feats,
+                                      const uint8_t *baked, const float *conf, const float *params,
+                                      float scale, unsigned flags, uint64_t *gfeat_fx,
+                                      uint64_t *gconf_fx, uint8_t *touched, uint64_t *gparams_fx,
+                                      uint64_t *loss_fx, float *dy_out, void *stream) {
+    using pg::fx_t;
+    return pg::train_fused<fx_t, fx_t>(grid, mlp, xs, targets, B, feats, baked, conf, params, scale,
+                                       flags, (fx_t *)gfeat_fx, (fx_t *)gconf_fx, touched,
+                                       (fx_t *)gparams_fx, (fx_t *)loss_fx, dy_out,
+                                       pg::as_stream(stream));
 }

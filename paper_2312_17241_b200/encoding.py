@@ -69,8 +69,21 @@ def encode_forward_device(model: Model, xs: torch.Tensor, y: torch.Tensor = None
     return y
 
 
-def encode_backward_device(model: Model, xs: torch.Tensor, dy: torch.Tensor, stream=None):
-    """Launch the fused backward: accumulate into model.grads / touched."""
+def encode_backward_device(model: Model, xs: torch.Tensor, dy: torch.Tensor, stream=None,
+                           deterministic: bool = False, flush: bool = True):
+    """Launch the fused backward: accumulate into model.grads / touched.
+    deterministic=True accumulates in fixed point (run-to-run identical);
+    flush=False leaves the sums in model.grads_fx for the caller to flush."""
+    if deterministic:
+        if model.tdtype != torch.float32:
+            raise ValueError("deterministic mode is float32-only")
+        gf, _, gc = model.fx_ptrs()
+        _lib.call("pg_encode_bwd_det_f32", model.grid, _lib.ptr(xs), xs.shape[0], _lib.ptr(dy),
+                  _lib.ptr(model.feats), _lib.ptr(model.conf), gf, gc, _lib.ptr(model.touched),
+                  _lib.stream_ptr(stream))
+        if flush:
+            model.fx_flush(stream=stream)
+        return
     _lib.call(f"pg_encode_bwd_{_sfx(model)}", model.grid, _lib.ptr(xs), xs.shape[0], _lib.ptr(dy),
               _lib.ptr(model.feats), _lib.ptr(model.conf), _lib.ptr(model.gfeats),
               _lib.ptr(model.gconf), _lib.ptr(model.touched), _lib.stream_ptr(stream))
@@ -93,8 +106,9 @@ def encode_forward(model: Model, xs, surrogate: bool = False):
     return (y.cpu().numpy() if was_numpy else y), trace
 
 
-def encode_backward(model: Model, trace: EncodeTrace, upstream) -> None:
-    """Accumulate codebook gradients from an encoded batch (encoding.py:119-133)."""
+def encode_backward(model: Model, trace: EncodeTrace, upstream, deterministic: bool = False) -> None:
+    """Accumulate codebook gradients from an encoded batch (encoding.py:119-133).
+    deterministic=True: order-independent fixed-point accumulation (float32)."""
     if not isinstance(trace, EncodeTrace) or len(trace) != len(model.levels):
         raise StaleTrace("trace level count does not match the model")
     if trace.model_id != id(model) or trace.layout_version != model.layout_version:
@@ -107,4 +121,4 @@ def encode_backward(model: Model, trace: EncodeTrace, upstream) -> None:
         dy = torch.from_numpy(np.ascontiguousarray(upstream, dtype=model.dtype)).to(model.device)
     if tuple(dy.shape) != (trace.xs.shape[0], model.hyper.encoded_width):
         raise StaleTrace(f"upstream shape {tuple(dy.shape)} does not match the trace")
-    encode_backward_device(model, trace.xs, dy)
+    encode_backward_device(model, trace.xs, dy, deterministic=deterministic)

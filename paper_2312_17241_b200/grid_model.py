@@ -171,6 +171,36 @@ class Model:
         gw, gb = self._mlp_views(self.gmlp)
         self.mlp = MlpView(w, b, gw, gb)
 
+    # -- deterministic mode: 64-bit fixed-point accumulators ------------------
+    @property
+    def grads_fx(self):
+        """uint64 accumulators laid out like `grads` (deterministic mode)."""
+        if getattr(self, "_grads_fx", None) is None:
+            self._grads_fx = torch.zeros(self.off_gconf + self.n_conf, dtype=torch.int64,
+                                         device=self.device)
+            self._loss_fx = torch.zeros(1, dtype=torch.int64, device=self.device)
+        return self._grads_fx
+
+    @property
+    def loss_fx(self):
+        self.grads_fx  # noqa: B018 (allocates both)
+        return self._loss_fx
+
+    def fx_ptrs(self):
+        """(gfeat_fx, gmlp_fx, gconf_fx) device pointers into grads_fx."""
+        base = self.grads_fx.data_ptr()
+        return (_lib.ctypes.c_void_p(base), _lib.ctypes.c_void_p(base + 8 * self.n_feat),
+                _lib.ctypes.c_void_p(base + 8 * self.off_gconf))
+
+    def fx_flush(self, loss_sum=None, stream=None) -> None:
+        """Add the fixed-point accumulators into the float gradients (and the
+        loss into loss_sum), clearing them."""
+        s = _lib.stream_ptr(stream)
+        _lib.call("pg_fx_accumulate_f32", _lib.ptr(self.grads_fx), self.grads_fx.numel(),
+                  _lib.ptr(self.grads), s)
+        if loss_sum is not None:
+            _lib.call("pg_fx_loss", _lib.ptr(self.loss_fx), _lib.ptr(loss_sum), s)
+
     # -- reference Model methods (model.py:108-130) -------------------------
     def zero_grads(self) -> None:
         self.grads.zero_()

@@ -89,7 +89,7 @@ class TrainState:
     """Optimizer state bound to one device model; drives individual steps."""
 
     def __init__(self, model: Model, image, cfg: TrainConfig, sampler: str = "reference",
-                 fused: bool | None = None):
+                 fused: bool | None = None, deterministic: bool = False):
         cfg.validate()
         if sampler not in ("reference", "device"):
             raise InvalidHyperparameter(f"unknown sampler {sampler!r}")
@@ -122,6 +122,9 @@ class TrainState:
         self.targets = torch.empty((B, h.out_dim), dtype=tdt, device=dev)
         if fused is not None:
             self.fused = self.fused and bool(fused)
+        if deterministic and model.tdtype != torch.float32:
+            raise InvalidHyperparameter("deterministic mode is float32-only")
+        self.deterministic = deterministic
         if not self.fused:
             self.y = torch.empty((B, h.encoded_width), dtype=tdt, device=dev)
             self.dy = torch.empty_like(self.y)
@@ -205,6 +208,23 @@ class TrainState:
         m, cfg, s = self.model, self.cfg, _lib.stream_ptr()
         flags = _lib.PG_SIGMOID if m.hyper.out_sigmoid else 0
         scale = float(np.dtype(m.dtype).type(self.scale))
+        if self.deterministic:
+            gf, gm, gc = m.fx_ptrs()
+            if self.fused:
+                _lib.call("pg_train_fused_det_f32", m.grid, m.mlp_desc, _lib.ptr(xs),
+                          _lib.ptr(targets), xs.shape[0], _lib.ptr(m.feats), _lib.ptr(m.baked),
+                          _lib.ptr(m.conf), _lib.ptr(m.mlp_params), scale, flags, gf, gc,
+                          _lib.ptr(m.touched), gm, _lib.ptr(m.loss_fx), _lib.ptr(dy_out), s)
+            else:
+                encode_forward_device(m, xs, self.y)
+                _lib.call("pg_mlp_train_det_f32", m.mlp_desc, _lib.ptr(self.y), _lib.ptr(targets),
+                          xs.shape[0], _lib.ptr(m.mlp_params), scale, flags, gm,
+                          _lib.ptr(self.dy), _lib.ptr(m.loss_fx), _lib.ptr(self.ws), s)
+                if dy_out is not None:
+                    dy_out.copy_(self.dy)
+                encode_backward_device(m, xs, self.dy, deterministic=True, flush=False)
+            m.fx_flush(loss_sum=self.loss_sum)
+            return
         if self.fused:
             _lib.call("pg_train_fused_f32", m.grid, m.mlp_desc, _lib.ptr(xs), _lib.ptr(targets),
                       xs.shape[0], _lib.ptr(m.feats), _lib.ptr(m.baked), _lib.ptr(m.conf),
@@ -281,11 +301,11 @@ def psnr(reference, test) -> float:
 
 
 def fit(image, hyper: HyperParams, cfg: TrainConfig, force_probed: bool = False,
-        sampler: str = "reference") -> FitResult:
+        sampler: str = "reference", deterministic: bool = False) -> FitResult:
     """Fit one image on the GPU (trainer.py:196-242)."""
     from .decode import decode_image, to_inference
     model = init_model(hyper, cfg.seed, cfg.dtype, force_probed=force_probed)
-    state = TrainState(model, image, cfg, sampler=sampler)
+    state = TrainState(model, image, cfg, sampler=sampler, deterministic=deterministic)
     sink = open(cfg.metrics_path, "w") if cfg.metrics_path else None
     losses, step_ms = [], []
     t_start = time.perf_counter()

@@ -424,3 +424,81 @@ def test_decode_generic_shape_matches_oracle():
     q = np.random.default_rng(6).random((999, 2)).astype(np.float32)
     np.testing.assert_allclose(pg.decode_pixels(inf, q), O.decode_pixels(O.to_inference(om), q),
                                rtol=1e-6, atol=1e-7)
+
+
+# ------------------------------------------------------- deterministic mode
+TINY = dict(n_f=32, n_c=64, n_p=4, n_levels=3, n_min=4, n_max=16, n_neurons=8)
+
+
+def _small_image(seed):
+    return np.random.default_rng(seed).random((12, 12, 3)).astype(np.float32)
+
+
+@pytest.mark.parametrize("kw", [TINY, C1])
+def test_deterministic_training_is_bit_reproducible(kw):
+    """test_trainer.py:115-121 on the GPU: same seed -> identical losses and
+    parameters, run after run (fixed-point accumulation)."""
+    import paper_2312_17241_b200 as pg
+    img = _smooth() if kw is C1 else _small_image(1)
+    cfg = pg.TrainConfig(steps=12, batch_size=4096 if kw is C1 else 128, seed=7)
+    a = pg.fit(img, pg.HyperParams(**kw), cfg, deterministic=True)
+    b = pg.fit(img, pg.HyperParams(**kw), cfg, deterministic=True)
+    assert a.losses == b.losses
+    assert a.final_psnr == b.final_psnr
+    eq(a.model.dense.cpu().numpy(), b.model.dense.cpu().numpy())
+    eq(a.model.conf.cpu().numpy(), b.model.conf.cpu().numpy())
+
+
+@pytest.mark.parametrize("kw", [dict(TINY, n_p=1), dict(C1, n_p=1)])
+def test_np1_probed_equals_plain_bit_exact(kw):
+    """test_trainer.py:131-141 / test_acceptance.py:78-90: the probed path at
+    N_p = 1 is bit-identical to plain hashing (losses, features, MLP)."""
+    import paper_2312_17241_b200 as pg
+    big = kw["n_f"] == 2**12
+    img = _smooth() if big else _small_image(3)
+    cfg = pg.TrainConfig(steps=20 if big else 40, batch_size=4096 if big else 128, seed=3)
+    hyper = pg.HyperParams(**kw)
+    plain = pg.fit(img, hyper, cfg, force_probed=False, deterministic=True)
+    probed = pg.fit(img, hyper, cfg, force_probed=True, deterministic=True)
+    assert probed.model.probed and not plain.model.probed
+    assert plain.losses == probed.losses
+    eq(plain.model.feats.cpu().numpy(), probed.model.feats.cpu().numpy())
+    eq(plain.model.mlp_params.cpu().numpy(), probed.model.mlp_params.cpu().numpy())
+
+
+def test_degenerate_lookup_equivalence_grid(cuda):
+    """test_acceptance.py:56-76: over every vertex of a 65x65 grid the batched
+    probed lookup with log2 N_p = 0 equals the plain hashed lookup."""
+    rng = np.random.default_rng(0)
+    feats = rng.standard_normal((256, 2)).astype(np.float32)
+    ax = np.arange(65, dtype=np.float32) / 64.0
+    xs = np.stack(np.meshgrid(ax, ax, indexing="ij"), -1).reshape(-1, 2)
+    out_p, base, row, w_p = cuda.probed_fwd(xs, 64, 256, 64, 0, feats, np.zeros(64, np.uint8),
+                                            O.PRIMARY, O.AUX)
+    out_h, idx, w_h = cuda.hashed_fwd(xs, 64, 256, feats, O.PRIMARY)
+    eq(base, idx)
+    eq(out_p, out_h)
+
+
+def test_deterministic_gradients_match_oracle():
+    import paper_2312_17241_b200 as pg
+    img = _smooth()
+    m, om = _models(C1, perturb=False)
+    st = pg.TrainState(m, img, pg.TrainConfig(batch_size=8192, seed=0), deterministic=True)
+    xs, targets = st.sample_batch()
+    st.loss_sum.zero_()
+    st.compute_grads(xs, targets)
+    ost = O.TrainState(om, img, O.TrainCfg(batch_size=8192, seed=0))
+    oxs, otg = ost.sample_batch()
+    y, traces = O.encode_forward(om, oxs)
+    out, cache = O.mlp_forward(om.W, om.b, y)
+    diff = out - otg
+    ody = O.mlp_backward(om.W, om.Wg, om.bg, cache, diff * np.float32(2.0 / diff.size))
+    O.encode_backward(om, traces, ody)
+    oloss = float(np.mean(diff.astype(np.float64) ** 2))
+    assert abs(float(st.loss_sum.item()) / (8192 * 3) - oloss) <= 1e-9 * oloss
+    for i in range(3):
+        np.testing.assert_allclose(m.mlp.weight_grads[i].cpu().numpy(), om.Wg[i], rtol=1e-5, atol=1e-9)
+    gf = m.gfeats.cpu().numpy()
+    for L in om.levels:
+        np.testing.assert_allclose(gf[L.level], L.fgrad, rtol=1e-5, atol=1e-10)
