@@ -178,7 +178,7 @@ def measure_l2(lib_call, torch, table_mib=8):
 
 
 # ------------------------------------------------------------------ CPU arm
-def cpu_decode_baseline(hyper, budget_s=12.0, sample=1 << 20, threads=None):
+def cpu_decode_baseline(hyper, budget_s=15.0, sample=1 << 24, threads=None):
     """The reference's decode_pixels on the host: the reference's own compiled
     Cython core (oracle/_ref) when it was built, else the C port, driven by the
     oracle's restatement of model_io.decode_pixels; chunks of 16384 queries
@@ -233,7 +233,7 @@ def cpu_train_baseline(budget_s=8.0):
         st.step()
     times = []
     t0 = time.perf_counter()
-    while time.perf_counter() - t0 < budget_s and len(times) < 40:
+    while time.perf_counter() - t0 < budget_s and len(times) < 400:
         a = time.perf_counter()
         st.step()
         times.append(time.perf_counter() - a)
@@ -329,6 +329,12 @@ def run_gpu(args, rank, world, local_rank):
 
     # ---------------- training (C1, data parallel) ----------------
     train = run_train(args, pg, torch, dist, rank, world, dev, barrier, max_over_ranks)
+    extra = {}
+    if not args.quick:
+        extra["train_c3"] = run_train_field(args, pg, torch, dist, rank, world, barrier, max_over_ranks, "c3")
+        extra["train_c4"] = run_train_field(args, pg, torch, dist, rank, world, barrier, max_over_ranks, "c4")
+        if world == 1:
+            extra["sweep_inference_c2_c5"] = run_sweep(args, pg, torch, decode_device)
 
     line = {
         "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": world,
@@ -359,6 +365,7 @@ def run_gpu(args, rank, world, local_rank):
         "clocks": clk,
         "ablation_queries_per_s": ablation,
         "train": train,
+        **extra,
     }
     return line, e2e_launches
 
@@ -400,6 +407,98 @@ def run_train(args, pg, torch, dist, rank, world, dev, barrier, max_over_ranks):
             "last_loss": loss, "scaling": "weak"}
 
 
+def _time_steps(torch, step, steps, warmup, barrier, max_over_ranks):
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    return max_over_ranks(e0.elapsed_time(e1)) / steps
+
+
+def field_points(kind, n, seed):
+    """Synthetic 3-D training sets of SURVEY 8(d): C3 sphere SDF
+    f(x) = |x - 0.5| - 0.3 with x ~ U[0,1)^3; C4 NeRF-style ray samples (rays
+    from a radius-1.5 sphere around the centre, 64 uniform samples per ray
+    inside [0.1, 0.9]^3) with an analytic (density, rgb) field."""
+    rng = np.random.default_rng(seed)
+    if kind == "c3":
+        x = rng.random((n, 3), dtype=np.float32)
+        v = (np.linalg.norm(x - 0.5, axis=1) - 0.3).astype(np.float32)[:, None]
+        return x, v
+    rays = n // 64
+    d = rng.standard_normal((rays, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    origin = 0.5 + 1.5 * d
+    t = np.sort(rng.random((rays, 64)), axis=1)
+    pts = origin[:, None, :] - (0.6 + 1.8 * t)[:, :, None] * d[:, None, :]
+    x = np.clip(pts.reshape(-1, 3), 0.1, 0.9).astype(np.float32)
+    r2 = np.sum((x - 0.5) ** 2, axis=1, keepdims=True)
+    v = np.concatenate([np.exp(-8.0 * r2), x], axis=1).astype(np.float32)
+    return x, v
+
+
+def run_train_field(args, pg, torch, dist, rank, world, barrier, max_over_ranks, kind):
+    """C3 (3-D SDF, 2^22 points/step) or C4 (NeRF-style, N_p=8, out 4, 2^18
+    samples/step) training step; data parallel under torchrun."""
+    if kind == "c3":
+        hk = dict(d=3, n_f=2**8, n_c=2**16, n_p=4, n_max=512, out_dim=1)
+        B = 1 << 22
+    else:
+        hk = dict(d=3, n_f=2**8, n_c=2**16, n_p=8, n_max=2048, out_dim=4)
+        B = 1 << 18
+    hyper = pg.HyperParams(**hk)
+    model = pg.init_model(hyper, seed=0)
+    x, v = field_points(kind, 2 * B * world, seed=1)
+    st = pg.FieldTrainState(model, x, v, pg.TrainConfig(batch_size=B, seed=rank))
+    dp = None
+    if world > 1:
+        from paper_2312_17241_b200.dist import DataParallel
+        dp = DataParallel(st, dist)
+    steps = max(3, args.steps // 4)
+    ms = _time_steps(torch, dp.launch_step if dp else st.launch_step, steps, args.warmup, barrier,
+                     max_over_ranks)
+    bps = train_bytes_per_sample(hyper, len(model.probed))
+    return {"metric": "train samples/s", "value": world * B / (ms * 1e-3), "unit": "samples/s",
+            "ms_per_step": ms, "steps": steps,
+            "config": {"workload": f"{kind.upper()} 3-D field fit step", **hk,
+                       "samples_per_gpu_per_step": B, "mlp": hyper.mlp_widths(),
+                       "probed_levels": len(model.probed), "parallelism": f"dp{world}"},
+            "encode_bytes_per_sample": bps, "encode_algorithmic_gbs": B * bps / (ms * 1e-3) / 1e9,
+            "last_loss": st.loss_value()}
+
+
+def run_sweep(args, pg, torch, decode_device):
+    """configs[1] / [4] sweep: decode q/s for log2 n_f in {14,16,18} x N_p in
+    {2,4,8,16} (n_c = 2^16, n_max = 8192) and the unprobed N_p = 1 hash grid
+    at equal table size (C5), 2^22 queries per call, tcgen05 path."""
+    B = 1 << 22
+    xs = torch.rand((B, 2), device="cuda", generator=torch.Generator("cuda").manual_seed(7))
+    out = torch.empty((B, 3), device="cuda")
+    res = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for lnf in (14, 16, 18):
+        for n_p in (1, 2, 4, 8, 16):
+            _, inf = inference_model(pg, pg.HyperParams(n_f=2**lnf, n_c=2**16, n_p=n_p, n_max=8192))
+            for _ in range(3):
+                decode_device(inf, xs, out, exact=False)
+            e0.record()
+            for _ in range(5):
+                decode_device(inf, xs, out, exact=False)
+            e1.record()
+            torch.cuda.synchronize()
+            res.append({"log2_n_f": lnf, "n_p": n_p, "probed_levels": len(inf.probed),
+                        "queries_per_s": B * 5 / (e0.elapsed_time(e1) * 1e-3)})
+            del inf
+    return res
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference's own CPU path on this host."""
     if rank != 0:
@@ -431,6 +530,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--exact", action="store_true", help="reference-order (bit-exact) MLP")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="headline + C1 train only")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 

@@ -31,7 +31,7 @@ def __getattr__(name):
     if name in ("encode_forward", "encode_backward"):
         from . import encoding
         return getattr(encoding, name)
-    if name in ("TrainConfig", "TrainState", "fit", "adam_update"):
+    if name in ("TrainConfig", "TrainState", "FieldTrainState", "fit", "adam_update"):
         from . import train
         return getattr(train, name)
     if name in ("to_inference", "decode_pixels", "decode_at", "decode_rect", "decode_image",

@@ -91,18 +91,19 @@ class TrainState:
     def __init__(self, model: Model, image, cfg: TrainConfig, sampler: str = "reference",
                  fused: bool | None = None, deterministic: bool = False):
         cfg.validate()
-        if sampler not in ("reference", "device"):
+        if sampler not in ("reference", "device", "points"):
             raise InvalidHyperparameter(f"unknown sampler {sampler!r}")
-        img = image if isinstance(image, torch.Tensor) else torch.from_numpy(
-            np.ascontiguousarray(image, dtype=model.dtype))
-        if img.ndim != 3 or img.shape[2] != model.hyper.out_dim:
-            raise InvalidHyperparameter(
-                f"image shape {tuple(img.shape)} does not match output dim {model.hyper.out_dim}")
-        if model.hyper.d != 2:
-            raise InvalidHyperparameter("the image trainer is 2-D (trainer.py:109-116)")
         self.model, self.cfg, self.sampler = model, cfg, sampler
-        self.image = img.to(device=model.device, dtype=model.tdtype).contiguous()
-        self.height, self.width = int(img.shape[0]), int(img.shape[1])
+        if sampler != "points":
+            img = image if isinstance(image, torch.Tensor) else torch.from_numpy(
+                np.ascontiguousarray(image, dtype=model.dtype))
+            if img.ndim != 3 or img.shape[2] != model.hyper.out_dim:
+                raise InvalidHyperparameter(
+                    f"image shape {tuple(img.shape)} does not match output dim {model.hyper.out_dim}")
+            if model.hyper.d != 2:
+                raise InvalidHyperparameter("the image trainer is 2-D (trainer.py:109-116)")
+            self.image = img.to(device=model.device, dtype=model.tdtype).contiguous()
+            self.height, self.width = int(img.shape[0]), int(img.shape[1])
         self.rng = seeded_rng(cfg.seed, SEED_BATCH)
         self.t = 0
         dev, tdt = model.device, model.tdtype
@@ -118,7 +119,7 @@ class TrainState:
         self.pix_host = torch.empty(B, dtype=torch.int64, pin_memory=True)
         self.pix_copied = torch.cuda.Event()
         self.pix = torch.empty(B, dtype=torch.int64, device=dev)
-        self.xs = torch.empty((B, 2), dtype=tdt, device=dev)
+        self.xs = torch.empty((B, h.d), dtype=tdt, device=dev)
         self.targets = torch.empty((B, h.out_dim), dtype=tdt, device=dev)
         if fused is not None:
             self.fused = self.fused and bool(fused)
@@ -149,6 +150,13 @@ class TrainState:
         """Draw the next batch; returns device (xs, targets)."""
         m, B, s = self.model, self.cfg.batch_size, _lib.stream_ptr()
         sfx = "f64" if m.tdtype == torch.float64 else "f32"
+        if self.sampler == "points":
+            # next contiguous slice of a resident point set (cyclic): zero-copy views
+            n = self.points.shape[0]
+            lo = (self.t * self.world + self.rank) * B % n
+            if lo + B > n:
+                lo = 0
+            return self.points[lo:lo + B], self.values[lo:lo + B]
         if self.sampler == "reference":
             # trainer.py:110-111; replicas draw the global batch and keep their slice
             pix = self.rng.integers(0, self.width * self.height, size=B * self.world)
@@ -278,6 +286,26 @@ class TrainState:
             if bad.numel():
                 raise TrainingDiverged(
                     f"incremental bake diverged on level {m.probed[int(bad[0])]}")
+
+
+class FieldTrainState(TrainState):
+    """Training on an arbitrary d-dimensional field (2-D or 3-D SDF, density,
+    radiance samples): batches are successive slices of a device-resident
+    point set with target values.  The reference has no trainer for these
+    (trainer.py:92-95 is image-only); the step is the same composition of
+    encode / MLP / Adam / lazy-Adam it uses (SURVEY 7.4 hazard 13)."""
+
+    def __init__(self, model: Model, points, values, cfg: TrainConfig, **kw):
+        pts = torch.as_tensor(points).to(device=model.device, dtype=model.tdtype).contiguous()
+        val = torch.as_tensor(values).to(device=model.device, dtype=model.tdtype).contiguous()
+        if pts.ndim != 2 or pts.shape[1] != model.hyper.d:
+            raise InvalidHyperparameter(f"points must be (N, {model.hyper.d})")
+        if val.shape != (pts.shape[0], model.hyper.out_dim):
+            raise InvalidHyperparameter(f"values must be (N, {model.hyper.out_dim})")
+        if pts.shape[0] < cfg.batch_size:
+            raise InvalidHyperparameter("point set smaller than one batch")
+        super().__init__(model, None, cfg, sampler="points", **kw)
+        self.points, self.values = pts, val
 
 
 @dataclass

@@ -502,3 +502,97 @@ def test_deterministic_gradients_match_oracle():
     gf = m.gfeats.cpu().numpy()
     for L in om.levels:
         np.testing.assert_allclose(gf[L.level], L.fgrad, rtol=1e-5, atol=1e-10)
+
+
+def test_full_pipeline_gradients_match_finite_differences_f64():
+    """test_acceptance.py:97-162 (criterion 2) on the GPU, fp64: surrogate
+    encode -> MLP -> MSE; analytic gradients from the device backward passes
+    (straight-through confidences, MLP) vs central differences, < 1e-4."""
+    import paper_2312_17241_b200 as pg
+    from paper_2312_17241_b200 import _lib
+    from paper_2312_17241_b200.encoding import encode_backward_device, encode_forward_device
+    hyper = pg.HyperParams(n_f=16, n_c=8, n_p=4, n_levels=2, n_min=4, n_max=8, n_neurons=64)
+    m = pg.init_model(hyper, seed=3, dtype=np.float64)
+    assert len(m.probed) == 2
+    rng = np.random.default_rng(4)
+    with torch.no_grad():
+        m.feats.copy_(torch.from_numpy(rng.uniform(-0.5, 0.5, tuple(m.feats.shape))))
+        m.conf.copy_(torch.from_numpy(rng.standard_normal(tuple(m.conf.shape))))
+        m.rebake_all()
+    img = rng.random((8, 8, 3))
+    cols, rows = np.meshgrid(np.arange(8), np.arange(8))
+    xs = torch.from_numpy(np.stack([(cols.ravel() + 0.5) / 8, (rows.ravel() + 0.5) / 8], 1)).cuda()
+    tg = torch.from_numpy(img.reshape(-1, 3).copy()).cuda()
+    B = xs.shape[0]
+    dy = torch.empty((B, hyper.encoded_width), dtype=torch.float64, device="cuda")
+    ws = torch.empty(int(_lib.lib().pg_mlp_train_workspace_floats(B, m.mlp_desc)), dtype=torch.float64,
+                     device="cuda")
+    loss_sum = torch.zeros(1, dtype=torch.float64, device="cuda")
+
+    def run(backward):
+        y = encode_forward_device(m, xs, surrogate=True)
+        m.zero_grads()
+        loss_sum.zero_()
+        _lib.call("pg_mlp_train_f64", m.mlp_desc, _lib.ptr(y), _lib.ptr(tg), B, _lib.ptr(m.mlp_params),
+                  2.0 / (B * 3), 0, _lib.ptr(m.gmlp), _lib.ptr(dy), _lib.ptr(loss_sum), _lib.ptr(ws),
+                  _lib.stream_ptr())
+        if backward:
+            encode_backward_device(m, xs, dy)
+        return float(loss_sum.item()) / (B * 3)
+
+    run(True)
+    analytic = {"feats": m.gfeats.clone(), "conf": m.gconf.clone(), "mlp": m.gmlp.clone()}
+    h, worst = 1e-7, 0.0
+    fd_rng = np.random.default_rng(5)
+    for name, vals in (("feats", m.feats), ("conf", m.conf), ("mlp", m.mlp_params)):
+        flat, g = vals.reshape(-1), analytic[name].reshape(-1).cpu().numpy()
+        idx = np.arange(flat.numel()) if name != "mlp" else fd_rng.choice(flat.numel(), 400, replace=False)
+        for i in idx:
+            orig = float(flat[i])
+            flat[i] = orig + h
+            hi = run(False)
+            flat[i] = orig - h
+            lo = run(False)
+            flat[i] = orig
+            fd = (hi - lo) / (2 * h)
+            err = abs(fd - g[i]) / max(1e-3, abs(fd), abs(g[i]))
+            worst = max(worst, err)
+            assert err < 1e-4, (name, i, fd, g[i])
+    print("full-pipeline FD worst relative error", worst)
+
+
+@pytest.mark.parametrize("n_p,out_dim", [(4, 1), (8, 4)])
+def test_field_trainer_3d_gradients_vs_oracle(n_p, out_dim):
+    """C3 / C4 shapes (d = 3): the fused 3-D training pass. dL/dy bit-exact
+    vs numpy/OpenBLAS, MLP and table gradients within 1e-5."""
+    import paper_2312_17241_b200 as pg
+    kw = dict(d=3, n_f=2**8, n_c=2**16, n_p=n_p, n_max=512, out_dim=out_dim)
+    m, om = _models(kw, perturb=False)
+    rng = np.random.default_rng(2)
+    x = rng.random((4096, 3), dtype=np.float32)
+    v = rng.random((4096, out_dim), dtype=np.float32)
+    st = pg.FieldTrainState(m, x, v, pg.TrainConfig(batch_size=4096, seed=0))
+    assert st.fused
+    xs, tg = st.sample_batch()
+    dy = torch.empty((4096, 32), device="cuda")
+    st.loss_sum.zero_()
+    st.compute_grads(xs, tg, dy_out=dy)
+    y, traces = O.encode_forward(om, x)
+    out, cache = O.mlp_forward(om.W, om.b, y)
+    diff = out - v
+    ody = O.mlp_backward(om.W, om.Wg, om.bg, cache, diff * np.float32(2.0 / diff.size))
+    if out_dim == 1:
+        # OpenBLAS forwards N = 1 GEMMs to its GEMV kernel, which sums in a
+        # different order than the GEMM microkernel: tolerance, not bits
+        np.testing.assert_allclose(dy.cpu().numpy(), ody, rtol=1e-5, atol=1e-10)
+    else:
+        eq(dy.cpu().numpy(), ody)
+    O.encode_backward(om, traces, ody)
+    gf = m.gfeats.cpu().numpy()
+    gc = m.gconf.cpu().numpy()
+    for L in om.levels:
+        np.testing.assert_allclose(gf[L.level], L.fgrad, rtol=1e-5, atol=1e-10)
+    for i, lv in enumerate(m.probed):
+        np.testing.assert_allclose(gc[i], om.levels[lv].cgrad, rtol=1e-5, atol=1e-10)
+    for i in range(3):
+        np.testing.assert_allclose(m.mlp.weight_grads[i].cpu().numpy(), om.Wg[i], rtol=1e-5, atol=1e-9)
