@@ -1,4 +1,4 @@
-// Fused training pass on sm_100a: for every 128-sample tile, ONE kernel does
+// Fused training pass on sm_100a: for every 64-sample tile, ONE kernel does
 //   encode fwd (16 levels, F=2)  ->  MLP [32,64,64,out<=4] fwd  ->  squared
 //   error + dpred  ->  MLP bwd (weight grads held in registers across tiles,
 //   dgrads)  ->  encode bwd (straight-through scatter into gfeat/gconf)
@@ -17,8 +17,9 @@
 
 namespace pg {
 
-constexpr int kT = 128;   // samples per tile
-constexpr int kNT = 512;  // threads per CTA
+constexpr int kT = 64;    // samples per tile
+constexpr int kNT = 256;  // threads per CTA (2 CTAs per SM: one's memory-bound
+                          // encode phases overlap the other's FFMA MLP phases)
 constexpr int kI = 32;    // L*F
 constexpr int kH = 64;    // hidden width
 constexpr int kO = 4;     // padded output width
@@ -75,7 +76,7 @@ __device__ __forceinline__ void fwd_layer(const float *__restrict__ inT, const f
 }
 
 template <typename FT, int D, int NPM, typename ACC, typename LACC>
-__global__ void __launch_bounds__(kNT, 1)
+__global__ void __launch_bounds__(kNT, 2)
     train_fused_kernel(const pg_grid g, const float *__restrict__ xs, const float *__restrict__ targets,
                        int64_t B, const FT *__restrict__ feats_fwd, const float *__restrict__ feats,
                        const uint8_t *__restrict__ baked, const float *__restrict__ conf,
@@ -115,11 +116,11 @@ __global__ void __launch_bounds__(kNT, 1)
         for (int i = tid; i < kO; i += kNT) S.b2[i] = i < od ? p[i] : 0.0f;
     }
     // persistent per-thread gradient accumulators
-    float gW2 = 0.0f;                 // (k = tid&63, j = (tid>>6)&3), half = tid>>8
+    float gW2 = 0.0f;                 // (k = tid&63, j = tid>>6)
     float gB2 = 0.0f;                 // j = tid (tid < 4)
-    float gW1[2][4] = {};             // i = (tid>>4)*2 + a, j = (tid&15)*4 + b
+    float gW1[4][4] = {};             // i = (tid>>4)*4 + u, j = (tid&15)*4 + v
     float gB1 = 0.0f;                 // j = tid (tid < 64)
-    float gW0[4] = {};                // i = tid>>4, j = (tid&15)*4 + b
+    float gW0[2][4] = {};             // i = (tid>>4)*2 + u, j = (tid&15)*4 + v
     float gB0 = 0.0f;                 // j = tid (tid < 64)
     double lsum = 0.0;
 
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(kNT, 1)
         }
         __syncthreads();
         // ---- encode forward: thread = (sample pl, levels lsub + 4*it) ----
-        const int pl = tid & (kT - 1), lsub = tid >> 7;
+        const int pl = tid & (kT - 1), lsub = tid >> 6;
         float x[D];
 #pragma unroll
         for (int a = 0; a < D; ++a) x[a] = S.xs[pl * D + a];
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(kNT, 1)
         __syncthreads();
         // ---- output layer, loss, dpred (trainer.py:122-136) ----
         {
-            const int q = tid & (kT - 1), j = tid >> 7;
+            const int q = tid & (kT - 1), j = tid >> 6;
             float d = 0.0f;
             if (j < od && q < nv) {
                 float acc = 0.0f;
@@ -171,9 +172,9 @@ __global__ void __launch_bounds__(kNT, 1)
         __syncthreads();
         // ---- dW2 += relu(z2)^T d3, db2 += sum d3 ----
         {
-            const int k = tid & 63, j = (tid >> 6) & 3, half = tid >> 8;
+            const int k = tid & 63, j = tid >> 6;
             float acc = 0.0f;
-            for (int q = half * 64; q < half * 64 + 64; ++q)
+            for (int q = 0; q < kT; ++q)
                 acc = __fmaf_rn(relu_np(S.z2T[sw(k, q)]), S.d3[q * kO + j], acc);
             gW2 += acc;
             if (tid < kO) {
@@ -206,17 +207,17 @@ __global__ void __launch_bounds__(kNT, 1)
         {
             const int jg = tid & 15, ig = tid >> 4;
             for (int q = 0; q < kT; q += 4) {
-                float4 a[2], dd[4];
+                float4 a[4], dd[4];
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    a[u] = *reinterpret_cast<const float4 *>(S.z1T + sw(ig * 2 + u, q));
+                for (int u = 0; u < 4; ++u) {
+                    a[u] = *reinterpret_cast<const float4 *>(S.z1T + sw(ig * 4 + u, q));
                     a[u].x = relu_np(a[u].x); a[u].y = relu_np(a[u].y);
                     a[u].z = relu_np(a[u].z); a[u].w = relu_np(a[u].w);
                 }
 #pragma unroll
                 for (int v = 0; v < 4; ++v) dd[v] = *reinterpret_cast<const float4 *>(S.z2T + sw(jg * 4 + v, q));
 #pragma unroll
-                for (int u = 0; u < 2; ++u)
+                for (int u = 0; u < 4; ++u)
 #pragma unroll
                     for (int v = 0; v < 4; ++v) {
                         float s = gW1[u][v];
@@ -263,19 +264,24 @@ __global__ void __launch_bounds__(kNT, 1)
         __syncthreads();
         // ---- dW0 += y^T delta1, db0 += sum delta1 ----
         {
-            const int jg = tid & 15, i = tid >> 4;
+            const int jg = tid & 15, ig = tid >> 4;
             for (int q = 0; q < kT; q += 4) {
-                const float4 a = *reinterpret_cast<const float4 *>(S.yT + sw(i, q));
+                float4 a[2], dd[4];
 #pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    const float4 dd = *reinterpret_cast<const float4 *>(S.z1T + sw(jg * 4 + v, q));
-                    float s = gW0[v];
-                    s = __fmaf_rn(a.x, dd.x, s);
-                    s = __fmaf_rn(a.y, dd.y, s);
-                    s = __fmaf_rn(a.z, dd.z, s);
-                    s = __fmaf_rn(a.w, dd.w, s);
-                    gW0[v] = s;
-                }
+                for (int u = 0; u < 2; ++u) a[u] = *reinterpret_cast<const float4 *>(S.yT + sw(ig * 2 + u, q));
+#pragma unroll
+                for (int v = 0; v < 4; ++v) dd[v] = *reinterpret_cast<const float4 *>(S.z1T + sw(jg * 4 + v, q));
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        float s = gW0[u][v];
+                        s = __fmaf_rn(a[u].x, dd[v].x, s);
+                        s = __fmaf_rn(a[u].y, dd[v].y, s);
+                        s = __fmaf_rn(a[u].z, dd[v].z, s);
+                        s = __fmaf_rn(a[u].w, dd[v].w, s);
+                        gW0[u][v] = s;
+                    }
             }
             if (tid < kH) {
                 float s = 0.0f;
@@ -327,15 +333,16 @@ __global__ void __launch_bounds__(kNT, 1)
     ACC *gW0p = gparams, *gb0p = gW0p + kI * kH, *gW1p = gb0p + kH, *gb1p = gW1p + kH * kH;
     ACC *gW2p = gb1p + kH, *gb2p = gW2p + kH * od;
     {
-        const int jg = tid & 15;
-        const int i0 = tid >> 4;
-#pragma unroll
-        for (int v = 0; v < 4; ++v) red_add(gW0p + i0 * kH + jg * 4 + v, gW0[v]);
+        const int jg = tid & 15, ig = tid >> 4;
 #pragma unroll
         for (int u = 0; u < 2; ++u)
 #pragma unroll
-            for (int v = 0; v < 4; ++v) red_add(gW1p + ((tid >> 4) * 2 + u) * kH + jg * 4 + v, gW1[u][v]);
-        const int k = tid & 63, j = (tid >> 6) & 3;
+            for (int v = 0; v < 4; ++v) red_add(gW0p + (ig * 2 + u) * kH + jg * 4 + v, gW0[u][v]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) red_add(gW1p + (ig * 4 + u) * kH + jg * 4 + v, gW1[u][v]);
+        const int k = tid & 63, j = tid >> 6;
         if (j < od) red_add(gW2p + k * od + j, gW2);
         if (tid < kH) {
             red_add(gb0p + tid, gB0);
@@ -378,7 +385,7 @@ int train_fused(const pg_grid *g, const pg_mlp *m, const float *xs, const float 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t ntiles = (B + kT - 1) / kT;
-    const int grd = (int)(ntiles < sms ? ntiles : sms);
+    const int grd = (int)(ntiles < 2 * sms ? ntiles : 2 * sms);
     const bool np4 = g->log2_np <= 2;
 #define PG_TRAIN_LAUNCH(D_, NP_, IDX)                                                                 \
     do {                                                                                              \

@@ -1,5 +1,7 @@
-"""tcgen05 building blocks: one kind::tf32 UMMA GEMM through TMEM against an
-fp64 reference (single pass at tf32 precision, 2-term split at ~fp32)."""
+"""tcgen05 building blocks: kind::tf32 UMMA GEMMs through TMEM against fp64
+references — K-major and MN-major shared-memory operands (the "RG" layout the
+fused kernels use), M = 128 and M = 64 accumulators, single pass and the
+2-term (hi + lo) split."""
 
 import numpy as np
 import pytest
@@ -8,21 +10,66 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
+def _run(A, B, code):
+    from paper_2312_17241_b200 import _lib
+    tA, tB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    tD = torch.full((128, 64), np.nan, device="cuda")
+    _lib.call("pg_selftest_umma_tf32", _lib.ptr(tA), _lib.ptr(tB), _lib.ptr(tD), code,
+              _lib.stream_ptr())
+    return tD.cpu().numpy()
+
+
+def _scaled_err(D, ref, A, B, transpose_a=False):
+    absA = np.abs(A.astype(np.float64))
+    denom = (absA.T if transpose_a else absA) @ np.abs(B.astype(np.float64)).T \
+        if not transpose_a else absA.T @ np.abs(B.astype(np.float64))
+    return np.abs(D - ref) / denom
+
+
 @pytest.mark.parametrize("split,tol", [(0, 3e-3), (1, 2e-6)])
-def test_umma_tf32_gemm(split, tol):
+def test_umma_kmajor_m128(split, tol):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    from paper_2312_17241_b200 import _lib
     rng = np.random.default_rng(split)
     A = rng.standard_normal((128, 32)).astype(np.float32)
     # B exactly representable in tf32 (like the fp16-rounded inference MLP)
     B = rng.standard_normal((64, 32)).astype(np.float16).astype(np.float32)
-    tA, tB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
-    tD = torch.zeros((128, 64), device="cuda")
-    _lib.call("pg_selftest_umma_tf32", _lib.ptr(tA), _lib.ptr(tB), _lib.ptr(tD), split,
-              _lib.stream_ptr())
-    D = tD.cpu().numpy()
+    D = _run(A, B, split)
     ref = A.astype(np.float64) @ B.astype(np.float64).T
     err = np.abs(D - ref) / (np.abs(A).astype(np.float64) @ np.abs(B).astype(np.float64).T)
-    print("max scaled error", err.max())
+    print("mode0 max scaled error", err.max())
     assert err.max() <= tol
+
+
+def test_umma_kmajor_k64():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    rng = np.random.default_rng(2)
+    A = rng.standard_normal((128, 64)).astype(np.float16).astype(np.float32)
+    B = rng.standard_normal((64, 64)).astype(np.float16).astype(np.float32)
+    D = _run(A, B, 2 << 4)
+    ref = A.astype(np.float64) @ B.astype(np.float64).T
+    np.testing.assert_allclose(D, ref, rtol=1e-5, atol=1e-4)
+
+
+def test_umma_mn_major_m64_layout():
+    """D[64x64] = A^T B with both operands MN-major (weight-gradient shape):
+    locate the M=64 accumulator rows in TMEM and check the values."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((128, 64)).astype(np.float16).astype(np.float32)
+    B = rng.standard_normal((128, 64)).astype(np.float16).astype(np.float32)
+    D = _run(A, B, 1 << 4)
+    ref = A.astype(np.float64).T @ B.astype(np.float64)   # [i][j]
+    where = {}
+    for lane in range(128):
+        row = D[lane]
+        if not np.all(np.isfinite(row)):
+            continue
+        for i in range(64):
+            if np.allclose(row, ref[i], rtol=1e-5, atol=1e-3):
+                where[lane] = i
+                break
+    print("M=64 accumulator rows by TMEM lane:", where)
+    assert sorted(where.values()) == list(range(64))
