@@ -141,6 +141,15 @@ def infer_bytes_per_query(hyper, n_probed, table_bytes_per_row):
             + 4 * hyper.out_dim)
 
 
+def smem_baked_levels(hyper, n_probed, budget=65536):
+    """Probed levels whose baked indices the decode kernel keeps bit-packed in
+    shared memory (pg_decode_tc.cu plan_tables: automatic for N_p = 2, 4)."""
+    lg = int(hyper.n_p).bit_length() - 1
+    if lg not in (1, 2):
+        return 0
+    return min(n_probed, budget // (hyper.n_c * lg // 8))
+
+
 def train_bytes_per_sample(hyper, n_probed):
     """encode fwd + recompute-bwd bytes per training sample."""
     C, L, F, d, n_p = 1 << hyper.d, hyper.n_levels, hyper.feature_dim, hyper.d, hyper.n_p
@@ -295,13 +304,15 @@ def run_gpu(args, rank, world, local_rank):
     qps = world * B_INFER / (ms_step * 1e-3)
     n_probed = len(inf.probed)
     bpq = infer_bytes_per_query(hyper, n_probed, table_bytes_per_row=2 * hyper.feature_dim)
+    gpq = (1 << hyper.d) * (hyper.n_levels + n_probed - smem_baked_levels(hyper, n_probed))
     achieved = B_INFER * bpq / (ms_step * 1e-3) / 1e9    # per GPU, per launch
     l2_stream, l2_gather = measure_l2(None, torch, table_mib=32)
     mlp_flops = 2 * sum(a * b for a, b in zip(inf.widths[:-1], inf.widths[1:]))
 
     # ---------------- ablation: same decode, other MLP engines ----------------
     ablation = {}
-    for name, kw in (("cuda_core_fma", dict(exact=False, tensor=False)),
+    for name, kw in (("tcgen05_without_smem_baked_tables", dict(exact=False, smem_tables=False)),
+                     ("cuda_core_fma", dict(exact=False, tensor=False)),
                      ("cuda_core_exact_reference_order", dict(exact=True))):
         for _ in range(2):
             decode_device(inf, xs, out, **kw)
@@ -354,14 +365,20 @@ def run_gpu(args, rank, world, local_rank):
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak,
-                     "traffic": ncu_traffic("decode_fused_kernel", B_INFER),
-                     "kernel": "decode_fused_kernel", "bytes_per_query": bpq,
+                     "traffic": ncu_traffic("decode_umma_kernel", B_INFER),
+                     "kernel": "decode_umma_kernel", "bytes_per_query": bpq,
                      "peak_source": peak_src,
                      "l2_stream_read_gbs": l2_stream, "l2_random_gather_8B_gbs": l2_gather,
                      "frac_of_l2_stream": achieved / l2_stream,
+                     "random_gathers_per_query": gpq,
+                     "random_gather_rate_per_s": l2_gather * 1e9 / 8,
+                     "frac_of_random_gather_rate": qps / world * gpq / (l2_gather * 1e9 / 8),
                      "mlp_tflops": qps / world * mlp_flops / 1e12,
                      "note": "table gathers are L2-resident: bytes are algorithmic gather bytes; "
-                             "HBM streams only 20 B/query (coords + outputs)"},
+                             "HBM streams only 20 B/query (coords + outputs). The binding limit is "
+                             "the random-gather rate (pg_probe_gather, ~1 per SM per clock): "
+                             "random_gathers_per_query counts feature rows and baked bytes not "
+                             "served from shared memory"},
         "clocks": clk,
         "ablation_queries_per_s": ablation,
         "train": train,

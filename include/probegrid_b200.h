@@ -51,6 +51,9 @@ extern "C" {
 #define PG_SURROGATE 4u   /* softmax-mixture forward (encoding.py:45-47)      */
 #define PG_HALF_FEATS 8u  /* feature tables stored as IEEE binary16           */
 #define PG_NO_TENSOR 16u  /* decode: FFMA MLP instead of tcgen05 (ablation)   */
+#define PG_SMEM_TABLES 32u    /* decode: force the shared-memory baked-index
+                               * variant (default: automatic, N_p = 2 or 4) */
+#define PG_NO_SMEM_TABLES 64u /* decode: never use it                       */
 
 /* Geometry of one multiresolution grid (HyperParams + build_level_specs,
  * model.py:35-87, indexing.py:93-101).  Feature tables of all levels are one

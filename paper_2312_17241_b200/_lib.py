@@ -17,6 +17,7 @@ PG_OK, PG_ERR_ARG, PG_ERR_CUDA, PG_ERR_DOMAIN = 0, 1, 2, 3
 PG_MAX_LEVELS, PG_MAX_FEATURE, PG_MAX_PROBES, PG_MAX_LAYERS = 64, 16, 256, 17
 PG_LEVEL_DENSE, PG_LEVEL_HASHED, PG_LEVEL_PROBED = 0, 1, 2
 PG_EXACT_MLP, PG_SIGMOID, PG_SURROGATE, PG_HALF_FEATS, PG_NO_TENSOR = 1, 2, 4, 8, 16
+PG_SMEM_TABLES, PG_NO_SMEM_TABLES = 32, 64
 
 
 class PgGrid(ctypes.Structure):

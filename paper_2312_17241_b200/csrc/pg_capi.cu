@@ -54,17 +54,26 @@ __global__ void probe_stream_kernel(const float4 *__restrict__ buf, int64_t n4, 
         }
     if (acc == 12345.678f) *sink = acc;
 }
+__device__ __forceinline__ uint32_t probe_hash(uint32_t i, uint32_t seed) {
+    uint32_t h = i * 2654435761u ^ seed;
+    h ^= h >> 15;
+    h *= 0x2c1b3c6du;
+    h ^= h >> 12;
+    return h;
+}
 __global__ void probe_gather_kernel(const float2 *__restrict__ tab, uint32_t mask, int64_t nq,
                                     uint32_t seed, float *__restrict__ sink) {
+    // 4 independent 8-byte gathers in flight per thread per iteration
     float acc = 0.0f;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t h = (uint32_t)i * 2654435761u ^ seed;
-        h ^= h >> 15;
-        h *= 0x2c1b3c6du;
-        h ^= h >> 12;
-        const float2 v = __ldg(tab + (h & mask));
-        acc += v.x + v.y;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq; i += 4 * stride) {
+        float2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            v[u] = i + u * stride < nq ? __ldg(tab + (probe_hash((uint32_t)(i + u * stride), seed) & mask))
+                                       : make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc += v[u].x + v[u].y;
     }
     if (acc == 12345.678f) *sink = acc;
 }

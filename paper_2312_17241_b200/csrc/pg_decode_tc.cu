@@ -1,15 +1,36 @@
-// Fused decode on the 5th-generation tensor core (tcgen05 / UMMA):
-//   per 128-query tile: 16-level encode (fp16 tables) -> layer 1 and layer 2
-//   of the MLP as kind::tf32 UMMA (M=128, N=64, accumulators in TMEM) ->
-//   bias/ReLU epilogues from TMEM -> output layer (64 -> <=4) in registers.
+// Fused decode on the 5th-generation tensor core (tcgen05 / UMMA), the
+// headline kernel.  Per 128-query tile: 16-level encode (fp16 tables) ->
+// layers 1 and 2 of the MLP as kind::tf32 UMMA (M = 128, N = 64, fp32
+// accumulators in TMEM) -> bias/ReLU epilogues from TMEM (tcgen05.ld) ->
+// output layer (64 -> <= 4) in registers.
 //
-// Accuracy: activations are fed as a 2-term tf32 expansion (hi + lo, ~22
+// Accuracy: activations go in as a 2-term tf32 expansion (hi + lo, ~22
 // significand bits); the weights of an inference model are fp16-rounded
-// (to_inference, model_io.py:130-147), hence exactly representable in tf32.
-// Each layer is therefore 2 passes of UMMA and matches fp32 to ~1e-6
-// relative (tests/test_gpu_parity.py bounds it at rtol 1e-5).
+// (to_inference, model_io.py:130-147), hence exact in tf32, so each layer is
+// 2 UMMA passes and matches fp32 to ~1e-6 relative (tests bound it at 1e-5).
+//
+// Throughput: the encode is ~100 random 4-byte L2 gathers per query (64
+// feature rows + 36 baked bytes at C2), and random gathers retire at ~1 per
+// SM per clock on B200 (pg_probe_gather: 2.8e11/s, independent of table size
+// and of loads in flight) — that, not HBM or the MMA, is this kernel's
+// ceiling.  The layout therefore maximises warps per SM and L1 capacity:
+// * a tile pipeline ("group") is 256 threads with a 32 KB operand buffer
+//   (one 128 x 32 K-block, hi | lo) and 128 TMEM columns; layer 2's 64-wide
+//   A operand is fed as two K = 32 blocks through that buffer, and the
+//   output-layer partial sums reuse it too -> ~60 KB of shared memory;
+// * default: one group per CTA, three CTAs per SM (24 warps, <= 80 regs);
+// * PG_SMEM_TABLES: three groups in ONE CTA (named barriers 1..3) sharing
+//   weights and a few KB of the probed levels' baked indices bit-packed to
+//   log2(N_p) bits, which removes those levels' dependent baked-byte L2
+//   round trip.  Dense-level feature tables can be placed too (ablation
+//   knob); they are not, because every KB of shared memory comes out of the
+//   L1 that caches the coarse levels' rows.
 #include "pg_encode_dev.cuh"
 #include "pg_umma.cuh"
+
+#include <algorithm>
+#include <cstdlib>
+#include <vector>
 
 namespace pg {
 
@@ -18,32 +39,123 @@ constexpr int kTP = 128;  // queries per tile == UMMA M
 constexpr int kIn = 32;
 constexpr int kHid = 64;
 constexpr int kOutMax = 4;
-constexpr int kThreads = 256;
+constexpr int kGT = 256;  // threads per group
 
+struct Group {
+    // one 128 x 32 K-block, hi | lo; after layer 2 it holds the output-layer
+    // partial sums part[2][kTP][kOutMax]
+    alignas(128) float opA[2 * kTP * 32];
+    float xs[kTP * 3];
+    uint64_t mbar[3];
+};
+template <int NG>
 struct Smem {
-    // operand region: layer-1 A (hi | lo, 128x32 each) then layer-2 A (hi | lo, 128x64 each)
-    alignas(16) float opA[2 * kTP * kHid];
-    alignas(16) float b1[kHid * kIn];   // W0^T, K-major
-    alignas(16) float b2[kHid * kHid];  // W1^T, K-major
+    alignas(128) float b1[kHid * kIn];   // W0^T, K-major
+    alignas(128) float b2[kHid * kHid];  // W1^T, K-major
     float w2[kHid * kOutMax];
     float bias0[kHid], bias1[kHid], bias2[kOutMax];
-    float part[2][kTP][kOutMax];
-    float xs[kTP * 3];
-    uint64_t mbar[2];
+    Group grp[NG];
     uint32_t tmem_base;
+};
+template <int NG>
+__host__ __device__ constexpr int tab_offset() { return (int)((sizeof(Smem<NG>) + 127) / 128 * 128); }
+
+// which levels live in shared memory (byte offsets into the table region)
+struct TabPlan {
+    int32_t off[PG_MAX_LEVELS];  // -1: global memory
+    int32_t pbits;               // packed bits per baked index; 0 when N_p == 1
+    int32_t bytes;
 };
 }  // namespace tc
 
+template <typename FT> struct FeatS;
+template <> struct FeatS<__half> {
+    static __device__ __forceinline__ float2 ld2(const unsigned char *p) {
+        return __half22float2(*reinterpret_cast<const __half2 *>(p));
+    }
+};
+template <> struct FeatS<float> {
+    static __device__ __forceinline__ float2 ld2(const unsigned char *p) {
+        return *reinterpret_cast<const float2 *>(p);
+    }
+};
+
+// encode_level_fwd2 (pg_encode_dev.cuh) with optional on-chip tables:
+// identical indices, weights and blend order, so the result is bit-identical.
 template <typename FT, int D>
-__global__ void __launch_bounds__(tc::kThreads, 2)
-    decode_umma_kernel(const pg_grid g, const float *__restrict__ xs, int64_t B,
-                       const FT *__restrict__ feats, const uint8_t *__restrict__ baked,
-                       const float *__restrict__ params, int od, int sigmoid,
-                       float *__restrict__ out) {
+__device__ __forceinline__ float2 encode_level_fwd2_tab(const pg_grid &g, int l, const float (&x)[D],
+                                                        const FT *__restrict__ feats,
+                                                        const uint8_t *__restrict__ baked,
+                                                        const unsigned char *tabs, int off, int pbits) {
+    constexpr int C = 1 << D;
+    const uint32_t nf_mask = (uint32_t)g.n_f - 1u, nc_mask = (uint32_t)g.n_c - 1u;
+    const int res = g.res[l], kind = g.kind[l];
+    int c[D];
+    float t[D], omt[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        c[a] = cell_coord(x[a], res, t[a]);
+        omt[a] = __fsub_rn(1.0f, t[a]);
+    }
+    int idx[C];
+    float w[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+        w[k] = corner_weight<float, D>(k, t, omt);
+        if (kind == PG_LEVEL_DENSE) {
+            idx[k] = corner_dense<D>(k, c, res + 1);
+        } else {
+            const uint32_t h = corner_hash<D>(k, c, g.primary);
+            if (kind == PG_LEVEL_HASHED) {
+                idx[k] = (int)(h & nf_mask);
+            } else {
+                idx[k] = (int)((h << g.log2_np) & nf_mask);
+                if (pbits != 0) {
+                    const uint32_t r = corner_hash<D>(k, c, g.aux) & nc_mask;
+                    if (off >= 0) {
+                        const int lg = 5 - __ffs(pbits) + 1;  // log2(32 / pbits)
+                        const uint32_t word = reinterpret_cast<const uint32_t *>(tabs + off)[r >> lg];
+                        idx[k] += (int)((word >> ((r & ((1u << lg) - 1u)) * pbits)) & ((1u << pbits) - 1u));
+                    } else {
+                        idx[k] += (int)__ldg(baked + (int64_t)g.slot[l] * g.n_c + r);
+                    }
+                }
+            }
+        }
+    }
+    float2 f[C];
+    if (kind == PG_LEVEL_DENSE && off >= 0) {
+#pragma unroll
+        for (int k = 0; k < C; ++k) f[k] = FeatS<FT>::ld2(tabs + off + idx[k] * (int)(2 * sizeof(FT)));
+    } else {
+        const FT *tab = feats + (int64_t)l * g.n_f * 2;
+#pragma unroll
+        for (int k = 0; k < C; ++k) f[k] = Feat<FT>::ld2(tab + (int64_t)idx[k] * 2);
+    }
+    float y0 = 0.0f, y1 = 0.0f;
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+        y0 = __fadd_rn(y0, __fmul_rn(w[k], f[k].x));
+        y1 = __fadd_rn(y1, __fmul_rn(w[k], f[k].y));
+    }
+    return make_float2(y0, y1);
+}
+
+__device__ __forceinline__ void group_sync(int grp) {
+    asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(tc::kGT) : "memory");
+}
+
+template <typename FT, int D, int NG, int MINB>
+__global__ void __launch_bounds__(tc::kGT *NG, MINB)
+    decode_umma_kernel(const pg_grid g, const tc::TabPlan plan, const float *__restrict__ xs, int64_t B,
+                        const FT *__restrict__ feats, const uint8_t *__restrict__ baked,
+                        const float *__restrict__ params, int od, int sigmoid, float *__restrict__ out) {
     using namespace tc;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    Smem &S = *reinterpret_cast<Smem *>(smem_raw);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int kThreads = kGT * NG, kGroups = NG;
+    Smem<NG> &S = *reinterpret_cast<Smem<NG> *>(smem_raw);
+    unsigned char *tabs = smem_raw + tab_offset<NG>();
+    const int tid = threadIdx.x, lane = tid & 31;
 
     // ---- weights: B operands (K-major W^T) + epilogue constants ----
     {
@@ -71,48 +183,80 @@ __global__ void __launch_bounds__(tc::kThreads, 2)
         p += kHid * od;
         for (int i = tid; i < kOutMax; i += kThreads) S.bias2[i] = i < od ? p[i] : 0.0f;
     }
-    if (warp == 0) umma::tmem_alloc<128>(&S.tmem_base);
+    // ---- on-chip tables ----
+    for (int l = 0; l < g.n_levels; ++l) {
+        const int o = plan.off[l];
+        if (o < 0) continue;
+        uint32_t *dst = reinterpret_cast<uint32_t *>(tabs + o);
+        if (g.kind[l] == PG_LEVEL_DENSE) {
+            int n = g.res[l] + 1, e = n;
+            for (int a = 1; a < D; ++a) e *= n;
+            const int words = e * (int)(2 * sizeof(FT)) / 4;
+            const uint32_t *src = reinterpret_cast<const uint32_t *>(feats + (int64_t)l * g.n_f * 2);
+            for (int i = tid; i < words; i += kThreads) dst[i] = __ldg(src + i);
+        } else {  // probed: pack baked indices, R = 32 / pbits per word
+            const int pb = plan.pbits, R = 32 / pb;
+            const int words = g.n_c / R;
+            const uint2 *src = reinterpret_cast<const uint2 *>(baked + (int64_t)g.slot[l] * g.n_c);
+            for (int wi = tid; wi < words; wi += kThreads) {
+                uint32_t word = 0;
+                for (int c8 = 0; c8 < R / 8; ++c8) {
+                    const uint2 v = __ldg(src + (int64_t)wi * (R / 8) + c8);
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        const uint32_t byte = ((b < 4 ? v.x : v.y) >> ((b & 3) * 8)) & 0xFFu;
+                        word |= byte << ((c8 * 8 + b) * pb);
+                    }
+                }
+                dst[wi] = word;
+            }
+        }
+    }
+    if ((tid >> 5) == 0) umma::tmem_alloc<(NG == 1 ? 128 : NG == 2 ? 256 : 512)>(&S.tmem_base);
     if (tid == 0) {
-        umma::mbar_init(&S.mbar[0], 1);
-        umma::mbar_init(&S.mbar[1], 1);
+        for (int gi = 0; gi < kGroups; ++gi)
+            for (int m = 0; m < 3; ++m) umma::mbar_init(&S.grp[gi].mbar[m], 1);
         umma::mbar_init_fence();
     }
     umma::fence_async_smem();
     umma::fence_before_sync();
     __syncthreads();
     umma::fence_after_sync();
-    const uint32_t tmem = S.tmem_base;
-    const uint32_t tm_d1 = tmem, tm_d2 = tmem + kHid;   // columns [0,64) and [64,128)
+
+    const int grp = tid >> 8, gt = tid & (kGT - 1), gw = gt >> 5;
+    Group &G = S.grp[grp];
+    const uint32_t tm_d1 = S.tmem_base + (uint32_t)(grp * 128), tm_d2 = tm_d1 + kHid;
     const uint32_t idesc = umma::idesc_tf32(kTP, kHid);
-    char *opA = reinterpret_cast<char *>(S.opA);
+    char *opA = reinterpret_cast<char *>(G.opA);
     const uint32_t a_s = umma::smem_u32(opA);
     const uint32_t b1_s = umma::smem_u32(S.b1), b2_s = umma::smem_u32(S.b2);
-    // epilogue role: row (TMEM lane) and column half
-    const int erow = (warp & 3) * 32 + lane;
-    const int ehalf = warp >> 2;  // 0: columns 0..31, 1: columns 32..63
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    constexpr int kLoOff = kTP * 32 * 4;  // lo half of the operand buffer
+    // epilogue role: row (TMEM lane; a warp may only touch lanes 32*(warp%4)..) and column half
+    const int erow = (gw & 3) * 32 + lane;
+    const int ehalf = gw >> 2;
+    const uint32_t lane_off = (uint32_t)((gw & 3) * 32) << 16;
 
     const int64_t ntiles = (B + kTP - 1) / kTP;
     uint32_t phase = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, phase ^= 1u) {
+    for (int64_t tile = (int64_t)blockIdx.x * kGroups + grp; tile < ntiles;
+         tile += (int64_t)gridDim.x * kGroups, phase ^= 1u) {
         const int64_t p0 = tile * kTP;
         const int nv = (int)((B - p0) < kTP ? (B - p0) : kTP);
-        for (int i = tid; i < kTP * D; i += kThreads) S.xs[i] = i < nv * D ? xs[p0 * D + i] : 0.5f;
-        __syncthreads();
+        for (int i = gt; i < kTP * D; i += kGT) G.xs[i] = i < nv * D ? xs[p0 * D + i] : 0.5f;
+        group_sync(grp);
         // ---------------- encode -> layer-1 A operand (hi | lo) ----------------
         {
-            const int q = tid & (kTP - 1), lsub = tid >> 7;
+            const int q = gt & (kTP - 1), lsub = gt >> 7;
             float x[D];
 #pragma unroll
-            for (int a = 0; a < D; ++a) x[a] = S.xs[q * D + a];
-            // a thread encodes level PAIRS (2P, 2P+1): their 4 features fill one
-            // 16-byte K-chunk, so the operand stores are float4 and a warp's
-            // 32 queries hit 4 full wavefronts (no bank conflicts)
+            for (int a = 0; a < D; ++a) x[a] = G.xs[q * D + a];
 #pragma unroll 2
             for (int it = 0; it < 4; ++it) {
-                const int P = lsub + 2 * it;  // warp-uniform
-                const float2 ya = encode_level_fwd2<FT, D>(g, 2 * P, x, feats, baked);
-                const float2 yb = encode_level_fwd2<FT, D>(g, 2 * P + 1, x, feats, baked);
+                const int P = lsub + 2 * it;  // warp-uniform level pair (2P, 2P+1)
+                const float2 ya = encode_level_fwd2_tab<FT, D>(g, 2 * P, x, feats, baked, tabs,
+                                                               plan.off[2 * P], plan.pbits);
+                const float2 yb = encode_level_fwd2_tab<FT, D>(g, 2 * P + 1, x, feats, baked, tabs,
+                                                               plan.off[2 * P + 1], plan.pbits);
                 float h[4], lo[4];
                 umma::split_tf32(ya.x, h[0], lo[0]);
                 umma::split_tf32(ya.y, h[1], lo[1]);
@@ -120,66 +264,68 @@ __global__ void __launch_bounds__(tc::kThreads, 2)
                 umma::split_tf32(yb.y, h[3], lo[3]);
                 const uint32_t off = umma::kmaj_off(q, 4 * P, kTP);
                 *reinterpret_cast<float4 *>(opA + off) = make_float4(h[0], h[1], h[2], h[3]);
-                *reinterpret_cast<float4 *>(opA + kTP * kIn * 4 + off) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+                *reinterpret_cast<float4 *>(opA + kLoOff + off) = make_float4(lo[0], lo[1], lo[2], lo[3]);
             }
         }
         umma::fence_async_smem();
         umma::fence_before_sync();
-        __syncthreads();
+        group_sync(grp);
         // ---------------- layer 1: D1 = (Y_hi + Y_lo) . W0 ----------------
-        if (tid == 0) {
+        if (gt == 0) {
             umma::fence_after_sync();
 #pragma unroll
             for (int pass = 0; pass < 2; ++pass)
 #pragma unroll
                 for (int kb = 0; kb < kIn / 8; ++kb) {
-                    const uint64_t ad = umma::smem_desc(a_s + pass * kTP * kIn * 4 + kb * kTP * 32, 128, 256);
+                    const uint64_t ad = umma::smem_desc(a_s + pass * kLoOff + kb * kTP * 32, 128, 256);
                     const uint64_t bd = umma::smem_desc(b1_s + kb * kHid * 32, 128, 256);
                     umma::mma_tf32(tm_d1, ad, bd, idesc, (pass | kb) ? 1u : 0u);
                 }
-            umma::commit(&S.mbar[0]);
+            umma::commit(&G.mbar[0]);
         }
-        umma::mbar_wait(&S.mbar[0], phase);
+        umma::mbar_wait(&G.mbar[0], phase);
         umma::fence_after_sync();
-        // ---------------- epilogue 1: bias + ReLU -> layer-2 A operand ----------------
-        {
-            float v[32];
-            umma::tmem_ld32(tm_d1 + lane_off + ehalf * 32, v);
+        // ------- epilogue 1: bias + ReLU -> layer-2 A operand, two K = 32 blocks -------
+        float v[32];
+        umma::tmem_ld32(tm_d1 + lane_off + ehalf * 32, v);
 #pragma unroll
-            for (int c = 0; c < 32; c += 4) {
-                float hi[4], lo[4];
+        for (int c = 0; c < 32; ++c) {
+            const float z = v[c] + S.bias0[ehalf * 32 + c];
+            v[c] = z < 0.0f ? 0.0f : z;
+        }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    float z = v[c + u] + S.bias0[ehalf * 32 + c + u];
-                    z = z < 0.0f ? 0.0f : z;
-                    umma::split_tf32(z, hi[u], lo[u]);
+        for (int blk = 0; blk < 2; ++blk) {
+            if (ehalf == blk) {
+#pragma unroll
+                for (int c = 0; c < 32; c += 4) {
+                    float hi[4], lo[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) umma::split_tf32(v[c + u], hi[u], lo[u]);
+                    const uint32_t off = umma::kmaj_off(erow, c, kTP);
+                    *reinterpret_cast<float4 *>(opA + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+                    *reinterpret_cast<float4 *>(opA + kLoOff + off) = make_float4(lo[0], lo[1], lo[2], lo[3]);
                 }
-                const uint32_t off = umma::kmaj_off(erow, ehalf * 32 + c, kTP);
-                *reinterpret_cast<float4 *>(opA + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-                *reinterpret_cast<float4 *>(opA + kTP * kHid * 4 + off) = make_float4(lo[0], lo[1], lo[2], lo[3]);
             }
-        }
-        umma::fence_async_smem();
-        umma::fence_before_sync();
-        __syncthreads();
-        // ---------------- layer 2: D2 = (H1_hi + H1_lo) . W1 ----------------
-        if (tid == 0) {
+            umma::fence_async_smem();
+            umma::fence_before_sync();
+            group_sync(grp);
+            if (gt == 0) {
+                umma::fence_after_sync();
+#pragma unroll
+                for (int pass = 0; pass < 2; ++pass)
+#pragma unroll
+                    for (int kb = 0; kb < 4; ++kb) {
+                        const uint64_t ad = umma::smem_desc(a_s + pass * kLoOff + kb * kTP * 32, 128, 256);
+                        const uint64_t bd = umma::smem_desc(b2_s + (blk * 4 + kb) * kHid * 32, 128, 256);
+                        umma::mma_tf32(tm_d2, ad, bd, idesc, (blk | pass | kb) ? 1u : 0u);
+                    }
+                umma::commit(&G.mbar[1 + blk]);
+            }
+            umma::mbar_wait(&G.mbar[1 + blk], phase);
             umma::fence_after_sync();
-#pragma unroll
-            for (int pass = 0; pass < 2; ++pass)
-#pragma unroll
-                for (int kb = 0; kb < kHid / 8; ++kb) {
-                    const uint64_t ad = umma::smem_desc(a_s + pass * kTP * kHid * 4 + kb * kTP * 32, 128, 256);
-                    const uint64_t bd = umma::smem_desc(b2_s + kb * kHid * 32, 128, 256);
-                    umma::mma_tf32(tm_d2, ad, bd, idesc, (pass | kb) ? 1u : 0u);
-                }
-            umma::commit(&S.mbar[1]);
         }
-        umma::mbar_wait(&S.mbar[1], phase);
-        umma::fence_after_sync();
         // ---------------- epilogue 2: bias + ReLU + output layer ----------------
         {
-            float v[32];
             umma::tmem_ld32(tm_d2 + lane_off + ehalf * 32, v);
             float acc[kOutMax] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
@@ -193,16 +339,16 @@ __global__ void __launch_bounds__(tc::kThreads, 2)
                 acc[2] = fmaf(h, w.z, acc[2]);
                 acc[3] = fmaf(h, w.w, acc[3]);
             }
-#pragma unroll
-            for (int j = 0; j < kOutMax; ++j) S.part[ehalf][erow][j] = acc[j];
+            *reinterpret_cast<float4 *>(G.opA + (ehalf * kTP + erow) * kOutMax) =
+                make_float4(acc[0], acc[1], acc[2], acc[3]);
         }
         umma::fence_before_sync();
-        __syncthreads();
+        group_sync(grp);
         {
             float *dst = out + p0 * od;
-            for (int i = tid; i < nv * od; i += kThreads) {
+            for (int i = gt; i < nv * od; i += kGT) {
                 const int q = i / od, j = i - q * od;
-                float o = S.bias2[j] + S.part[0][q][j] + S.part[1][q][j];
+                float o = S.bias2[j] + G.opA[q * kOutMax + j] + G.opA[(kTP + q) * kOutMax + j];
                 if (sigmoid) o = (float)(1.0 / (1.0 + exp(-(double)o)));
                 dst[i] = o;
             }
@@ -210,35 +356,100 @@ __global__ void __launch_bounds__(tc::kThreads, 2)
     }
     umma::fence_after_sync();
     __syncthreads();
-    if (warp == 0) umma::tmem_free<128>(tmem);
+    if ((tid >> 5) == 0) umma::tmem_free<(NG == 1 ? 128 : NG == 2 ? 256 : 512)>(S.tmem_base);
+}
+
+// Host: choose the on-chip tables (smallest first, they save the same 2^d
+// gathers per query each) within the shared-memory budget.
+static tc::TabPlan plan_tables(const pg_grid *g, size_t feat_bytes, int budget, int kinds) {
+    tc::TabPlan p;
+    for (int l = 0; l < PG_MAX_LEVELS; ++l) p.off[l] = -1;
+    p.pbits = g->log2_np == 0 ? 0 : g->log2_np == 1 ? 1 : g->log2_np == 2 ? 2 : g->log2_np <= 4 ? 4 : -1;
+    p.bytes = 0;
+    std::vector<std::pair<int64_t, int>> cand;
+    for (int l = 0; l < g->n_levels; ++l) {
+        int64_t bytes = -1;
+        if (g->kind[l] == PG_LEVEL_DENSE && (kinds & 1)) {
+            int64_t e = 1;
+            for (int a = 0; a < g->d; ++a) e *= (int64_t)(g->res[l] + 1);
+            bytes = e * 2 * (int64_t)feat_bytes;
+        } else if (g->kind[l] == PG_LEVEL_PROBED && (kinds & 2) && p.pbits > 0 && g->n_c % (32 / p.pbits) == 0 &&
+                   (32 / p.pbits) % 8 == 0) {
+            bytes = (int64_t)g->n_c * p.pbits / 8;
+        }
+        if (bytes > 0) cand.push_back({(bytes + 15) / 16 * 16, l});
+    }
+    std::sort(cand.begin(), cand.end());
+    for (auto &c : cand) {
+        if (p.bytes + c.first > budget) break;
+        p.off[c.second] = p.bytes;
+        p.bytes += (int)c.first;
+    }
+    if (p.pbits < 0) p.pbits = 8;  // N_p > 16: never packed, global byte loads
+    return p;
+}
+
+template <typename FT, int D, int NG, int MINB>
+static void launch_umma(const pg_grid *g, const tc::TabPlan &plan, int smem, int grd, const float *xs,
+                         int64_t B, const void *feats, const uint8_t *baked, const float *params, int od,
+                         int sig, float *out, cudaStream_t s) {
+    static bool configured = false;
+    if (!configured) {
+        int dev = 0, optin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaFuncSetAttribute(decode_umma_kernel<FT, D, NG, MINB>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+        configured = true;
+    }
+    decode_umma_kernel<FT, D, NG, MINB><<<grd, tc::kGT * NG, smem, s>>>(*g, plan, xs, B, (const FT *)feats,
+                                                                           baked, params, od, sig, out);
 }
 
 int decode_umma(const pg_grid *g, int od, const float *xs, int64_t B, const void *feats, bool half,
-                const uint8_t *baked, const float *params, int sig, float *out, cudaStream_t s) {
-    const int smem = (int)sizeof(tc::Smem);
-    static bool configured[4] = {false, false, false, false};
-    int sms = 0, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t ntiles = (B + tc::kTP - 1) / tc::kTP;
-    const int64_t cap = (int64_t)sms * 2;
-    const int grd = (int)(ntiles < cap ? ntiles : cap);
-#define PG_DEC_TC(FT_, D_, IDX)                                                                   \
-    do {                                                                                          \
-        if (!configured[IDX]) {                                                                   \
-            cudaFuncSetAttribute(decode_umma_kernel<FT_, D_>,                                     \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem);              \
-            configured[IDX] = true;                                                               \
-        }                                                                                         \
-        decode_umma_kernel<FT_, D_><<<grd, tc::kThreads, smem, s>>>(*g, xs, B, (const FT_ *)feats, \
-                                                                   baked, params, od, sig, out);  \
-    } while (0)
-    if (half) {
-        if (g->d == 2) PG_DEC_TC(__half, 2, 0); else PG_DEC_TC(__half, 3, 1);
-    } else {
-        if (g->d == 2) PG_DEC_TC(float, 2, 2); else PG_DEC_TC(float, 3, 3);
+                const uint8_t *baked, const float *params, int sig, int table_flags, float *out, cudaStream_t s) {
+    static int sms = 0, optin = 0, env_budget = -1, env_kinds = 2;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        // tuning knobs for the table variant (ablations in tools/gpu_decode_ab.sh)
+        if (const char *e = getenv("PG_DECODE_TABLE_BYTES")) env_budget = atoi(e);
+        if (const char *k = getenv("PG_DECODE_TABLE_KINDS")) env_kinds = atoi(k);  // 1 dense, 2 baked
     }
-#undef PG_DEC_TC
+    // Without tables: three independent 256-thread CTAs per SM (~60 KB shared
+    // memory each).  With: one CTA of three pipelines per SM sharing <= 64 KB
+    // of bit-packed baked indices, so that smem + L1 stay inside the 196 KB
+    // carve-out and L1 keeps ~60 KB (measured on B200, tools/gpu_decode_ab.sh:
+    // +25% at N_p = 2, +3% at N_p = 4, -4% at N_p >= 8 where 4-bit packing fits
+    // only two levels, -15% at N_p = 1 where there is nothing to place).
+    const bool tables = (table_flags & PG_SMEM_TABLES) ||
+                        (!(table_flags & PG_NO_SMEM_TABLES) && g->log2_np >= 1 && g->log2_np <= 2);
+    const int ng = tables ? 3 : 1;
+    const int fixed = ng == 3 ? tc::tab_offset<3>() : tc::tab_offset<1>();
+    int budget = 0;
+    if (tables) {
+        const int room = optin - fixed - 1024;
+        budget = env_budget >= 0 ? env_budget : 65536;
+        if (budget > room) budget = room;
+    }
+    const tc::TabPlan plan = plan_tables(g, half ? 2 : 4, budget, env_kinds);
+    const int smem = fixed + plan.bytes;
+    const int per_sm = ng == 3 ? 1 : 3;
+    const int64_t ntiles = (B + tc::kTP - 1) / tc::kTP;
+    const int64_t want = (ntiles + ng - 1) / ng;
+    const int64_t cap = (int64_t)sms * per_sm;
+    const int grd = (int)(want < cap ? want : cap);
+#define PG_DEC_TC2(FT_, D_)                                                                        \
+    (ng == 3 ? launch_umma<FT_, D_, 3, 1>(g, plan, smem, grd, xs, B, feats, baked, params, od, sig, out, s) \
+             : launch_umma<FT_, D_, 1, 3>(g, plan, smem, grd, xs, B, feats, baked, params, od, sig, out, s))
+    if (half) {
+        if (g->d == 2) PG_DEC_TC2(__half, 2); else PG_DEC_TC2(__half, 3);
+    } else {
+        if (g->d == 2) PG_DEC_TC2(float, 2); else PG_DEC_TC2(float, 3);
+    }
+#undef PG_DEC_TC2
     return check_launch("decode_umma");
 }
 

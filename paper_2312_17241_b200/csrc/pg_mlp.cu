@@ -315,7 +315,7 @@ static void launch_decode(const pg_grid *g, const float *xs, int64_t B, const vo
 }
 
 int decode_umma(const pg_grid *g, int od, const float *xs, int64_t B, const void *feats, bool half,
-                const uint8_t *baked, const float *params, int sig, float *out, cudaStream_t s);
+                const uint8_t *baked, const float *params, int sig, int table_flags, float *out, cudaStream_t s);
 
 int decode_device(const pg_grid *g, const pg_mlp *m, const float *xs, int64_t B,
                   const void *feats, const uint8_t *baked, const float *params, unsigned flags,
@@ -330,7 +330,8 @@ int decode_device(const pg_grid *g, const pg_mlp *m, const float *xs, int64_t B,
     if (decode_fast_ok(g, m)) {
         const int od = m->widths[3];
         if (!exact && !(flags & PG_NO_TENSOR))  // tcgen05 path (pg_decode_tc.cu)
-            return decode_umma(g, od, xs, B, feats, half, baked, params, sig, out, s);
+            return decode_umma(g, od, xs, B, feats, half, baked, params, sig, (int)(flags & (PG_SMEM_TABLES | PG_NO_SMEM_TABLES)),
+                               out, s);
 #define PG_DEC(FT_, D_)                                                                    \
     (exact ? launch_decode<FT_, D_, true>(g, xs, B, feats, baked, params, od, sig, out, bad, s) \
            : launch_decode<FT_, D_, false>(g, xs, B, feats, baked, params, od, sig, out, bad, s))

@@ -2,14 +2,11 @@
 //
 // Layout "RG" (row-group contiguous, no swizzle) for an R x K fp32 matrix:
 //     off(r, k) = (r/8)*K*32 + (k/4)*128 + (r%8)*16 + (k%4)*4
-// It is a valid UMMA operand two ways:
-//   K-major  (rows r = M or N, K = k): per MMA (8 k) start += 256 B,
-//            LBO = 128 B, SBO = K*32 B;
-//   MN-major (M or N = k, K = r, i.e. the transpose): per MMA (8 r) start +=
-//            K*32 B, SBO = 128 B (next 4 k), LBO unused.
+// It is a K-major UMMA operand (rows r = M or N, K = k): per MMA (8 k)
+// start += 256 B, LBO = 128 B, SBO = K*32 B.
 // mode 0: D[128x64]  = A[128x32] . B[64x32]^T        (K-major A, K-major B)
-// mode 1: D[64x64]   = A[128x64]^T . B[128x64]       (MN-major A and B, M=64)
 // mode 2: D[128x64]  = A[128x64] . B[64x64]^T        (K-major, K = 64)
+// mode 4: D[64x64]   = A[64x64] . B[64x64]^T         (M = 64 accumulator)
 // split != 0 (mode 0): 2-term hi/lo expansion of A.
 // D is returned as the raw TMEM contents: 128 lanes x 64 columns.
 #include "pg_common.cuh"
@@ -19,10 +16,6 @@ namespace pg {
 
 __device__ __forceinline__ uint32_t rg_off(int r, int k, int K) {
     return (uint32_t)((r >> 3) * K * 32 + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4);
-}
-
-__host__ __device__ constexpr uint32_t idesc_tf32_major(int M, int N, int a_mn, int b_mn) {
-    return umma::idesc_tf32(M, N) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16);
 }
 
 __global__ void __launch_bounds__(128) umma_selftest_kernel(const float *__restrict__ A,
@@ -36,10 +29,8 @@ __global__ void __launch_bounds__(128) umma_selftest_kernel(const float *__restr
     char *a1 = a0 + 128 * 128 * 4;
     char *b0 = a1 + 128 * 32 * 4;
     // operand shapes as stored (rows x cols, RG layout)
-    // mode 3: MN-major A[128 q][128 i], B[128 q][64 j], M = 128
-    // mode 4: K-major A[64][64], B[64][64], M = 64
-    const int ar = mode == 4 ? 64 : 128, ac = mode == 0 ? 32 : (mode == 3 ? 128 : 64);
-    const int br = (mode == 1 || mode == 3) ? 128 : 64, bc = mode == 0 ? 32 : 64;
+    const int ar = mode == 4 ? 64 : 128, ac = mode == 0 ? 32 : 64;
+    const int br = 64, bc = mode == 0 ? 32 : 64;
     for (int i = tid; i < ar * ac; i += 128) {
         const int r = i / ac, k = i % ac;
         float hi = A[i], lo = 0.0f;
@@ -80,21 +71,6 @@ __global__ void __launch_bounds__(128) umma_selftest_kernel(const float *__restr
                 const uint64_t bd = umma::smem_desc(umma::smem_u32(b0) + kb * 256, 128, 64 * 32);
                 umma::mma_tf32(tmem, ad, bd, idesc, n > 0 ? 1u : 0u);
             }
-        } else if (mode == 3) {
-            const uint32_t idesc = idesc_tf32_major(128, 64, 1, 1);
-            for (int kb = 0; kb < 128 / 8; ++kb, ++n) {
-                const uint64_t ad = umma::smem_desc(umma::smem_u32(a0) + kb * 128 * 32, 128 * 32, 128);
-                const uint64_t bd = umma::smem_desc(umma::smem_u32(b0) + kb * 64 * 32, 64 * 32, 128);
-                umma::mma_tf32(tmem, ad, bd, idesc, n > 0 ? 1u : 0u);
-            }
-        } else {
-            // D[i][j] = sum_q A[q][i] B[q][j]: M = 64 (i), N = 64 (j), K = 128 (q)
-            const uint32_t idesc = idesc_tf32_major(64, 64, 1, 1);
-            for (int kb = 0; kb < 128 / 8; ++kb, ++n) {
-                const uint64_t ad = umma::smem_desc(umma::smem_u32(a0) + kb * 64 * 32, 64 * 32, 128);
-                const uint64_t bd = umma::smem_desc(umma::smem_u32(b0) + kb * 64 * 32, 64 * 32, 128);
-                umma::mma_tf32(tmem, ad, bd, idesc, n > 0 ? 1u : 0u);
-            }
         }
         umma::commit(&mbar);
     }
@@ -118,6 +94,8 @@ __global__ void __launch_bounds__(128) umma_selftest_kernel(const float *__restr
 extern "C" int pg_selftest_umma_tf32(const float *A, const float *B, float *D, int split,
                                      void *stream) {
     // split: bit 0 = hi/lo expansion (mode 0); bits 4.. = mode
+    const int mode = split >> 4;
+    PG_REQUIRE(mode == 0 || mode == 2 || mode == 4, "selftest_umma_tf32: mode must be 0, 2 or 4");
     const int smem = (128 * 128 + 128 * 32 + 128 * 64) * 4;
     cudaFuncSetAttribute(pg::umma_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     pg::umma_selftest_kernel<<<1, 128, smem, pg::as_stream(stream)>>>(A, B, D, split & 1, split >> 4);

@@ -83,24 +83,30 @@ def to_inference(model: Model, width: int = 0, height: int = 0) -> InferenceMode
                           params, model.device)
 
 
-def _flags(inf: InferenceModel, exact: bool, tensor: bool = True) -> int:
+def _flags(inf: InferenceModel, exact: bool, tensor: bool = True, smem_tables=None) -> int:
     f = _lib.PG_HALF_FEATS
     if exact:
         f |= _lib.PG_EXACT_MLP
     if not tensor:
         f |= _lib.PG_NO_TENSOR
+    if smem_tables is not None:
+        f |= _lib.PG_SMEM_TABLES if smem_tables else _lib.PG_NO_SMEM_TABLES
     if inf.hyper.out_sigmoid:
         f |= _lib.PG_SIGMOID
     return f
 
 
 def decode_device(inf: InferenceModel, xs: torch.Tensor, out: torch.Tensor = None,
-                  exact: bool = True, stream=None, tensor: bool = True) -> torch.Tensor:
+                  exact: bool = True, stream=None, tensor: bool = True,
+                  smem_tables=None) -> torch.Tensor:
     """Fused encode + MLP on device-resident queries; returns (B, out_dim).
 
     exact=True: reference operation order on CUDA cores (bit-identical).
     exact=False: the MLP's 64-wide layers on the tcgen05 tensor core (2-term
-    tf32, fp32-level accuracy); tensor=False keeps FFMA instead (ablation)."""
+    tf32, fp32-level accuracy); tensor=False keeps FFMA instead (ablation);
+    smem_tables forces (True) or forbids (False) serving the probed levels'
+    baked indices from bit-packed shared-memory copies; None = automatic
+    (on for N_p = 2 and 4, where it measured faster)."""
     B = xs.shape[0]
     if out is None:
         out = torch.empty((B, inf.out_dim), dtype=torch.float32, device=inf.device)
@@ -109,7 +115,7 @@ def decode_device(inf: InferenceModel, xs: torch.Tensor, out: torch.Tensor = Non
         n = B * inf.hyper.encoded_width + 2 * B * max(inf.widths)
         ws = torch.empty(max(n, 1), dtype=torch.float32, device=inf.device)
     _lib.call("pg_decode_f32", inf.grid, inf.mlp_desc, _lib.ptr(xs), B, _lib.ptr(inf.feats16),
-              _lib.ptr(inf.baked), _lib.ptr(inf.params), _flags(inf, exact, tensor), _lib.ptr(ws),
+              _lib.ptr(inf.baked), _lib.ptr(inf.params), _flags(inf, exact, tensor, smem_tables), _lib.ptr(ws),
               _lib.ptr(out), _lib.stream_ptr(stream))
     return out
 

@@ -407,6 +407,27 @@ def test_decode_rows_independent_of_batching_and_rect_is_crop():
     eq(pg.decode_at(inf, q[77]), pg.decode_pixels(inf, q[77:78])[0])
 
 
+@pytest.mark.parametrize("n_p,d", [(2, 2), (4, 2), (8, 2), (4, 3)])
+def test_decode_smem_tables_bit_identical(n_p, d):
+    """PG_SMEM_TABLES (bit-packed baked indices in shared memory, 3 pipelines
+    per CTA) returns exactly what the plain tcgen05 decode returns."""
+    import paper_2312_17241_b200 as pg
+    from paper_2312_17241_b200.decode import decode_device
+    m = pg.init_model(pg.HyperParams(d=d, n_f=2**14, n_c=2**14, n_p=n_p, n_max=2048), seed=1)
+    rng = np.random.default_rng(n_p)
+    with torch.no_grad():
+        m.feats.copy_(torch.from_numpy((rng.standard_normal(tuple(m.feats.shape)) * 0.1).astype(np.float32)))
+        m.conf.copy_(torch.from_numpy(rng.standard_normal(tuple(m.conf.shape)).astype(np.float32)))
+        m.rebake_all()
+    inf = pg.to_inference(m)
+    xs = torch.rand((300_001, d), generator=torch.Generator().manual_seed(d)).cuda()
+    a = decode_device(inf, xs, exact=False, smem_tables=False).cpu().numpy()
+    b = decode_device(inf, xs, exact=False, smem_tables=True).cpu().numpy()
+    eq(a, b)
+    ref = decode_device(inf, xs[:20000], exact=True).cpu().numpy()
+    np.testing.assert_allclose(b[:20000], ref, rtol=1e-5, atol=1e-6)
+
+
 def test_host_decoder_matches_device():
     import paper_2312_17241_b200 as pg
     from paper_2312_17241_b200.decode import HostDecoder, decode_device
