@@ -29,8 +29,8 @@ struct TrainSmem {
     float w0t[kH * kI], w1t[kH * kH], w2t[kO * kH];   // [out][in]
     float b0[kH], b1[kH], b2[kO];
     float yT[kI * kT];    // encodings, later dL/dy       (swizzled rows)
-    float z1T[kH * kT];   // layer-1 pre-activations, later delta_1
-    float z2T[kH * kT];   // layer-2 pre-activations, later delta_2
+    float z1T[kH * kT];   // layer-1 activations relu(z1), later delta_1
+    float z2T[kH * kT];   // layer-2 activations relu(z2), later delta_2
     float d3[kT * kO];    // dL/d(out), sample-major
     float xs[kT * 3];
     float tg[kT * kO];
@@ -44,18 +44,17 @@ __device__ __forceinline__ int sw(int row, int col) {
 __device__ __forceinline__ float relu_np(float z) { return z < 0.0f ? 0.0f : z; }  // np.maximum(z, 0)
 __device__ __forceinline__ float mask_np(float z) { return z > 0.0f ? 1.0f : 0.0f; }  // (pre > 0)
 
-// out^T[j][q] = fma-chain_k( act(in^T[k][q]) * W[k][j] ) + b[j]   (j < 64, q < 128)
-template <int K, bool RELU_IN>
+// out^T[j][q] = relu( fma-chain_k( in^T[k][q] * W[k][j] ) + b[j] )   (j < 64, q < 64)
+// The ReLU is applied once at the write (np.maximum(z, 0) of the reference);
+// the backward masks test h > 0, the same predicate as z > 0.
+template <int K>
 __device__ __forceinline__ void fwd_layer(const float *__restrict__ inT, const float *__restrict__ W,
                                           const float *__restrict__ b, float *__restrict__ outT) {
     const int og = threadIdx.x & 15, pg = threadIdx.x >> 4;  // 4 outputs x 4 samples
     float acc[4][4] = {};
 #pragma unroll 8
     for (int k = 0; k < K; ++k) {
-        float4 a = *reinterpret_cast<const float4 *>(inT + sw(k, pg * 4));
-        if (RELU_IN) {
-            a.x = relu_np(a.x); a.y = relu_np(a.y); a.z = relu_np(a.z); a.w = relu_np(a.w);
-        }
+        const float4 a = *reinterpret_cast<const float4 *>(inT + sw(k, pg * 4));
         const float4 w = *reinterpret_cast<const float4 *>(W + k * kH + og * 4);
         const float av[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
@@ -70,8 +69,8 @@ __device__ __forceinline__ void fwd_layer(const float *__restrict__ inT, const f
     for (int j = 0; j < 4; ++j) {
         const float bj = b[og * 4 + j];
         *reinterpret_cast<float4 *>(outT + sw(og * 4 + j, pg * 4)) =
-            make_float4(__fadd_rn(acc[0][j], bj), __fadd_rn(acc[1][j], bj),
-                        __fadd_rn(acc[2][j], bj), __fadd_rn(acc[3][j], bj));
+            make_float4(relu_np(__fadd_rn(acc[0][j], bj)), relu_np(__fadd_rn(acc[1][j], bj)),
+                        relu_np(__fadd_rn(acc[2][j], bj)), relu_np(__fadd_rn(acc[3][j], bj)));
     }
 }
 
@@ -117,11 +116,11 @@ __global__ void __launch_bounds__(kNT, 2)
     }
     // persistent per-thread gradient accumulators
     float gW2 = 0.0f;                 // (k = tid&63, j = tid>>6)
-    float gB2 = 0.0f;                 // j = tid (tid < 4)
+    float gB2 = 0.0f;                 // j = tid>>6 (threads with tid&63 == 0)
     float gW1[4][4] = {};             // i = (tid>>4)*4 + u, j = (tid&15)*4 + v
-    float gB1 = 0.0f;                 // j = tid (tid < 64)
+    float gB1[4] = {};                // j = tid*4 + v (tid < 16)
     float gW0[2][4] = {};             // i = (tid>>4)*2 + u, j = (tid&15)*4 + v
-    float gB0 = 0.0f;                 // j = tid (tid < 64)
+    float gB0[4] = {};                // j = tid*4 + v (tid < 16)
     double lsum = 0.0;
 
     const int64_t ntiles = (B + kT - 1) / kT;
@@ -148,9 +147,9 @@ __global__ void __launch_bounds__(kNT, 2)
             S.yT[sw(2 * l + 1, pl)] = yv.y;
         }
         __syncthreads();
-        fwd_layer<kI, false>(S.yT, S.w0, S.b0, S.z1T);
+        fwd_layer<kI>(S.yT, S.w0, S.b0, S.z1T);
         __syncthreads();
-        fwd_layer<kH, true>(S.z1T, S.w1, S.b1, S.z2T);
+        fwd_layer<kH>(S.z1T, S.w1, S.b1, S.z2T);
         __syncthreads();
         // ---- output layer, loss, dpred (trainer.py:122-136) ----
         {
@@ -159,7 +158,7 @@ __global__ void __launch_bounds__(kNT, 2)
             if (j < od && q < nv) {
                 float acc = 0.0f;
 #pragma unroll 16
-                for (int k = 0; k < kH; ++k) acc = __fmaf_rn(relu_np(S.z2T[sw(k, q)]), S.w2[k * kO + j], acc);
+                for (int k = 0; k < kH; ++k) acc = __fmaf_rn(S.z2T[sw(k, q)], S.w2[k * kO + j], acc);
                 const float o = __fadd_rn(acc, S.b2[j]);
                 const float pred = sigmoid ? 1.0f / (1.0f + expf(-o)) : o;
                 const float diff = __fsub_rn(pred, S.tg[q * kO + j]);
@@ -170,18 +169,23 @@ __global__ void __launch_bounds__(kNT, 2)
             S.d3[q * kO + j] = d;
         }
         __syncthreads();
-        // ---- dW2 += relu(z2)^T d3, db2 += sum d3 ----
+        // ---- dW2 += h2^T d3, db2 += sum d3 (4 samples per shared load) ----
         {
             const int k = tid & 63, j = tid >> 6;
-            float acc = 0.0f;
-            for (int q = 0; q < kT; ++q)
-                acc = __fmaf_rn(relu_np(S.z2T[sw(k, q)]), S.d3[q * kO + j], acc);
-            gW2 += acc;
-            if (tid < kO) {
-                float s = 0.0f;
-                for (int q = 0; q < kT; ++q) s += S.d3[q * kO + tid];
-                gB2 += s;
+            float acc = 0.0f, bs = 0.0f;
+#pragma unroll 4
+            for (int q = 0; q < kT; q += 4) {
+                const float4 h = *reinterpret_cast<const float4 *>(S.z2T + sw(k, q));
+                const float d0 = S.d3[q * kO + j], d1 = S.d3[(q + 1) * kO + j];
+                const float d2 = S.d3[(q + 2) * kO + j], d3v = S.d3[(q + 3) * kO + j];
+                acc = __fmaf_rn(h.x, d0, acc);
+                acc = __fmaf_rn(h.y, d1, acc);
+                acc = __fmaf_rn(h.z, d2, acc);
+                acc = __fmaf_rn(h.w, d3v, acc);
+                bs += (d0 + d1) + (d2 + d3v);
             }
+            gW2 += acc;
+            if (k == 0) gB2 += bs;
         }
         __syncthreads();
         // ---- delta2 = (d3 @ W2^T) * (z2 > 0), in place over z2 ----
@@ -203,19 +207,20 @@ __global__ void __launch_bounds__(kNT, 2)
             }
         }
         __syncthreads();
-        // ---- dW1 += relu(z1)^T delta2, db1 += sum delta2 ----
+        // ---- dW1 += h1^T delta2, db1 += sum delta2 (summed by the ig == 0 threads) ----
         {
             const int jg = tid & 15, ig = tid >> 4;
+            float bs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
             for (int q = 0; q < kT; q += 4) {
                 float4 a[4], dd[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    a[u] = *reinterpret_cast<const float4 *>(S.z1T + sw(ig * 4 + u, q));
-                    a[u].x = relu_np(a[u].x); a[u].y = relu_np(a[u].y);
-                    a[u].z = relu_np(a[u].z); a[u].w = relu_np(a[u].w);
-                }
+                for (int u = 0; u < 4; ++u) a[u] = *reinterpret_cast<const float4 *>(S.z1T + sw(ig * 4 + u, q));
 #pragma unroll
                 for (int v = 0; v < 4; ++v) dd[v] = *reinterpret_cast<const float4 *>(S.z2T + sw(jg * 4 + v, q));
+                if (ig == 0) {
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) bs[v] += (dd[v].x + dd[v].y) + (dd[v].z + dd[v].w);
+                }
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -228,10 +233,9 @@ __global__ void __launch_bounds__(kNT, 2)
                         gW1[u][v] = s;
                     }
             }
-            if (tid < kH) {
-                float s = 0.0f;
-                for (int q = 0; q < kT; ++q) s += S.z2T[sw(tid, q)];
-                gB1 += s;
+            if (ig == 0) {
+#pragma unroll
+                for (int v = 0; v < 4; ++v) gB1[v] += bs[v];
             }
         }
         __syncthreads();
@@ -262,15 +266,20 @@ __global__ void __launch_bounds__(kNT, 2)
             }
         }
         __syncthreads();
-        // ---- dW0 += y^T delta1, db0 += sum delta1 ----
+        // ---- dW0 += y^T delta1, db0 += sum delta1 (summed by the ig == 0 threads) ----
         {
             const int jg = tid & 15, ig = tid >> 4;
+            float bs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
             for (int q = 0; q < kT; q += 4) {
                 float4 a[2], dd[4];
 #pragma unroll
                 for (int u = 0; u < 2; ++u) a[u] = *reinterpret_cast<const float4 *>(S.yT + sw(ig * 2 + u, q));
 #pragma unroll
                 for (int v = 0; v < 4; ++v) dd[v] = *reinterpret_cast<const float4 *>(S.z1T + sw(jg * 4 + v, q));
+                if (ig == 0) {
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) bs[v] += (dd[v].x + dd[v].y) + (dd[v].z + dd[v].w);
+                }
 #pragma unroll
                 for (int u = 0; u < 2; ++u)
 #pragma unroll
@@ -283,10 +292,9 @@ __global__ void __launch_bounds__(kNT, 2)
                         gW0[u][v] = s;
                     }
             }
-            if (tid < kH) {
-                float s = 0.0f;
-                for (int q = 0; q < kT; ++q) s += S.z1T[sw(tid, q)];
-                gB0 += s;
+            if (ig == 0) {
+#pragma unroll
+                for (int v = 0; v < 4; ++v) gB0[v] += bs[v];
             }
         }
         __syncthreads();
@@ -344,11 +352,14 @@ __global__ void __launch_bounds__(kNT, 2)
             for (int v = 0; v < 4; ++v) red_add(gW1p + (ig * 4 + u) * kH + jg * 4 + v, gW1[u][v]);
         const int k = tid & 63, j = tid >> 6;
         if (j < od) red_add(gW2p + k * od + j, gW2);
-        if (tid < kH) {
-            red_add(gb0p + tid, gB0);
-            red_add(gb1p + tid, gB1);
+        if (tid < 16) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                red_add(gb0p + tid * 4 + v, gB0[v]);
+                red_add(gb1p + tid * 4 + v, gB1[v]);
+            }
         }
-        if (tid < od) red_add(gb2p + tid, gB2);
+        if (k == 0 && j < od) red_add(gb2p + j, gB2);
     }
     // loss: block reduce in fp64
 #pragma unroll
