@@ -235,7 +235,7 @@ int pg_mlp_train_f64(const pg_mlp *mlp, const double *y, const double *targets,
                      unsigned flags, double *gparams, double *dy,
                      double *loss_sum, double *ws, void *stream);
 
-/* Fused training pass (trainer.py:118-148): per 128-sample tile one kernel
+/* Fused training pass (trainer.py:118-148): per 64-sample tile one kernel
  * runs encode fwd -> MLP fwd -> squared error -> MLP bwd -> encode bwd with
  * activations in shared memory.  Shape: F = 2, 16 levels, N_p <= 16, MLP
  * [32, 64, 64, out_dim <= 4].  Forward and data-gradient GEMMs follow
@@ -251,6 +251,28 @@ int pg_train_fused_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
                        float *gfeat, float *gconf, uint8_t *touched,
                        float *gparams, double *loss_sum, float *dy_out,
                        void *stream);
+
+/* Reference-order MLP gradients (parity mode).  pg_train_fused_ref_f32 is
+ * pg_train_fused_f32 except that it leaves gparams untouched and writes, per
+ * sample, every layer's input and output delta to acts, laid out as
+ * [a_0 | a_1 | .. | a_{n-1} | delta_0 | .. | delta_{n-1}], each block B rows
+ * of its width (a_0 = y, a_l = relu activations, delta_l = dL/d(pre-activation
+ * of layer l)); pg_mlp_acts_floats(B, mlp) floats.  pg_mlp_wgrad_blas_f32
+ * then forms gparams += every weight and bias gradient in numpy/OpenBLAS
+ * order (mlp.py:80-84): the sgemm K loop over samples is blocked by 448 (the
+ * last two blocks balanced), each block one sequential FMA chain from 0,
+ * blocks added in order; bias sums sequential over samples.  With the forward
+ * already in OpenBLAS order this makes the MLP gradients bit-identical to the
+ * reference's for out_dim >= 2 (out_dim 1 goes through sgemv there). */
+int64_t pg_mlp_acts_floats(int64_t B, const pg_mlp *mlp);
+int pg_train_fused_ref_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
+                           const float *targets, int64_t B, const float *feats,
+                           const uint8_t *baked, const float *conf,
+                           const float *params, float scale, unsigned flags,
+                           float *gfeat, float *gconf, uint8_t *touched,
+                           double *loss_sum, float *acts, void *stream);
+int pg_mlp_wgrad_blas_f32(const pg_mlp *mlp, const float *acts, int64_t B,
+                          float *gparams, void *stream);
 
 /* Deterministic mode.  Same passes as pg_encode_bwd_f32 / pg_mlp_train_f32 /
  * pg_train_fused_f32, but every cross-thread sum (table scatters, weight

@@ -95,6 +95,7 @@ def _load_orc():
         getattr(lib, f"orc_sigmoid_rows_{sfx}").argtypes = [_P, _I64]
     lib.orc_dedup_rows.argtypes = [_P, _I64, _P, _I64, _P, _P]
     lib.orc_dedup_rows.restype = _I64
+    lib.orc_wgrad_blas_f32.argtypes = [_P, _I64, _I32, _P, _I32, _P, _P]
     return lib
 
 
@@ -114,6 +115,15 @@ def _sfx(dtype):
 
 def _c(a, dtype=None):
     return np.ascontiguousarray(a, dtype=dtype)
+
+
+def wgrad_blas(a, delta, gw, gb):
+    """gw += a.T @ delta and gb += delta.sum(0) in numpy/OpenBLAS order
+    (orc_wgrad_blas_f32; float32 only), in place."""
+    a, delta = _c(a, np.float32), _c(delta, np.float32)
+    assert gw.flags.c_contiguous and gb.flags.c_contiguous and gw.dtype == np.float32
+    _orc().orc_wgrad_blas_f32(_ptr(a), a.shape[0], a.shape[1], _ptr(delta), delta.shape[1],
+                              _ptr(gw), _ptr(gb))
 
 
 class CBackend:

@@ -272,3 +272,37 @@ int64_t orc_dedup_rows(const int32_t *row, int64_t n, int32_t *mark, int64_t n_c
     }
     return u;
 }
+
+/* OpenBLAS 0.3.30 (SkylakeX) sgemm order for the MLP weight gradient
+ * W_grad += a^T @ delta (mlp.py:81; OpenBLAS is a numpy dependency, not part
+ * of the reference tree): C = 0; the K loop (samples) is blocked by Q = 448,
+ * the last two blocks balanced (a remainder in (Q, 2Q) is split in half,
+ * driver/level3 GEMM_Q logic); inside a block each C element is ONE
+ * sequential fused-multiply-add chain from 0; block results are added to C in
+ * order.  Then the numpy in-place add into gw.  Bias: delta.sum(axis=0) is a
+ * sequential sum over rows (mlp.py:82).  Pinned against numpy in
+ * tests/test_oracle.py::test_openblas_wgrad_order. */
+void orc_wgrad_blas_f32(const float *a, int64_t K, int fin, const float *d, int fout,
+                        float *gw, float *gb)
+{
+    const int64_t Q = 448;
+    for (int i = 0; i < fin; ++i)
+        for (int j = 0; j < fout; ++j) {
+            float c = 0.0f;
+            for (int64_t ls = 0; ls < K;) {
+                int64_t ml = K - ls;
+                if (ml >= 2 * Q) ml = Q;
+                else if (ml > Q) ml = ml / 2;
+                float acc = 0.0f;
+                for (int64_t k = ls; k < ls + ml; ++k) acc = fmaf(a[k * fin + i], d[k * fout + j], acc);
+                c = c + acc;
+                ls += ml;
+            }
+            gw[(int64_t)i * fout + j] = gw[(int64_t)i * fout + j] + c;
+        }
+    for (int j = 0; j < fout; ++j) {
+        float s = 0.0f;
+        for (int64_t k = 0; k < K; ++k) s = s + d[k * fout + j];
+        gb[j] = gb[j] + s;
+    }
+}

@@ -80,6 +80,9 @@ _SIGS.update({
     "pg_touched_from_f32": [_P, _I64, _P, _P],
     "pg_train_fused_f32": [_G, _M, _P, _P, _I64, _P, _P, _P, _P, _F, ctypes.c_uint, _P, _P, _P,
                            _P, _P, _P, _P],
+    "pg_train_fused_ref_f32": [_G, _M, _P, _P, _I64, _P, _P, _P, _P, _F, ctypes.c_uint, _P, _P,
+                               _P, _P, _P, _P],
+    "pg_mlp_wgrad_blas_f32": [_M, _P, _I64, _P, _P],
     "pg_encode_bwd_det_f32": [_G, _P, _I64, _P, _P, _P, _P, _P, _P, _P],
     "pg_mlp_train_det_f32": [_M, _P, _P, _I64, _P, _F, ctypes.c_uint, _P, _P, _P, _P, _P],
     "pg_train_fused_det_f32": [_G, _M, _P, _P, _I64, _P, _P, _P, _P, _F, ctypes.c_uint, _P, _P,
@@ -91,7 +94,8 @@ _SIGS.update({
     "pg_probe_gather": [_P, _I64, _I64, _U32, _P, _P],
 })
 _RESTYPE_I64 = {"pg_dedup_workspace_bytes": [_I64, _I64],
-                "pg_mlp_train_workspace_floats": [_I64, _M]}
+                "pg_mlp_train_workspace_floats": [_I64, _M],
+                "pg_mlp_acts_floats": [_I64, _M]}
 
 _LIB = None
 

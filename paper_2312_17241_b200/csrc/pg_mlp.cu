@@ -508,6 +508,70 @@ int64_t mlp_train_ws(int64_t B, const pg_mlp *m) {
 }
 int64_t mlp_params(const pg_mlp *m) { return mlp_param_count(m); }
 
+// =========================================================================
+// Reference-order weight/bias gradients (parity mode, mlp.py:80-84):
+//   W_grad[l] += a_l^T @ delta_l     via OpenBLAS sgemm: C = 0; K (= samples)
+//                                    blocked by kBlasQ, the last two blocks
+//                                    balanced; per block one sequential FMA
+//                                    chain from 0; C += block, in order
+//   b_grad[l] += delta_l.sum(axis=0) sequential over samples
+// One thread per gradient element.  The blocking was pinned against numpy
+// 2.3 / OpenBLAS 0.3.30 (SkylakeX) in this image for K from 128 to 2^18,
+// 1 to 8 BLAS threads (the CPU test test_openblas_wgrad_order pins it).
+// =========================================================================
+constexpr int64_t kBlasQ = 448;
+
+__global__ void wgrad_blas_kernel(const float *__restrict__ a, int fin, const float *__restrict__ d, int fout,
+                                  int64_t B, float *__restrict__ gW, float *__restrict__ gb) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < fin * fout) {
+        const int i = e / fout, j = e - (e / fout) * fout;
+        float c = 0.0f;
+        for (int64_t ls = 0; ls < B;) {
+            int64_t ml = B - ls;
+            if (ml >= 2 * kBlasQ) ml = kBlasQ;
+            else if (ml > kBlasQ) ml = ml / 2;
+            float acc = 0.0f;
+#pragma unroll 8
+            for (int64_t k = ls; k < ls + ml; ++k) acc = __fmaf_rn(__ldg(a + k * fin + i), __ldg(d + k * fout + j), acc);
+            c = __fadd_rn(c, acc);
+            ls += ml;
+        }
+        gW[e] = __fadd_rn(gW[e], c);
+    } else if (e < fin * fout + fout) {
+        const int j = e - fin * fout;
+        float sacc = 0.0f;
+#pragma unroll 8
+        for (int64_t k = 0; k < B; ++k) sacc = __fadd_rn(sacc, __ldg(d + k * fout + j));
+        gb[j] = __fadd_rn(gb[j], sacc);
+    }
+}
+
+int64_t mlp_acts_floats(int64_t B, const pg_mlp *m) {
+    int64_t w = 0;
+    for (int l = 0; l < m->n_layers; ++l) w += m->widths[l] + m->widths[l + 1];
+    return B * w;
+}
+
+int mlp_wgrad_blas(const pg_mlp *m, const float *acts, int64_t B, float *gparams, cudaStream_t s) {
+    if (int e = validate_mlp(m)) return e;
+    if (B == 0) return PG_OK;
+    // acts = [a_0 | .. | a_{n-1} | delta_0 | .. | delta_{n-1}]
+    int64_t a_off = 0, d_off = 0;
+    for (int l = 0; l < m->n_layers; ++l) d_off += B * m->widths[l];
+    float *g = gparams;
+    for (int l = 0; l < m->n_layers; ++l) {
+        const int fin = m->widths[l], fout = m->widths[l + 1];
+        const int n = fin * fout + fout;
+        wgrad_blas_kernel<<<(n + 127) / 128, 128, 0, s>>>(acts + a_off, fin, acts + d_off, fout, B, g,
+                                                          g + (int64_t)fin * fout);
+        a_off += B * fin;
+        d_off += B * fout;
+        g += (int64_t)fin * fout + fout;
+    }
+    return check_launch("mlp_wgrad_blas");
+}
+
 }  // namespace pg
 
 using namespace pg;
@@ -571,6 +635,10 @@ int pg_mlp_train_det_f32(const pg_mlp *mlp, const float *y, const float *targets
     return mlp_train_generic<float, fx_t, fx_t>(mlp, y, targets, B, params, scale, flags,
                                                 (fx_t *)gparams_fx, dy, (fx_t *)loss_fx, ws,
                                                 as_stream(stream));
+}
+int64_t pg_mlp_acts_floats(int64_t B, const pg_mlp *mlp) { return mlp_acts_floats(B, mlp); }
+int pg_mlp_wgrad_blas_f32(const pg_mlp *mlp, const float *acts, int64_t B, float *gparams, void *stream) {
+    return mlp_wgrad_blas(mlp, acts, B, gparams, as_stream(stream));
 }
 int pg_mlp_train_f64(const pg_mlp *mlp, const double *y, const double *targets, int64_t B,
                      const double *params, double scale, unsigned flags, double *gparams,

@@ -17,6 +17,29 @@
 
 namespace pg {
 
+// Optional per-phase cycle accounting (make prof -> tools/_prof/): thread 0 of
+// every CTA adds the clock64() time between consecutive barriers to
+// g_phase_cycles[phase]; read with pg_phase_prof_read.
+#ifdef PG_PHASE_PROF
+__device__ unsigned long long g_phase_cycles[16];
+#define PG_PH_INIT                  \
+    long long ph_t = clock64();     \
+    unsigned long long ph_acc[12] = {};
+#define PG_PH(i)                                   \
+    do {                                           \
+        const long long ph_n = clock64();          \
+        ph_acc[i] += (unsigned long long)(ph_n - ph_t); \
+        ph_t = ph_n;                               \
+    } while (0)
+#define PG_PH_FLUSH                                                         \
+    if (threadIdx.x == 0)                                                   \
+        for (int i = 0; i < 12; ++i) atomicAdd(&g_phase_cycles[i], ph_acc[i]);
+#else
+#define PG_PH_INIT
+#define PG_PH(i)
+#define PG_PH_FLUSH
+#endif
+
 constexpr int kT = 64;    // samples per tile
 constexpr int kNT = 256;  // threads per CTA (2 CTAs per SM: one's memory-bound
                           // encode phases overlap the other's FFMA MLP phases)
@@ -26,7 +49,7 @@ constexpr int kO = 4;     // padded output width
 
 struct TrainSmem {
     float w0[kI * kH], w1[kH * kH], w2[kH * kO];      // [in][out]
-    float w0t[kH * kI], w1t[kH * kH], w2t[kO * kH];   // [out][in]
+    float w0t[kH * kI], w1t[kH * kH];                 // [out][in]
     float b0[kH], b1[kH], b2[kO];
     float yT[kI * kT];    // encodings, later dL/dy       (swizzled rows)
     float z1T[kH * kT];   // layer-1 activations relu(z1), later delta_1
@@ -40,6 +63,13 @@ struct TrainSmem {
 __device__ __forceinline__ int sw(int row, int col) {
     const int chunk = (col >> 2) ^ ((row >> 2) & 7);
     return row * kT + (chunk << 2) + (col & 3);
+}
+// parity mode: copy a transposed smem tile (rows = features) to acts rows
+__device__ __forceinline__ void dump_tile(const float *srcT, int width, int nv, float *dst) {
+    for (int i = threadIdx.x; i < nv * width; i += kNT) {
+        const int q = i / width, c = i - q * width;
+        dst[(int64_t)q * width + c] = srcT[sw(c, q)];
+    }
 }
 __device__ __forceinline__ float relu_np(float z) { return z < 0.0f ? 0.0f : z; }  // np.maximum(z, 0)
 __device__ __forceinline__ float mask_np(float z) { return z > 0.0f ? 1.0f : 0.0f; }  // (pre > 0)
@@ -82,7 +112,8 @@ __global__ void __launch_bounds__(kNT, 2)
                        const float *__restrict__ params, int od, float scale, int sigmoid,
                        ACC *__restrict__ gfeat, ACC *__restrict__ gconf,
                        uint8_t *__restrict__ touched, ACC *__restrict__ gparams,
-                       LACC *__restrict__ loss_sum, float *__restrict__ dy_out) {
+                       LACC *__restrict__ loss_sum, float *__restrict__ dy_out,
+                       float *__restrict__ acts) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TrainSmem &S = *reinterpret_cast<TrainSmem *>(smem_raw);
     const int tid = threadIdx.x;
@@ -109,7 +140,6 @@ __global__ void __launch_bounds__(kNT, 2)
             const int k = i / kO, j = i % kO;
             const float v = j < od ? p[k * od + j] : 0.0f;
             S.w2[i] = v;
-            S.w2t[j * kH + k] = v;
         }
         p += kH * od;
         for (int i = tid; i < kO; i += kNT) S.b2[i] = i < od ? p[i] : 0.0f;
@@ -122,18 +152,31 @@ __global__ void __launch_bounds__(kNT, 2)
     float gW0[2][4] = {};             // i = (tid>>4)*2 + u, j = (tid&15)*4 + v
     float gB0[4] = {};                // j = tid*4 + v (tid < 16)
     double lsum = 0.0;
+    PG_PH_INIT
 
     const int64_t ntiles = (B + kT - 1) / kT;
+    // a tile's coordinates and targets (one value of each per thread, since
+    // kT*D <= kNT and kT*kO == kNT) are fetched one tile ahead into registers
+    static_assert(kT * 3 <= kNT && kT * kO == kNT, "one prefetched value per thread");
+    auto fetch = [&](int64_t t, float &fx, float &ft) {
+        const int64_t q0 = t * kT;
+        const int n = t < ntiles ? (int)((B - q0) < kT ? (B - q0) : kT) : 0;
+        fx = (tid < kT * D && tid < n * D) ? __ldg(xs + q0 * D + tid) : 0.5f;
+        const int q = tid / kO, j = tid % kO;
+        ft = (q < n && j < od) ? __ldg(targets + (q0 + q) * od + j) : 0.0f;
+    };
+    float pf_x, pf_t;
+    fetch(blockIdx.x, pf_x, pf_t);
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t p0 = tile * kT;
         const int nv = (int)((B - p0) < kT ? (B - p0) : kT);
         __syncthreads();
-        for (int i = tid; i < kT * D; i += kNT) S.xs[i] = i < nv * D ? xs[p0 * D + i] : 0.5f;
-        for (int i = tid; i < kT * kO; i += kNT) {
-            const int q = i / kO, j = i % kO;
-            S.tg[i] = (q < nv && j < od) ? targets[(p0 + q) * od + j] : 0.0f;
-        }
+        PG_PH(11);
+        if (tid < kT * D) S.xs[tid] = pf_x;
+        S.tg[tid] = pf_t;
+        fetch(tile + gridDim.x, pf_x, pf_t);
         __syncthreads();
+        PG_PH(0);
         // ---- encode forward: thread = (sample pl, levels lsub + 4*it) ----
         const int pl = tid & (kT - 1), lsub = tid >> 6;
         float x[D];
@@ -147,10 +190,16 @@ __global__ void __launch_bounds__(kNT, 2)
             S.yT[sw(2 * l + 1, pl)] = yv.y;
         }
         __syncthreads();
+        PG_PH(1);
+        if (acts) dump_tile(S.yT, kI, nv, acts + p0 * kI);
         fwd_layer<kI>(S.yT, S.w0, S.b0, S.z1T);
         __syncthreads();
+        PG_PH(2);
+        if (acts) dump_tile(S.z1T, kH, nv, acts + B * kI + p0 * kH);
         fwd_layer<kH>(S.z1T, S.w1, S.b1, S.z2T);
         __syncthreads();
+        PG_PH(3);
+        if (acts) dump_tile(S.z2T, kH, nv, acts + B * (kI + kH) + p0 * kH);
         // ---- output layer, loss, dpred (trainer.py:122-136) ----
         {
             const int q = tid & (kT - 1), j = tid >> 6;
@@ -169,6 +218,10 @@ __global__ void __launch_bounds__(kNT, 2)
             S.d3[q * kO + j] = d;
         }
         __syncthreads();
+        PG_PH(4);
+        if (acts)
+            for (int i = tid; i < nv * od; i += kNT)
+                acts[B * (kI + 4 * kH) + p0 * od + i] = S.d3[(i / od) * kO + i % od];
         // ---- dW2 += h2^T d3, db2 += sum d3 (4 samples per shared load) ----
         {
             const int k = tid & 63, j = tid >> 6;
@@ -188,25 +241,37 @@ __global__ void __launch_bounds__(kNT, 2)
             if (k == 0) gB2 += bs;
         }
         __syncthreads();
+        PG_PH(5);
         // ---- delta2 = (d3 @ W2^T) * (z2 > 0), in place over z2 ----
         {
             const int og = tid & 15, pg = tid >> 4;
+            float dq[4][kO];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float4 v = *reinterpret_cast<const float4 *>(S.d3 + (pg * 4 + i) * kO);
+                dq[i][0] = v.x; dq[i][1] = v.y; dq[i][2] = v.z; dq[i][3] = v.w;
+            }
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
                 const int k = og * 4 + jj;
+                const float4 wv = *reinterpret_cast<const float4 *>(S.w2 + k * kO);
+                const float w[kO] = {wv.x, wv.y, wv.z, wv.w};
                 float4 z = *reinterpret_cast<float4 *>(S.z2T + sw(k, pg * 4));
                 float zv[4] = {z.x, z.y, z.z, z.w};
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const int q = pg * 4 + i;
-                    float acc = 0.0f;
-                    for (int j = 0; j < od; ++j) acc = __fmaf_rn(S.d3[q * kO + j], S.w2t[j * kH + k], acc);
+                    float acc = 0.0f;   // fma chain over j < od, as the sgemm kernel
+#pragma unroll
+                    for (int j = 0; j < kO; ++j)
+                        if (j < od) acc = __fmaf_rn(dq[i][j], w[j], acc);
                     zv[i] = __fmul_rn(acc, mask_np(zv[i]));
                 }
                 *reinterpret_cast<float4 *>(S.z2T + sw(k, pg * 4)) = make_float4(zv[0], zv[1], zv[2], zv[3]);
             }
         }
         __syncthreads();
+        PG_PH(6);
+        if (acts) dump_tile(S.z2T, kH, nv, acts + B * (kI + 3 * kH) + p0 * kH);
         // ---- dW1 += h1^T delta2, db1 += sum delta2 (summed by the ig == 0 threads) ----
         {
             const int jg = tid & 15, ig = tid >> 4;
@@ -239,6 +304,7 @@ __global__ void __launch_bounds__(kNT, 2)
             }
         }
         __syncthreads();
+        PG_PH(7);
         // ---- delta1 = (delta2 @ W1^T) * (z1 > 0), in place over z1 ----
         {
             const int og = tid & 15, pg = tid >> 4;
@@ -266,6 +332,8 @@ __global__ void __launch_bounds__(kNT, 2)
             }
         }
         __syncthreads();
+        PG_PH(8);
+        if (acts) dump_tile(S.z1T, kH, nv, acts + B * (kI + 2 * kH) + p0 * kH);
         // ---- dW0 += y^T delta1, db0 += sum delta1 (summed by the ig == 0 threads) ----
         {
             const int jg = tid & 15, ig = tid >> 4;
@@ -298,6 +366,7 @@ __global__ void __launch_bounds__(kNT, 2)
             }
         }
         __syncthreads();
+        PG_PH(9);
         // ---- dy = delta1 @ W0^T (fma chain over j), over yT ----
         {
             const int og = tid & 7, pg = tid >> 3;  // 4 inputs x 2 samples
@@ -321,6 +390,7 @@ __global__ void __launch_bounds__(kNT, 2)
                 *reinterpret_cast<float2 *>(S.yT + sw(og * 4 + ii, pg * 2)) = make_float2(acc[0][ii], acc[1][ii]);
         }
         __syncthreads();
+        PG_PH(10);
         if (dy_out) {  // optional copy of dL/dy (parity tests)
             for (int i = tid; i < nv * kI; i += kNT) {
                 const int q = i / kI, c = i % kI;
@@ -337,10 +407,11 @@ __global__ void __launch_bounds__(kNT, 2)
             }
         }
     }
+    PG_PH_FLUSH
     // ---- flush gradient accumulators ----
     ACC *gW0p = gparams, *gb0p = gW0p + kI * kH, *gW1p = gb0p + kH, *gb1p = gW1p + kH * kH;
     ACC *gW2p = gb1p + kH, *gb2p = gW2p + kH * od;
-    {
+    if (!acts) {  // (parity mode: pg_mlp_wgrad_blas_f32 forms them from acts)
         const int jg = tid & 15, ig = tid >> 4;
 #pragma unroll
         for (int u = 0; u < 2; ++u)
@@ -384,7 +455,7 @@ template <typename ACC, typename LACC>
 int train_fused(const pg_grid *g, const pg_mlp *m, const float *xs, const float *targets, int64_t B,
                 const float *feats, const uint8_t *baked, const float *conf, const float *params,
                 float scale, unsigned flags, ACC *gfeat, ACC *gconf, uint8_t *touched,
-                ACC *gparams, LACC *loss_sum, float *dy_out, cudaStream_t s) {
+                ACC *gparams, LACC *loss_sum, float *dy_out, float *acts, cudaStream_t s) {
     if (int e = validate_grid(g)) return e;
     PG_REQUIRE(train_fast_ok(g, m), "fused training needs F=2, 16 levels, N_p<=16, MLP [32,64,64,<=4]");
     if (B == 0) return PG_OK;
@@ -406,7 +477,7 @@ int train_fused(const pg_grid *g, const pg_mlp *m, const float *xs, const float 
             configured[IDX] = true;                                                                   \
         }                                                                                             \
         kern<<<grd, kNT, smem, s>>>(*g, xs, targets, B, feats, feats, baked, conf, params, od, scale,  \
-                                    sig, gfeat, gconf, touched, gparams, loss_sum, dy_out);           \
+                                    sig, gfeat, gconf, touched, gparams, loss_sum, dy_out, acts);     \
     } while (0)
     if (g->d == 2) {
         if (np4) PG_TRAIN_LAUNCH(2, 4, 0); else PG_TRAIN_LAUNCH(2, 16, 1);
@@ -419,6 +490,17 @@ int train_fused(const pg_grid *g, const pg_mlp *m, const float *xs, const float 
 
 }  // namespace pg
 
+#ifdef PG_PHASE_PROF
+extern "C" int pg_phase_prof_read(unsigned long long *out16, int reset) {
+    cudaMemcpyFromSymbol(out16, pg::g_phase_cycles, 16 * sizeof(unsigned long long));
+    if (reset) {
+        static const unsigned long long zero[16] = {};
+        cudaMemcpyToSymbol(pg::g_phase_cycles, zero, sizeof(zero));
+    }
+    return pg::check_launch("phase_prof_read");
+}
+#endif
+
 extern "C" int pg_train_fused_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
                                   const float *targets, int64_t B, const float *feats,
                                   const uint8_t *baked, const float *conf, const float *params,
@@ -427,6 +509,17 @@ extern "C" int pg_train_fused_f32(const pg_grid *grid, const pg_mlp *mlp, const 
                                   void *stream) {
     return pg::train_fused<float, double>(grid, mlp, xs, targets, B, feats, baked, conf, params, scale,
                                           flags, gfeat, gconf, touched, gparams, loss_sum, dy_out,
+                                          nullptr, pg::as_stream(stream));
+}
+
+extern "C" int pg_train_fused_ref_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
+                                      const float *targets, int64_t B, const float *feats,
+                                      const uint8_t *baked, const float *conf, const float *params,
+                                      float scale, unsigned flags, float *gfeat, float *gconf,
+                                      uint8_t *touched, double *loss_sum, float *acts, void *stream) {
+    PG_REQUIRE(acts != nullptr, "pg_train_fused_ref_f32: acts is required");
+    return pg::train_fused<float, double>(grid, mlp, xs, targets, B, feats, baked, conf, params, scale,
+                                          flags, gfeat, gconf, touched, nullptr, loss_sum, nullptr, acts,
                                           pg::as_stream(stream));
 }
 
@@ -439,6 +532,6 @@ extern "C" int pg_train_fused_det_f32(const pg_grid *grid, const pg_mlp *mlp, co
     using pg::fx_t;
     return pg::train_fused<fx_t, fx_t>(grid, mlp, xs, targets, B, feats, baked, conf, params, scale,
                                        flags, (fx_t *)gfeat_fx, (fx_t *)gconf_fx, touched,
-                                       (fx_t *)gparams_fx, (fx_t *)loss_fx, dy_out,
+                                       (fx_t *)gparams_fx, (fx_t *)loss_fx, dy_out, nullptr,
                                        pg::as_stream(stream));
 }

@@ -89,7 +89,12 @@ class TrainState:
     """Optimizer state bound to one device model; drives individual steps."""
 
     def __init__(self, model: Model, image, cfg: TrainConfig, sampler: str = "reference",
-                 fused: bool | None = None, deterministic: bool = False):
+                 fused: bool | None = None, deterministic: bool = False,
+                 reference_order: bool = False):
+        """``reference_order``: MLP weight/bias gradients in numpy/OpenBLAS
+        summation order (pg_mlp_wgrad_blas_f32) instead of per-CTA partial
+        sums; with the forward already in OpenBLAS order this makes every MLP
+        gradient bit-identical to the reference's (parity mode, slower)."""
         cfg.validate()
         if sampler not in ("reference", "device", "points"):
             raise InvalidHyperparameter(f"unknown sampler {sampler!r}")
@@ -126,6 +131,13 @@ class TrainState:
         if deterministic and model.tdtype != torch.float32:
             raise InvalidHyperparameter("deterministic mode is float32-only")
         self.deterministic = deterministic
+        self.reference_order = reference_order
+        if reference_order:
+            if not self.fused or deterministic:
+                raise InvalidHyperparameter(
+                    "reference_order needs the fused float32 shape and is exclusive with deterministic")
+            na = int(_lib.lib().pg_mlp_acts_floats(B, model.mlp_desc))
+            self.acts = torch.empty(na, dtype=tdt, device=dev)
         if not self.fused:
             self.y = torch.empty((B, h.encoded_width), dtype=tdt, device=dev)
             self.dy = torch.empty_like(self.y)
@@ -233,6 +245,16 @@ class TrainState:
                 encode_backward_device(m, xs, self.dy, deterministic=True, flush=False)
             m.fx_flush(loss_sum=self.loss_sum)
             return
+        if self.reference_order:
+            if dy_out is not None:
+                raise InvalidHyperparameter("dy_out is not produced in reference_order mode")
+            _lib.call("pg_train_fused_ref_f32", m.grid, m.mlp_desc, _lib.ptr(xs), _lib.ptr(targets),
+                      xs.shape[0], _lib.ptr(m.feats), _lib.ptr(m.baked), _lib.ptr(m.conf),
+                      _lib.ptr(m.mlp_params), scale, flags, _lib.ptr(m.gfeats), _lib.ptr(m.gconf),
+                      _lib.ptr(m.touched), _lib.ptr(self.loss_sum), _lib.ptr(self.acts), s)
+            _lib.call("pg_mlp_wgrad_blas_f32", m.mlp_desc, _lib.ptr(self.acts), xs.shape[0],
+                      _lib.ptr(m.gmlp), s)
+            return
         if self.fused:
             _lib.call("pg_train_fused_f32", m.grid, m.mlp_desc, _lib.ptr(xs), _lib.ptr(targets),
                       xs.shape[0], _lib.ptr(m.feats), _lib.ptr(m.baked), _lib.ptr(m.conf),
@@ -329,11 +351,13 @@ def psnr(reference, test) -> float:
 
 
 def fit(image, hyper: HyperParams, cfg: TrainConfig, force_probed: bool = False,
-        sampler: str = "reference", deterministic: bool = False) -> FitResult:
+        sampler: str = "reference", deterministic: bool = False,
+        reference_order: bool = False) -> FitResult:
     """Fit one image on the GPU (trainer.py:196-242)."""
     from .decode import decode_image, to_inference
     model = init_model(hyper, cfg.seed, cfg.dtype, force_probed=force_probed)
-    state = TrainState(model, image, cfg, sampler=sampler, deterministic=deterministic)
+    state = TrainState(model, image, cfg, sampler=sampler, deterministic=deterministic,
+                       reference_order=reference_order)
     sink = open(cfg.metrics_path, "w") if cfg.metrics_path else None
     losses, step_ms = [], []
     t_start = time.perf_counter()

@@ -241,3 +241,24 @@ def test_live_reference_core_matches_oracle_kernels(d):
     b = REF.probed_fwd(xs, 77, 1024, 512, 3, feats, baked, O.PRIMARY, O.AUX)
     for x, y in zip(a, b):
         eq(x, y)
+
+
+@pytest.mark.parametrize("K,fin,fout", [(8192, 64, 64), (8192, 32, 64), (8192, 64, 3), (128, 64, 64),
+                                        (700, 64, 64), (702, 64, 64), (1000, 32, 64), (8492, 64, 4)])
+def test_openblas_wgrad_order(K, fin, fout):
+    """Pins the summation order of numpy's W_grad += a.T @ delta (OpenBLAS
+    sgemm: K blocked by 448, last two blocks balanced, FMA chain per block)
+    and of delta.sum(axis=0) (sequential) — the order pg_mlp_wgrad_blas_f32
+    reproduces on the GPU (mlp.py:81-82)."""
+    rng = np.random.default_rng(K + fin + fout)
+    a = np.maximum(rng.standard_normal((K, fin)), 0).astype(np.float32)
+    d = (rng.standard_normal((K, fout)) * 1e-3).astype(np.float32)
+    gw0 = (rng.standard_normal((fin, fout)) * 1e-2).astype(np.float32)
+    gb0 = (rng.standard_normal(fout) * 1e-2).astype(np.float32)
+    gw, gb = gw0.copy(), gb0.copy()
+    O.wgrad_blas(a, d, gw, gb)
+    want_w, want_b = gw0.copy(), gb0.copy()
+    want_w += a.T @ d
+    want_b += d.sum(axis=0)
+    eq(gw, want_w)
+    eq(gb, want_b)
