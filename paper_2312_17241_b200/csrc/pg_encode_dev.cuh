@@ -8,6 +8,13 @@
 
 namespace pg {
 
+// 256-bit read-only global load (sm_100: LDG.E.ENL2.256); p 32-byte aligned
+__device__ __forceinline__ void ld_nc_v8(const float *p, float (&v)[8]) {
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+        : "l"(p));
+}
+
 struct LevelGeo2 {
     int res, kind, slot;
 };
@@ -179,13 +186,30 @@ __device__ __forceinline__ void encode_level_bwd2(const pg_grid &g, int l, const
             const float *cr = conf + crow[k0 + u] * n_p;
             const float2 *fb = reinterpret_cast<const float2 *>(ftab + (int64_t)bs[k0 + u] * 2);
             if (NPMAX == 4 && n_p == 4) {
+                // conf row: 16 B; probing range (4 probes x F=2): ONE 32-byte load
                 const float4 c4 = __ldg(reinterpret_cast<const float4 *>(cr));
-                const float4 f01 = __ldg(reinterpret_cast<const float4 *>(fb));
-                const float4 f23 = __ldg(reinterpret_cast<const float4 *>(fb) + 1);
+                float f8[8];
+                ld_nc_v8(reinterpret_cast<const float *>(fb), f8);
                 cv[u][0] = c4.x; cv[u][1 % NPMAX] = c4.y; cv[u][2 % NPMAX] = c4.z; cv[u][3 % NPMAX] = c4.w;
-                fv[u][0][0] = f01.x; fv[u][0][1] = f01.y; fv[u][1 % NPMAX][0] = f01.z; fv[u][1 % NPMAX][1] = f01.w;
-                fv[u][2 % NPMAX][0] = f23.x; fv[u][2 % NPMAX][1] = f23.y;
-                fv[u][3 % NPMAX][0] = f23.z; fv[u][3 % NPMAX][1] = f23.w;
+                fv[u][0][0] = f8[0]; fv[u][0][1] = f8[1]; fv[u][1 % NPMAX][0] = f8[2]; fv[u][1 % NPMAX][1] = f8[3];
+                fv[u][2 % NPMAX][0] = f8[4]; fv[u][2 % NPMAX][1] = f8[5];
+                fv[u][3 % NPMAX][0] = f8[6]; fv[u][3 % NPMAX][1] = f8[7];
+            } else if (NPMAX >= 4 && n_p >= 4) {
+                // groups of 4 probes: 16-byte conf load + 32-byte feature load
+#pragma unroll
+                for (int j0 = 0; j0 < NPMAX; j0 += 4)
+                    if (j0 < n_p) {
+                        const float4 c4 = __ldg(reinterpret_cast<const float4 *>(cr + j0));
+                        float f8[8];
+                        ld_nc_v8(reinterpret_cast<const float *>(fb + j0), f8);
+                        cv[u][j0] = c4.x; cv[u][(j0 + 1) % NPMAX] = c4.y;
+                        cv[u][(j0 + 2) % NPMAX] = c4.z; cv[u][(j0 + 3) % NPMAX] = c4.w;
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            fv[u][(j0 + i) % NPMAX][0] = f8[2 * i];
+                            fv[u][(j0 + i) % NPMAX][1] = f8[2 * i + 1];
+                        }
+                    }
             } else {
 #pragma unroll
                 for (int j = 0; j < NPMAX; ++j)
