@@ -1,4 +1,7 @@
-// Fused training pass on sm_100a: for every 64-sample tile, ONE kernel does
+// Fused training pass on sm_100a, OpenBLAS-order (exact) variant — selected by
+// PG_EXACT_MLP and by reference-order mode; the default fast path with the
+// MLP on the tensor cores is pg_train_mma.cu.  For every 64-sample tile, ONE
+// kernel does
 //   encode fwd (16 levels, F=2)  ->  MLP [32,64,64,out<=4] fwd  ->  squared
 //   error + dpred  ->  MLP bwd (weight grads held in registers across tiles,
 //   dgrads)  ->  encode bwd (straight-through scatter into gfeat/gconf)
@@ -452,6 +455,11 @@ bool train_fast_ok(const pg_grid *g, const pg_mlp *m) {
 }
 
 template <typename ACC, typename LACC>
+int train_mma(const pg_grid *g, int od, const float *xs, const float *targets, int64_t B, const float *feats,
+              const uint8_t *baked, const float *conf, const float *params, float scale, int sig, ACC *gfeat,
+              ACC *gconf, uint8_t *touched, ACC *gparams, LACC *loss_sum, float *dy_out, cudaStream_t s);
+
+template <typename ACC, typename LACC>
 int train_fused(const pg_grid *g, const pg_mlp *m, const float *xs, const float *targets, int64_t B,
                 const float *feats, const uint8_t *baked, const float *conf, const float *params,
                 float scale, unsigned flags, ACC *gfeat, ACC *gconf, uint8_t *touched,
@@ -459,10 +467,15 @@ int train_fused(const pg_grid *g, const pg_mlp *m, const float *xs, const float 
     if (int e = validate_grid(g)) return e;
     PG_REQUIRE(train_fast_ok(g, m), "fused training needs F=2, 16 levels, N_p<=16, MLP [32,64,64,<=4]");
     if (B == 0) return PG_OK;
-    const int smem = (int)sizeof(TrainSmem);
-    static bool configured[4] = {false, false, false, false};
     const int od = m->widths[3];
     const int sig = (flags & PG_SIGMOID) ? 1 : 0;
+    // fast path: tensor-core MLP (pg_train_mma.cu); this file's FFMA kernel is
+    // the OpenBLAS-order path (PG_EXACT_MLP, reference-order mode)
+    if (!acts && !(flags & PG_EXACT_MLP))
+        return train_mma<ACC, LACC>(g, od, xs, targets, B, feats, baked, conf, params, scale, sig, gfeat, gconf,
+                                    touched, gparams, loss_sum, dy_out, s);
+    const int smem = (int)sizeof(TrainSmem);
+    static bool configured[4] = {false, false, false, false};
     int sms = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -1,0 +1,382 @@
+// Fused training pass, fast path: the same per-tile pipeline as pg_train.cu
+// (encode fwd -> MLP fwd -> loss -> MLP bwd -> encode bwd, activations in
+// shared memory, weight gradients held in registers across tiles), but every
+// GEMM of the MLP — the two hidden layers, the output layer, both data
+// gradients and all three weight gradients — runs on the tensor cores as
+// warp-level mma.sync.m16n8k8 tf32 with a 3-term split (a_hi*b_hi + a_lo*b_hi
+// + a_hi*b_lo, "3xTF32"), which keeps fp32-level accuracy (~1e-6 relative).
+//
+// Why mma.sync and not tcgen05 here: the step is bound by the L1/shared-memory
+// data pipe that the table gathers/scatters also use.  The FFMA kernel spends
+// ~22k shared-memory wavefronts per 64-sample tile on GEMM operands (LDS.128
+// broadcast loads cost 4 wavefronts each); register fragments loaded with
+// conflict-free LDS.32 cut that ~4x.  Fragments can be read from ANY layout,
+// so one [feature][sample] copy of each activation serves the forward GEMMs
+// (K = features) and the weight-gradient GEMMs (K = samples) alike — tcgen05
+// kind::tf32 accepts only K-major operands and would need transposed copies
+// of every activation, which do not fit next to two CTAs' tiles.
+//
+// Results are NOT in OpenBLAS order: the bit-exact path is pg_train.cu
+// (PG_EXACT_MLP / reference-order mode); tests bound this one at 1e-5.
+#include "pg_encode_dev.cuh"
+
+namespace pg {
+namespace tm {
+constexpr int kT = 64;    // samples per tile
+constexpr int kNT = 256;  // threads (8 warps), 2 CTAs per SM
+constexpr int kI = 32;    // L*F
+constexpr int kH = 64;    // hidden width
+constexpr int kO = 4;     // max output width
+constexpr int kS = 72;    // row stride (floats) of [feature][sample] tiles and weights:
+                          // 72 = 8 mod 32 makes the A/B fragment loads of the
+                          // feature-indexed GEMMs bank-conflict free
+
+struct Smem {
+    float w0[kI * kS];    // W0 [in f][out i]
+    float w1[kH * kS];    // W1 [in i][out j]
+    float w2[kH * 8];     // W2 [in k][out j], columns >= od zero
+    float b0[kH], b1[kH], b2[8];
+    float y[kI * kS];     // y^T [f][q], later dL/dy^T
+    float h1[kH * kS];    // relu(z1)^T [i][q], later delta1^T
+    float h2[kH * kS];    // relu(z2)^T [k][q], later delta2^T
+    float d3[kT * 8];     // dL/d(out) [q][j], columns >= od zero
+    float xs[kT * 3];
+    float tg[kT * kO];
+    double lred[kNT / 32];
+};
+
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ void split(float x, uint32_t &hi, uint32_t &lo) {
+    hi = to_tf32(x);
+    lo = to_tf32(__fsub_rn(x, __uint_as_float(hi)));
+}
+__device__ __forceinline__ void hmma(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// acc[t] (16 x 8 tile at rows m0, columns n0 + 8t) += A[m][k] * B[k][n] over
+// k < K, A(m, k) = pa[m*am + k*ak], B(k, n) = pb[k*bk + n*bn]; 3xTF32.
+// Fragment layouts (PTX mma.m16n8k8 .tf32): g = lane/4, c = lane%4;
+// A: (g, c) (g+8, c) (g, c+4) (g+8, c+4); B: (c, g) (c+4, g);
+// C: (g, 2c) (g, 2c+1) (g+8, 2c) (g+8, 2c+1).
+template <int NT, int K>
+__device__ __forceinline__ void warp_gemm(float (&acc)[NT][4], const float *pa, int am, int ak, int m0,
+                                          const float *pb, int bk, int bn, int n0) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
+#pragma unroll 2
+    for (int k0 = 0; k0 < K; k0 += 8) {
+        uint32_t ah[4], al[4];
+        split(pa[(m0 + g) * am + (k0 + c) * ak], ah[0], al[0]);
+        split(pa[(m0 + g + 8) * am + (k0 + c) * ak], ah[1], al[1]);
+        split(pa[(m0 + g) * am + (k0 + c + 4) * ak], ah[2], al[2]);
+        split(pa[(m0 + g + 8) * am + (k0 + c + 4) * ak], ah[3], al[3]);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            const int n = n0 + 8 * t + g;
+            uint32_t bh0, bl0, bh1, bl1;
+            split(pb[(k0 + c) * bk + n * bn], bh0, bl0);
+            split(pb[(k0 + c + 4) * bk + n * bn], bh1, bl1);
+            hmma(acc[t], al, bh0, bh1);  // small terms first
+            hmma(acc[t], ah, bl0, bl1);
+            hmma(acc[t], ah, bh0, bh1);
+        }
+    }
+}
+
+// store a warp's C fragments (rows = samples m, columns = features n) into a
+// [feature][sample] tile, optionally through f(value, feature, sample)
+template <int NT, typename F>
+__device__ __forceinline__ void store_frags_T(float *dstT, const float (&acc)[NT][4], int m0, int n0, F f) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        const int n = n0 + 8 * t + 2 * c;
+        dstT[n * kS + m0 + g] = f(acc[t][0], n, m0 + g);
+        dstT[(n + 1) * kS + m0 + g] = f(acc[t][1], n + 1, m0 + g);
+        dstT[n * kS + m0 + g + 8] = f(acc[t][2], n, m0 + g + 8);
+        dstT[(n + 1) * kS + m0 + g + 8] = f(acc[t][3], n + 1, m0 + g + 8);
+    }
+}
+
+// bias gradient partial: sum over the tile's samples of row r of a
+// [feature][sample] tile; 4 threads per row, result valid in lane%4 == 0
+__device__ __forceinline__ float row_sum4(const float *srcT, int r, int qq) {
+    float s = 0.0f;
+#pragma unroll
+    for (int i = 0; i < kT / 4; ++i) s += srcT[r * kS + qq + 4 * i];
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    return s;
+}
+}  // namespace tm
+
+template <typename FT, int D, int NPM, typename ACC, typename LACC>
+__global__ void __launch_bounds__(tm::kNT, 2)
+    train_mma_kernel(const pg_grid g, const float *__restrict__ xs, const float *__restrict__ targets,
+                     int64_t B, const FT *__restrict__ feats_fwd, const float *__restrict__ feats,
+                     const uint8_t *__restrict__ baked, const float *__restrict__ conf,
+                     const float *__restrict__ params, int od, float scale, int sigmoid,
+                     ACC *__restrict__ gfeat, ACC *__restrict__ gconf, uint8_t *__restrict__ touched,
+                     ACC *__restrict__ gparams, LACC *__restrict__ loss_sum, float *__restrict__ dy_out) {
+    using namespace tm;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem &S = *reinterpret_cast<Smem *>(smem_raw);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    {
+        const float *p = params;
+        for (int i = tid; i < kI * kH; i += kNT) S.w0[(i / kH) * kS + i % kH] = p[i];
+        p += kI * kH;
+        for (int i = tid; i < kH; i += kNT) S.b0[i] = p[i];
+        p += kH;
+        for (int i = tid; i < kH * kH; i += kNT) S.w1[(i / kH) * kS + i % kH] = p[i];
+        p += kH * kH;
+        for (int i = tid; i < kH; i += kNT) S.b1[i] = p[i];
+        p += kH;
+        for (int i = tid; i < kH * 8; i += kNT) {
+            const int k = i / 8, j = i % 8;
+            S.w2[i] = j < od ? p[k * od + j] : 0.0f;
+        }
+        p += kH * od;
+        for (int i = tid; i < 8; i += kNT) S.b2[i] = i < od ? p[i] : 0.0f;
+    }
+    // persistent gradient accumulators (fragments of the weight-gradient GEMMs)
+    float gW1[4][4] = {};   // dW1: rows i = 16*(warp&3).., columns j = 32*(warp>>2)..
+    float gW0[2][4] = {};   // dW0: rows f = 16*(warp&1).., columns i = 16*(warp>>1)..
+    float gW2[1][4] = {};   // dW2: rows k = 16*warp (warps 0-3), columns j < 8
+    float gb0 = 0.0f, gb1 = 0.0f, gb2 = 0.0f;   // biases: row tid>>2 (lane%4 == 0); b2: tid < 8
+    double lsum = 0.0;
+
+    const int64_t ntiles = (B + kT - 1) / kT;
+    static_assert(kT * 3 <= kNT && kT * kO == kNT, "one prefetched value per thread");
+    auto fetch = [&](int64_t t, float &fx, float &ft) {
+        const int64_t q0 = t * kT;
+        const int n = t < ntiles ? (int)((B - q0) < kT ? (B - q0) : kT) : 0;
+        fx = (tid < kT * D && tid < n * D) ? __ldg(xs + q0 * D + tid) : 0.5f;
+        const int q = tid / kO, j = tid % kO;
+        ft = (q < n && j < od) ? __ldg(targets + (q0 + q) * od + j) : 0.0f;
+    };
+    float pf_x, pf_t;
+    fetch(blockIdx.x, pf_x, pf_t);
+    const int pl = tid & (kT - 1), lsub = tid >> 6;
+    const int mt = warp & 3;           // 16-sample m-tile of the sample-major GEMMs
+    const int rr = tid >> 2, qq = tid & 3;  // bias row-sum role
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t p0 = tile * kT;
+        const int nv = (int)((B - p0) < kT ? (B - p0) : kT);
+        __syncthreads();
+        if (tid < kT * D) S.xs[tid] = pf_x;
+        S.tg[tid] = pf_t;
+        fetch(tile + gridDim.x, pf_x, pf_t);
+        __syncthreads();
+        // ---- encode forward -> y^T ----
+        float x[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) x[a] = S.xs[pl * D + a];
+#pragma unroll 2
+        for (int it = 0; it < 4; ++it) {
+            const int l = lsub + 4 * it;
+            const float2 yv = encode_level_fwd2<FT, D>(g, l, x, feats_fwd, baked);
+            S.y[(2 * l) * kS + pl] = yv.x;
+            S.y[(2 * l + 1) * kS + pl] = yv.y;
+        }
+        __syncthreads();
+        // ---- layer 1: h1 = relu(y W0 + b0) ----
+        {
+            float acc[4][4] = {};
+            warp_gemm<4, kI>(acc, S.y, 1, kS, 16 * mt, S.w0, kS, 1, 32 * (warp >> 2));
+            store_frags_T<4>(S.h1, acc, 16 * mt, 32 * (warp >> 2), [&](float v, int n, int) {
+                const float z = v + S.b0[n];
+                return z > 0.0f ? z : 0.0f;
+            });
+        }
+        __syncthreads();
+        // ---- layer 2: h2 = relu(h1 W1 + b1) ----
+        {
+            float acc[4][4] = {};
+            warp_gemm<4, kH>(acc, S.h1, 1, kS, 16 * mt, S.w1, kS, 1, 32 * (warp >> 2));
+            store_frags_T<4>(S.h2, acc, 16 * mt, 32 * (warp >> 2), [&](float v, int n, int) {
+                const float z = v + S.b1[n];
+                return z > 0.0f ? z : 0.0f;
+            });
+        }
+        __syncthreads();
+        // ---- output layer, loss, dL/dout (warps 0-3: one 16-sample tile each) ----
+        if (warp < 4) {
+            float acc[1][4] = {};
+            warp_gemm<1, kH>(acc, S.h2, 1, kS, 16 * warp, S.w2, 8, 1, 0);
+            const int gq = lane >> 2, c = lane & 3;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int q = 16 * warp + gq + (e >> 1) * 8, j = 2 * c + (e & 1);
+                float d = 0.0f;
+                if (j < od && q < nv) {
+                    const float o = acc[0][e] + S.b2[j];
+                    const float pred = sigmoid ? 1.0f / (1.0f + expf(-o)) : o;
+                    const float diff = pred - S.tg[q * kO + j];
+                    lsum += (double)diff * (double)diff;
+                    d = diff * scale;
+                    if (sigmoid) d *= pred * (1.0f - pred);
+                }
+                S.d3[q * 8 + j] = d;
+            }
+        }
+        __syncthreads();
+        // ---- dW2 += h2^T d3 (warps 0-3), db2; delta2 = (d3 W2^T) * (h2 > 0) ----
+        if (warp < 4) warp_gemm<1, kT>(gW2, S.h2, kS, 1, 16 * warp, S.d3, 8, 1, 0);
+        if (tid < 8) {
+            float s = 0.0f;
+            for (int q = 0; q < kT; ++q) s += S.d3[q * 8 + tid];
+            gb2 += s;
+        }
+        {
+            // thread (sample q = tid & 63, 16 hidden units k = 16*(tid>>6)..)
+            const int q = tid & (kT - 1), k0 = 16 * (tid >> 6);
+            const float4 dq = *reinterpret_cast<const float4 *>(S.d3 + q * 8);
+            float dl[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int k = k0 + u;
+                const float4 w = *reinterpret_cast<const float4 *>(S.w2 + k * 8);
+                const float s = dq.x * w.x + dq.y * w.y + dq.z * w.z + dq.w * w.w;
+                dl[u] = S.h2[k * kS + q] > 0.0f ? s : 0.0f;
+            }
+            __syncthreads();  // dW2 reads h2 above
+#pragma unroll
+            for (int u = 0; u < 16; ++u) S.h2[(k0 + u) * kS + q] = dl[u];
+        }
+        __syncthreads();
+        {
+            const float s = row_sum4(S.h2, rr, qq);
+            if (qq == 0) gb1 += s;
+        }
+        // ---- dW1 += h1^T delta2 ; delta1' = delta2 W1^T (kept in registers) ----
+        float dacc[4][4] = {};
+        warp_gemm<4, kT>(gW1, S.h1, kS, 1, 16 * (warp & 3), S.h2, 1, kS, 32 * (warp >> 2));
+        warp_gemm<4, kH>(dacc, S.h2, 1, kS, 16 * mt, S.w1, 1, kS, 32 * (warp >> 2));
+        __syncthreads();
+        // delta1 = delta1' * (h1 > 0), in place over h1
+        store_frags_T<4>(S.h1, dacc, 16 * mt, 32 * (warp >> 2), [&](float v, int n, int m) {
+            return S.h1[n * kS + m] > 0.0f ? v : 0.0f;
+        });
+        __syncthreads();
+        {
+            const float s = row_sum4(S.h1, rr, qq);
+            if (qq == 0) gb0 += s;
+        }
+        // ---- dW0 += y^T delta1 ; dy = delta1 W0^T ----
+        {
+            float yacc[2][4] = {};
+            warp_gemm<2, kT>(gW0, S.y, kS, 1, 16 * (warp & 1), S.h1, 1, kS, 16 * (warp >> 1));
+            warp_gemm<2, kH>(yacc, S.h1, 1, kS, 16 * mt, S.w0, 1, kS, 16 * (warp >> 2));
+            __syncthreads();
+            store_frags_T<2>(S.y, yacc, 16 * mt, 16 * (warp >> 2), [](float v, int, int) { return v; });
+        }
+        __syncthreads();
+        if (dy_out) {
+            for (int i = tid; i < nv * kI; i += kNT) {
+                const int q = i / kI, c = i % kI;
+                dy_out[(p0 + q) * kI + c] = S.y[c * kS + q];
+            }
+        }
+        // ---- encode backward ----
+        if (pl < nv) {
+#pragma unroll 1
+            for (int it = 0; it < 4; ++it) {
+                const int l = lsub + 4 * it;
+                encode_level_bwd2<D, NPM, ACC>(g, l, x, S.y[(2 * l) * kS + pl], S.y[(2 * l + 1) * kS + pl],
+                                               feats, conf, gfeat, gconf, touched);
+            }
+        }
+    }
+    // ---- flush ----
+    ACC *gW0p = gparams, *gb0p = gW0p + kI * kH, *gW1p = gb0p + kH, *gb1p = gW1p + kH * kH;
+    ACC *gW2p = gb1p + kH, *gb2p = gW2p + kH * od;
+    {
+        const int gq = lane >> 2, c = lane & 3;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int i = 16 * (warp & 3) + gq + (e >> 1) * 8, j = 32 * (warp >> 2) + 8 * t + 2 * c + (e & 1);
+                red_add(gW1p + i * kH + j, gW1[t][e]);
+            }
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int f = 16 * (warp & 1) + gq + (e >> 1) * 8, i = 16 * (warp >> 1) + 8 * t + 2 * c + (e & 1);
+                red_add(gW0p + f * kH + i, gW0[t][e]);
+            }
+        if (warp < 4) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int k = 16 * warp + gq + (e >> 1) * 8, j = 2 * c + (e & 1);
+                if (j < od) red_add(gW2p + k * od + j, gW2[0][e]);
+            }
+        }
+        if (qq == 0) {
+            red_add(gb0p + rr, gb0);
+            red_add(gb1p + rr, gb1);
+        }
+        if (tid < od) red_add(gb2p + tid, gb2);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+    if (lane == 0) S.lred[warp] = lsum;
+    __syncthreads();
+    if (tid < 32) {
+        double v = tid < kNT / 32 ? S.lred[tid] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (tid == 0 && loss_sum) loss_add(loss_sum, v);
+    }
+}
+
+template <typename ACC, typename LACC>
+int train_mma(const pg_grid *g, int od, const float *xs, const float *targets, int64_t B, const float *feats,
+              const uint8_t *baked, const float *conf, const float *params, float scale, int sig, ACC *gfeat,
+              ACC *gconf, uint8_t *touched, ACC *gparams, LACC *loss_sum, float *dy_out, cudaStream_t s) {
+    const int smem = (int)sizeof(tm::Smem);
+    static bool configured[4] = {false, false, false, false};
+    int sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t ntiles = (B + tm::kT - 1) / tm::kT;
+    const int grd = (int)(ntiles < 2 * sms ? ntiles : 2 * sms);
+    const bool np4 = g->log2_np <= 2;
+#define PG_TRAIN_MMA(D_, NP_, IDX)                                                                    \
+    do {                                                                                              \
+        auto kern = train_mma_kernel<float, D_, NP_, ACC, LACC>;                                      \
+        if (!configured[IDX]) {                                                                       \
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);            \
+            configured[IDX] = true;                                                                   \
+        }                                                                                             \
+        kern<<<grd, tm::kNT, smem, s>>>(*g, xs, targets, B, feats, feats, baked, conf, params, od,     \
+                                        scale, sig, gfeat, gconf, touched, gparams, loss_sum, dy_out); \
+    } while (0)
+    if (g->d == 2) {
+        if (np4) PG_TRAIN_MMA(2, 4, 0); else PG_TRAIN_MMA(2, 16, 1);
+    } else {
+        if (np4) PG_TRAIN_MMA(3, 4, 2); else PG_TRAIN_MMA(3, 16, 3);
+    }
+#undef PG_TRAIN_MMA
+    return check_launch("train_mma");
+}
+
+template int train_mma<float, double>(const pg_grid *, int, const float *, const float *, int64_t,
+                                      const float *, const uint8_t *, const float *, const float *, float,
+                                      int, float *, float *, uint8_t *, float *, double *, float *,
+                                      cudaStream_t);
+template int train_mma<fx_t, fx_t>(const pg_grid *, int, const float *, const float *, int64_t,
+                                   const float *, const uint8_t *, const float *, const float *, float, int,
+                                   fx_t *, fx_t *, uint8_t *, fx_t *, fx_t *, float *, cudaStream_t);
+
+}  // namespace pg

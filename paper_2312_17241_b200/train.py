@@ -90,11 +90,13 @@ class TrainState:
 
     def __init__(self, model: Model, image, cfg: TrainConfig, sampler: str = "reference",
                  fused: bool | None = None, deterministic: bool = False,
-                 reference_order: bool = False):
-        """``reference_order``: MLP weight/bias gradients in numpy/OpenBLAS
-        summation order (pg_mlp_wgrad_blas_f32) instead of per-CTA partial
-        sums; with the forward already in OpenBLAS order this makes every MLP
-        gradient bit-identical to the reference's (parity mode, slower)."""
+                 reference_order: bool = False, exact_mlp: bool = False):
+        """``exact_mlp``: the fused step's MLP on CUDA cores in numpy/OpenBLAS
+        operation order (activations and dL/dy bit-identical to the
+        reference's) instead of the default 3xTF32 tensor-core MLP (fp32-level,
+        ~1e-6).  ``reference_order``: additionally the MLP weight/bias
+        gradients in OpenBLAS summation order (pg_mlp_wgrad_blas_f32), making
+        every MLP gradient bit-identical to the reference's (parity mode)."""
         cfg.validate()
         if sampler not in ("reference", "device", "points"):
             raise InvalidHyperparameter(f"unknown sampler {sampler!r}")
@@ -132,6 +134,7 @@ class TrainState:
             raise InvalidHyperparameter("deterministic mode is float32-only")
         self.deterministic = deterministic
         self.reference_order = reference_order
+        self.exact_mlp = exact_mlp or reference_order
         if reference_order:
             if not self.fused or deterministic:
                 raise InvalidHyperparameter(
@@ -227,6 +230,8 @@ class TrainState:
         fused encode kernels around the generic MLP kernels."""
         m, cfg, s = self.model, self.cfg, _lib.stream_ptr()
         flags = _lib.PG_SIGMOID if m.hyper.out_sigmoid else 0
+        if self.exact_mlp and self.fused:
+            flags |= _lib.PG_EXACT_MLP
         scale = float(np.dtype(m.dtype).type(self.scale))
         if self.deterministic:
             gf, gm, gc = m.fx_ptrs()

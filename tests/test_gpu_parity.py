@@ -42,6 +42,16 @@ def eq(a, b):
     np.testing.assert_array_equal(a, b)
 
 
+def close_grad(actual, desired, atol, tensor):
+    """Gradient check: rtol 1e-5.  With the 3xTF32 tensor-core MLP every
+    product carries ~5e-7 relative error (tf32 hi/lo split), so sums that
+    cancel (bias / confidence gradients over thousands of samples) get an
+    absolute floor of 1e-5 of the array's largest magnitude as well."""
+    if tensor:
+        atol = max(atol, 1e-5 * float(np.abs(desired).max()))
+    np.testing.assert_allclose(actual, desired, rtol=1e-5, atol=atol)
+
+
 # ---------------------------------------------------------------- protocol
 @pytest.mark.parametrize("tag", ["float32", "float64"])
 @pytest.mark.parametrize("d", [2, 3])
@@ -240,7 +250,7 @@ def test_train_step_parity_c1():
     import paper_2312_17241_b200 as pg
     img = _smooth()
     st = pg.TrainState(pg.init_model(pg.HyperParams(**C1), seed=0), img,
-                       pg.TrainConfig(batch_size=8192, seed=0))
+                       pg.TrainConfig(batch_size=8192, seed=0), exact_mlp=True)
     ost = O.TrainState(O.init_model(O.Hyper(**C1), seed=0), img, O.TrainCfg(batch_size=8192, seed=0))
     # Confidences: Adam normalises each element's gradient, so an element
     # whose gradient is ~0 moves by up to +-lr per step on rounding noise.
@@ -275,15 +285,18 @@ def test_train_step_parity_c1():
             assert frac <= conf_bar and bfrac <= baked_bar
 
 
-@pytest.mark.parametrize("fused", [True, False])
-def test_step_gradients_vs_oracle(fused):
-    """Gradients of one batch (no optimizer): dL/dy BIT-EXACT with the
-    reference's numpy/OpenBLAS MLP (FMA-chain order), loss bit-exact up to the
-    fp64 summation order, MLP and table gradients within 1e-5."""
+@pytest.mark.parametrize("mode", ["fused_exact", "generic", "fused_tensor"])
+def test_step_gradients_vs_oracle(mode):
+    """Gradients of one batch (no optimizer) against numpy/OpenBLAS.  The
+    OpenBLAS-order MLPs (fused exact_mlp, generic kernels): dL/dy BIT-EXACT,
+    loss exact up to the fp64 summation order.  The default 3xTF32 tensor-core
+    MLP: dL/dy and loss within 1e-5.  MLP and table gradients within 1e-5."""
     import paper_2312_17241_b200 as pg
     img = _smooth()
     m, om = _models(C1, perturb=False)
-    st = pg.TrainState(m, img, pg.TrainConfig(batch_size=8192, seed=0), fused=fused)
+    fused = mode != "generic"
+    st = pg.TrainState(m, img, pg.TrainConfig(batch_size=8192, seed=0), fused=fused,
+                       exact_mlp=mode == "fused_exact")
     assert st.fused == fused
     xs, targets = st.sample_batch()
     dy = torch.empty((8192, 32), device="cuda")
@@ -300,20 +313,25 @@ def test_step_gradients_vs_oracle(fused):
     oloss = float(np.mean(diff.astype(np.float64) ** 2))
     dpred = diff * np.float32(2.0 / diff.size)
     ody = O.mlp_backward(om.W, om.Wg, om.bg, cache, dpred)
-    eq(dy.cpu().numpy(), ody)
-    assert abs(loss - oloss) <= 1e-12 * oloss
+    if mode == "fused_tensor":
+        np.testing.assert_allclose(dy.cpu().numpy(), ody, rtol=1e-5, atol=1e-10)
+        assert abs(loss - oloss) <= 1e-6 * oloss
+    else:
+        eq(dy.cpu().numpy(), ody)
+        assert abs(loss - oloss) <= 1e-12 * oloss
     O.encode_backward(om, traces, ody)
     gw = [w.cpu().numpy() for w in m.mlp.weight_grads]
     gb = [b.cpu().numpy() for b in m.mlp.bias_grads]
+    tc = mode == "fused_tensor"
     for i in range(3):
-        np.testing.assert_allclose(gw[i], om.Wg[i], rtol=1e-5, atol=1e-9)
-        np.testing.assert_allclose(gb[i], om.bg[i], rtol=1e-5, atol=1e-9)
+        close_grad(gw[i], om.Wg[i], 1e-9, tc)
+        close_grad(gb[i], om.bg[i], 1e-9, tc)
     gf = m.gfeats.cpu().numpy()
     gc = m.gconf.cpu().numpy()
     for L in om.levels:
-        np.testing.assert_allclose(gf[L.level], L.fgrad, rtol=1e-5, atol=1e-10)
+        close_grad(gf[L.level], L.fgrad, 1e-10, tc)
     for i, lv in enumerate(m.probed):
-        np.testing.assert_allclose(gc[i], om.levels[lv].cgrad, rtol=1e-5, atol=1e-10)
+        close_grad(gc[i], om.levels[lv].cgrad, 1e-10, tc)
 
 
 @pytest.mark.parametrize("od", [3, 2, 4])
@@ -361,22 +379,24 @@ def test_loss_curve_reference_order_30_steps():
     assert rel.max() <= 5e-5
 
 
-def test_loss_curve_tracks_reference_30_steps():
+@pytest.mark.parametrize("exact", [True, False])
+def test_loss_curve_tracks_reference_30_steps(exact):
     import paper_2312_17241_b200 as pg
     img = _smooth()
     st = pg.TrainState(pg.init_model(pg.HyperParams(**C1), seed=0), img,
-                       pg.TrainConfig(batch_size=8192, seed=0))
+                       pg.TrainConfig(batch_size=8192, seed=0), exact_mlp=exact)
     ost = O.TrainState(O.init_model(O.Hyper(**C1), seed=0), img, O.TrainCfg(batch_size=8192, seed=0))
     a = np.array([st.step() for _ in range(30)])
     b = np.array([ost.step() for _ in range(30)])
     rel = np.abs(a - b) / b
-    print("max rel loss diff over 30 steps:", rel.max(), "first 10:", rel[:10].max())
+    print(f"exact_mlp={exact}: max rel loss diff over 30 steps:", rel.max(), "first 10:", rel[:10].max())
     # SURVEY 8(c) asks <= 1e-5 for ~30 steps on the smooth image; the
     # reference's own backends reach 1.1e-6 there because they share one BLAS
     # MLP (identical weight gradients).  Ours reorders the cross-sample weight-
-    # gradient sums (atomics), and Adam turns that into +-lr moves on ~zero-
-    # gradient weights: measured drift 1e-7 over the first 10 steps, 2e-5 ..
-    # 1.5e-4 by step 30 depending on the run (the reference's own backends
+    # gradient sums, and Adam turns that into +-lr moves on ~zero-gradient
+    # weights (reference_order mode removes that: see the test above).
+    # Measured on B200, first 10 / 30 steps: exact MLP 2e-7 / 2e-5..1.5e-4,
+    # 3xTF32 tensor-core MLP 1.4e-6 / 3.3e-5 (the reference's own backends
     # drift 2e-4 by step 50 on the noise image).  Bars: 1e-5 / 5e-4.
     assert rel[:10].max() <= 1e-5
     assert rel.max() <= 5e-4
@@ -568,11 +588,11 @@ def test_deterministic_gradients_match_oracle():
     O.encode_backward(om, traces, ody)
     oloss = float(np.mean(diff.astype(np.float64) ** 2))
     assert abs(float(st.loss_sum.item()) / (8192 * 3) - oloss) <= 1e-9 * oloss
-    for i in range(3):
-        np.testing.assert_allclose(m.mlp.weight_grads[i].cpu().numpy(), om.Wg[i], rtol=1e-5, atol=1e-9)
+    for i in range(3):   # deterministic mode runs the tensor-core MLP
+        close_grad(m.mlp.weight_grads[i].cpu().numpy(), om.Wg[i], 1e-9, True)
     gf = m.gfeats.cpu().numpy()
     for L in om.levels:
-        np.testing.assert_allclose(gf[L.level], L.fgrad, rtol=1e-5, atol=1e-10)
+        close_grad(gf[L.level], L.fgrad, 1e-10, True)
 
 
 def test_full_pipeline_gradients_match_finite_differences_f64():
@@ -632,17 +652,19 @@ def test_full_pipeline_gradients_match_finite_differences_f64():
     print("full-pipeline FD worst relative error", worst)
 
 
+@pytest.mark.parametrize("exact", [True, False])
 @pytest.mark.parametrize("n_p,out_dim", [(4, 1), (8, 4)])
-def test_field_trainer_3d_gradients_vs_oracle(n_p, out_dim):
+def test_field_trainer_3d_gradients_vs_oracle(n_p, out_dim, exact):
     """C3 / C4 shapes (d = 3): the fused 3-D training pass. dL/dy bit-exact
-    vs numpy/OpenBLAS, MLP and table gradients within 1e-5."""
+    vs numpy/OpenBLAS with the exact MLP (1e-5 with the tensor-core MLP), MLP
+    and table gradients within 1e-5."""
     import paper_2312_17241_b200 as pg
     kw = dict(d=3, n_f=2**8, n_c=2**16, n_p=n_p, n_max=512, out_dim=out_dim)
     m, om = _models(kw, perturb=False)
     rng = np.random.default_rng(2)
     x = rng.random((4096, 3), dtype=np.float32)
     v = rng.random((4096, out_dim), dtype=np.float32)
-    st = pg.FieldTrainState(m, x, v, pg.TrainConfig(batch_size=4096, seed=0))
+    st = pg.FieldTrainState(m, x, v, pg.TrainConfig(batch_size=4096, seed=0), exact_mlp=exact)
     assert st.fused
     xs, tg = st.sample_batch()
     dy = torch.empty((4096, 32), device="cuda")
@@ -652,18 +674,18 @@ def test_field_trainer_3d_gradients_vs_oracle(n_p, out_dim):
     out, cache = O.mlp_forward(om.W, om.b, y)
     diff = out - v
     ody = O.mlp_backward(om.W, om.Wg, om.bg, cache, diff * np.float32(2.0 / diff.size))
-    if out_dim == 1:
+    if out_dim == 1 or not exact:
         # OpenBLAS forwards N = 1 GEMMs to its GEMV kernel, which sums in a
         # different order than the GEMM microkernel: tolerance, not bits
-        np.testing.assert_allclose(dy.cpu().numpy(), ody, rtol=1e-5, atol=1e-10)
+        close_grad(dy.cpu().numpy(), ody, 1e-10, not exact)
     else:
         eq(dy.cpu().numpy(), ody)
     O.encode_backward(om, traces, ody)
     gf = m.gfeats.cpu().numpy()
     gc = m.gconf.cpu().numpy()
     for L in om.levels:
-        np.testing.assert_allclose(gf[L.level], L.fgrad, rtol=1e-5, atol=1e-10)
+        close_grad(gf[L.level], L.fgrad, 1e-10, not exact)
     for i, lv in enumerate(m.probed):
-        np.testing.assert_allclose(gc[i], om.levels[lv].cgrad, rtol=1e-5, atol=1e-10)
+        close_grad(gc[i], om.levels[lv].cgrad, 1e-10, not exact)
     for i in range(3):
-        np.testing.assert_allclose(m.mlp.weight_grads[i].cpu().numpy(), om.Wg[i], rtol=1e-5, atol=1e-9)
+        close_grad(m.mlp.weight_grads[i].cpu().numpy(), om.Wg[i], 1e-9, not exact)
