@@ -17,31 +17,10 @@
 // reference for the same parameters and batch; only the cross-sample sums
 // (weight/bias gradients, table scatters) are reordered.
 #include "pg_encode_dev.cuh"
+#include "pg_phase.cuh"
 
 namespace pg {
 
-// Optional per-phase cycle accounting (make prof -> tools/_prof/): thread 0 of
-// every CTA adds the clock64() time between consecutive barriers to
-// g_phase_cycles[phase]; read with pg_phase_prof_read.
-#ifdef PG_PHASE_PROF
-__device__ unsigned long long g_phase_cycles[16];
-#define PG_PH_INIT                  \
-    long long ph_t = clock64();     \
-    unsigned long long ph_acc[12] = {};
-#define PG_PH(i)                                   \
-    do {                                           \
-        const long long ph_n = clock64();          \
-        ph_acc[i] += (unsigned long long)(ph_n - ph_t); \
-        ph_t = ph_n;                               \
-    } while (0)
-#define PG_PH_FLUSH                                                         \
-    if (threadIdx.x == 0)                                                   \
-        for (int i = 0; i < 12; ++i) atomicAdd(&g_phase_cycles[i], ph_acc[i]);
-#else
-#define PG_PH_INIT
-#define PG_PH(i)
-#define PG_PH_FLUSH
-#endif
 
 constexpr int kT = 64;    // samples per tile
 constexpr int kNT = 256;  // threads per CTA (2 CTAs per SM: one's memory-bound
@@ -503,16 +482,7 @@ int train_fused(const pg_grid *g, const pg_mlp *m, const float *xs, const float 
 
 }  // namespace pg
 
-#ifdef PG_PHASE_PROF
-extern "C" int pg_phase_prof_read(unsigned long long *out16, int reset) {
-    cudaMemcpyFromSymbol(out16, pg::g_phase_cycles, 16 * sizeof(unsigned long long));
-    if (reset) {
-        static const unsigned long long zero[16] = {};
-        cudaMemcpyToSymbol(pg::g_phase_cycles, zero, sizeof(zero));
-    }
-    return pg::check_launch("phase_prof_read");
-}
-#endif
+PG_PH_READER(pg_phase_prof_read)
 
 extern "C" int pg_train_fused_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
                                   const float *targets, int64_t B, const float *feats,

@@ -19,6 +19,7 @@
 // Results are NOT in OpenBLAS order: the bit-exact path is pg_train.cu
 // (PG_EXACT_MLP / reference-order mode); tests bound this one at 1e-5.
 #include "pg_encode_dev.cuh"
+#include "pg_phase.cuh"
 
 namespace pg {
 namespace tm {
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(tm::kNT, 2)
     float gW2[1][4] = {};   // dW2: rows k = 16*warp (warps 0-3), columns j < 8
     float gb0 = 0.0f, gb1 = 0.0f, gb2 = 0.0f;   // biases: row tid>>2 (lane%4 == 0); b2: tid < 8
     double lsum = 0.0;
+    PG_PH_INIT
 
     const int64_t ntiles = (B + kT - 1) / kT;
     static_assert(kT * 3 <= kNT && kT * kO == kNT, "one prefetched value per thread");
@@ -172,10 +174,12 @@ __global__ void __launch_bounds__(tm::kNT, 2)
         const int64_t p0 = tile * kT;
         const int nv = (int)((B - p0) < kT ? (B - p0) : kT);
         __syncthreads();
+        PG_PH(11);
         if (tid < kT * D) S.xs[tid] = pf_x;
         S.tg[tid] = pf_t;
         fetch(tile + gridDim.x, pf_x, pf_t);
         __syncthreads();
+        PG_PH(0);
         // ---- encode forward -> y^T ----
         float x[D];
 #pragma unroll
@@ -188,6 +192,7 @@ __global__ void __launch_bounds__(tm::kNT, 2)
             S.y[(2 * l + 1) * kS + pl] = yv.y;
         }
         __syncthreads();
+        PG_PH(1);
         // ---- layer 1: h1 = relu(y W0 + b0) ----
         {
             float acc[4][4] = {};
@@ -198,6 +203,7 @@ __global__ void __launch_bounds__(tm::kNT, 2)
             });
         }
         __syncthreads();
+        PG_PH(2);
         // ---- layer 2: h2 = relu(h1 W1 + b1) ----
         {
             float acc[4][4] = {};
@@ -208,6 +214,7 @@ __global__ void __launch_bounds__(tm::kNT, 2)
             });
         }
         __syncthreads();
+        PG_PH(3);
         // ---- output layer, loss, dL/dout (warps 0-3: one 16-sample tile each) ----
         if (warp < 4) {
             float acc[1][4] = {};
@@ -229,6 +236,7 @@ __global__ void __launch_bounds__(tm::kNT, 2)
             }
         }
         __syncthreads();
+        PG_PH(4);
         // ---- dW2 += h2^T d3 (warps 0-3), db2; delta2 = (d3 W2^T) * (h2 > 0) ----
         if (warp < 4) warp_gemm<1, kT>(gW2, S.h2, kS, 1, 16 * warp, S.d3, 8, 1, 0);
         if (tid < 8) {
@@ -249,10 +257,12 @@ __global__ void __launch_bounds__(tm::kNT, 2)
                 dl[u] = S.h2[k * kS + q] > 0.0f ? s : 0.0f;
             }
             __syncthreads();  // dW2 reads h2 above
+            PG_PH(5);
 #pragma unroll
             for (int u = 0; u < 16; ++u) S.h2[(k0 + u) * kS + q] = dl[u];
         }
         __syncthreads();
+        PG_PH(6);
         {
             const float s = row_sum4(S.h2, rr, qq);
             if (qq == 0) gb1 += s;
@@ -262,11 +272,13 @@ __global__ void __launch_bounds__(tm::kNT, 2)
         warp_gemm<4, kT>(gW1, S.h1, kS, 1, 16 * (warp & 3), S.h2, 1, kS, 32 * (warp >> 2));
         warp_gemm<4, kH>(dacc, S.h2, 1, kS, 16 * mt, S.w1, 1, kS, 32 * (warp >> 2));
         __syncthreads();
+        PG_PH(7);
         // delta1 = delta1' * (h1 > 0), in place over h1
         store_frags_T<4>(S.h1, dacc, 16 * mt, 32 * (warp >> 2), [&](float v, int n, int m) {
             return S.h1[n * kS + m] > 0.0f ? v : 0.0f;
         });
         __syncthreads();
+        PG_PH(8);
         {
             const float s = row_sum4(S.h1, rr, qq);
             if (qq == 0) gb0 += s;
@@ -277,9 +289,11 @@ __global__ void __launch_bounds__(tm::kNT, 2)
             warp_gemm<2, kT>(gW0, S.y, kS, 1, 16 * (warp & 1), S.h1, 1, kS, 16 * (warp >> 1));
             warp_gemm<2, kH>(yacc, S.h1, 1, kS, 16 * mt, S.w0, 1, kS, 16 * (warp >> 2));
             __syncthreads();
+            PG_PH(9);
             store_frags_T<2>(S.y, yacc, 16 * mt, 16 * (warp >> 2), [](float v, int, int) { return v; });
         }
         __syncthreads();
+        PG_PH(10);
         if (dy_out) {
             for (int i = tid; i < nv * kI; i += kNT) {
                 const int q = i / kI, c = i % kI;
@@ -296,6 +310,7 @@ __global__ void __launch_bounds__(tm::kNT, 2)
             }
         }
     }
+    PG_PH_FLUSH
     // ---- flush ----
     ACC *gW0p = gparams, *gb0p = gW0p + kI * kH, *gW1p = gb0p + kH, *gb1p = gW1p + kH * kH;
     ACC *gW2p = gb1p + kH, *gb2p = gW2p + kH * od;
@@ -339,6 +354,8 @@ __global__ void __launch_bounds__(tm::kNT, 2)
         if (tid == 0 && loss_sum) loss_add(loss_sum, v);
     }
 }
+
+PG_PH_READER(pg_phase_prof_read_mma)
 
 template <typename ACC, typename LACC>
 int train_mma(const pg_grid *g, int od, const float *xs, const float *targets, int64_t B, const float *feats,
