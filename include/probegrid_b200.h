@@ -252,6 +252,15 @@ int pg_train_fused_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
                        float *gparams, double *loss_sum, float *dy_out,
                        void *stream);
 
+/* .cngp index blocks (model_io.py:150-165, FORMAT.md "Index block packing"):
+ * n_rows blocks of n_c probe offsets at w = log2_np bits each, entry k in
+ * bits [k*w, (k+1)*w) LSB-first within bytes, each block padded to
+ * ceil(n_c*w/8) bytes.  Device pointers; exact integer transforms. */
+int pg_unpack_indices(const uint8_t *packed, int64_t n_rows, int64_t n_c,
+                      int log2_np, uint8_t *entries, void *stream);
+int pg_pack_indices(const uint8_t *entries, int64_t n_rows, int64_t n_c,
+                    int log2_np, uint8_t *packed, void *stream);
+
 /* Reference-order MLP gradients (parity mode).  pg_train_fused_ref_f32 is
  * pg_train_fused_f32 except that it leaves gparams untouched and writes, per
  * sample, every layer's input and output delta to acts, laid out as

@@ -9,8 +9,9 @@ libprobegrid_b200.so and fails loudly if it or a CUDA device is missing.
 
 __version__ = "0.1.0"
 
-from .errors import (DomainViolation, InvalidHyperparameter, ProbeGridError, ShapeMismatch,
-                     StaleTrace, TrainingDiverged, UnbakedModel)
+from .errors import (BadMagic, DomainViolation, InvalidHyperparameter, InvariantViolation,
+                     ModelFileError, ProbeGridError, ShapeMismatch, StaleTrace, TrainingDiverged,
+                     TruncatedFile, UnbakedModel, VersionMismatch)
 from .hyper import (AUX_PRIMES, PRIMARY_PRIMES, HyperParams, LevelMode, LevelSpec,
                     build_level_specs, level_resolution)
 
@@ -20,6 +21,9 @@ __all__ = [
     "ShapeMismatch", "StaleTrace", "TrainingDiverged", "UnbakedModel",
     "init_model", "Model", "encode_forward", "encode_backward", "TrainConfig", "TrainState", "fit",
     "to_inference", "decode_pixels", "decode_at", "decode_rect", "decode_image", "InferenceModel",
+    "ModelFileError", "BadMagic", "VersionMismatch", "TruncatedFile", "InvariantViolation",
+    "serialize", "deserialize", "read_header", "size_report", "SizeReport", "pack_indices",
+    "unpack_indices", "HEADER_BYTES", "load", "save",
 ]
 
 
@@ -38,4 +42,8 @@ def __getattr__(name):
                 "InferenceModel", "TouchCounter", "HostDecoder"):
         from . import decode
         return getattr(decode, name)
+    if name in ("serialize", "deserialize", "read_header", "size_report", "SizeReport", "pack_indices",
+                "unpack_indices", "HEADER_BYTES", "parse", "load", "save"):
+        from . import model_io
+        return getattr(model_io, name)
     raise AttributeError(name)

@@ -1,0 +1,85 @@
+"""The .cngp format on the GPU: device load of files written by the REAL
+reference, device unpack/pack of the index blocks, decode bit-exact vs the
+reference's decode_pixels of the same file, byte-identical round trips
+(test_model_io.py TestSerializeRoundTrip, FORMAT.md)."""
+
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLD = np.load(os.path.join(os.path.dirname(__file__), "golden", "cngp_files.npz"))
+NAMES = ["np4", "np16", "np8_d3", "np2_sig_f4", "np1"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_reference_file_device_load_and_decode(name):
+    import paper_2312_17241_b200 as pg
+    raw = bytes(GOLD[f"{name}_file"])
+    inf = pg.deserialize(raw)
+    # index blocks expanded on the device == the reference's unpack
+    np.testing.assert_array_equal(inf.baked.cpu().numpy(), GOLD[f"{name}_baked"])
+    got = pg.decode_pixels(inf, GOLD[f"{name}_xs"])          # exact (reference-order) decode
+    want = GOLD[f"{name}_decode"]
+    if inf.fast:
+        np.testing.assert_array_equal(got, want)
+    else:  # generic MLP shapes (F = 4, sigmoid): test_decode_generic_shape_matches_oracle bar
+        np.testing.assert_allclose(got, want, rtol=1e-6, atol=1e-7)
+    # the tensor-core decode of the same file
+    from paper_2312_17241_b200.decode import decode_device
+    fast = decode_device(inf, torch.from_numpy(GOLD[f"{name}_xs"]).cuda(), exact=False).cpu().numpy()
+    np.testing.assert_allclose(fast, want, rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("name", NAMES + ["format_example"])
+def test_serialize_round_trip_byte_identical(name):
+    import paper_2312_17241_b200 as pg
+    raw = bytes(GOLD[f"{name}_file"])
+    assert pg.serialize(pg.deserialize(raw)) == raw
+
+
+@pytest.mark.parametrize("w", list(range(1, 9)))
+def test_device_pack_unpack_matches_host(w):
+    from paper_2312_17241_b200 import _lib
+    from paper_2312_17241_b200 import model_io as mio
+    rng = np.random.default_rng(w)
+    for n_c in (1, 5, 8, 33, 1000, 4097):
+        rows = 3
+        e = rng.integers(0, 1 << w, size=(rows, n_c)).astype(np.uint8)
+        nb = (n_c * w + 7) // 8
+        de = torch.from_numpy(e).cuda()
+        dp = torch.empty((rows, nb), dtype=torch.uint8, device="cuda")
+        _lib.call("pg_pack_indices", _lib.ptr(de), rows, n_c, w, _lib.ptr(dp), _lib.stream_ptr())
+        host = np.stack([np.frombuffer(mio.pack_indices(e[r], 1 << w), np.uint8) for r in range(rows)])
+        np.testing.assert_array_equal(dp.cpu().numpy(), host)
+        du = torch.empty((rows, n_c), dtype=torch.uint8, device="cuda")
+        _lib.call("pg_unpack_indices", _lib.ptr(dp), rows, n_c, w, _lib.ptr(du), _lib.stream_ptr())
+        np.testing.assert_array_equal(du.cpu().numpy(), e)
+
+
+def test_trained_model_file_round_trip(tmp_path):
+    """A model trained on the GPU serializes into a valid reference-format file
+    whose decode equals the in-memory model's (test_model_io.py:107-112)."""
+    import paper_2312_17241_b200 as pg
+    from paper_2312_17241_b200 import model_io as mio
+    hyper = pg.HyperParams(n_f=64, n_c=256, n_p=4, n_levels=4, n_min=4, n_max=16, n_neurons=16)
+    img = np.random.default_rng(1).random((16, 16, 3)).astype(np.float32)
+    res = pg.fit(img, hyper, pg.TrainConfig(steps=15, batch_size=128, seed=1))
+    path = str(tmp_path / "m.cngp")
+    n = pg.save(res.inference, path)
+    assert n == mio.size_report(hyper).total_bytes
+    clone = pg.load(path)
+    xs = np.random.default_rng(2).random((64, 2)).astype(np.float32)
+    np.testing.assert_array_equal(pg.decode_pixels(res.inference, xs), pg.decode_pixels(clone, xs))
+    # serialize(Model) downcasts first, as the reference does (no image size)
+    raw = pg.serialize(res.model)
+    assert raw[:44] == open(path, "rb").read()[:44] and raw[52:] == open(path, "rb").read()[52:]
