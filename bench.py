@@ -339,7 +339,7 @@ def run_gpu(args, rank, world, local_rank):
     e2e_launches = args.steps * math.ceil(B_INFER / hd.chunk)
 
     # ---------------- training (C1, data parallel) ----------------
-    train = run_train(args, pg, torch, dist, rank, world, dev, barrier, max_over_ranks)
+    train = run_train(args, pg, torch, dist, rank, world, dev, barrier, max_over_ranks, l2_stream)
     extra = {}
     if not args.quick:
         extra["train_c3"] = run_train_field(args, pg, torch, dist, rank, world, barrier, max_over_ranks, "c3")
@@ -387,7 +387,7 @@ def run_gpu(args, rank, world, local_rank):
     return line, e2e_launches
 
 
-def run_train(args, pg, torch, dist, rank, world, dev, barrier, max_over_ranks):
+def run_train(args, pg, torch, dist, rank, world, dev, barrier, max_over_ranks, l2_stream=None):
     from tests.golden_util import smooth_image
     hyper = pg.HyperParams(**C1)
     model = pg.init_model(hyper, seed=0)
@@ -421,6 +421,9 @@ def run_train(args, pg, torch, dist, rank, world, dev, barrier, max_over_ranks):
                        "sampler": "device", "parallelism": f"dp{world}"},
             "encode_bytes_per_sample": bps,
             "encode_algorithmic_gbs": B_TRAIN * bps / (ms * 1e-3) / 1e9,
+            "encode_frac_of_l2_stream": (B_TRAIN * bps / (ms * 1e-3) / 1e9 / l2_stream) if l2_stream else None,
+            "kernel": "train_mma_kernel (3xTF32 mma.sync MLP; exact_mlp=True selects the OpenBLAS-order FFMA kernel)",
+            "traffic": ncu_traffic("train_mma_kernel", B_TRAIN),
             "last_loss": loss, "scaling": "weak"}
 
 
