@@ -37,7 +37,8 @@ struct Smem {
     float w1[kH * kS];    // W1 [in i][out j]
     float w2[kH * 8];     // W2 [in k][out j], columns >= od zero
     float b0[kH], b1[kH], b2[8];
-    float y[kI * kS];     // y^T [f][q], later dL/dy^T
+    float y[kI * kS];     // y^T [f][q] of the current tile, then of the next
+    float dy[kI * kS];    // dL/dy^T [f][q]
     float h1[kH * kS];    // relu(z1)^T [i][q], later delta1^T
     float h2[kH * kS];    // relu(z2)^T [k][q], later delta2^T
     float d3[kT * 8];     // dL/d(out) [q][j], columns >= od zero
@@ -166,24 +167,19 @@ __global__ void __launch_bounds__(tm::kNT, 2)
         ft = (q < n && j < od) ? __ldg(targets + (q0 + q) * od + j) : 0.0f;
     };
     float pf_x, pf_t;
-    fetch(blockIdx.x, pf_x, pf_t);
     const int pl = tid & (kT - 1), lsub = tid >> 6;
     const int mt = warp & 3;           // 16-sample m-tile of the sample-major GEMMs
     const int rr = tid >> 2, qq = tid & 3;  // bias row-sum role
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t p0 = tile * kT;
-        const int nv = (int)((B - p0) < kT ? (B - p0) : kT);
-        __syncthreads();
-        PG_PH(11);
-        if (tid < kT * D) S.xs[tid] = pf_x;
-        S.tg[tid] = pf_t;
-        fetch(tile + gridDim.x, pf_x, pf_t);
-        __syncthreads();
-        PG_PH(0);
-        // ---- encode forward -> y^T ----
-        float x[D];
+    // prologue: the first tile's inputs and encode forward
+    float x[D];
+    fetch(blockIdx.x, pf_x, pf_t);
+    if (tid < kT * D) S.xs[tid] = pf_x;
+    S.tg[tid] = pf_t;
+    fetch(blockIdx.x + gridDim.x, pf_x, pf_t);
+    __syncthreads();
 #pragma unroll
-        for (int a = 0; a < D; ++a) x[a] = S.xs[pl * D + a];
+    for (int a = 0; a < D; ++a) x[a] = S.xs[pl * D + a];
+    if (blockIdx.x < ntiles) {
 #pragma unroll 2
         for (int it = 0; it < 4; ++it) {
             const int l = lsub + 4 * it;
@@ -191,6 +187,10 @@ __global__ void __launch_bounds__(tm::kNT, 2)
             S.y[(2 * l) * kS + pl] = yv.x;
             S.y[(2 * l + 1) * kS + pl] = yv.y;
         }
+    }
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t p0 = tile * kT;
+        const int nv = (int)((B - p0) < kT ? (B - p0) : kT);
         __syncthreads();
         PG_PH(1);
         // ---- layer 1: h1 = relu(y W0 + b0) ----
@@ -288,27 +288,46 @@ __global__ void __launch_bounds__(tm::kNT, 2)
             float yacc[2][4] = {};
             warp_gemm<2, kT>(gW0, S.y, kS, 1, 16 * (warp & 1), S.h1, 1, kS, 16 * (warp >> 1));
             warp_gemm<2, kH>(yacc, S.h1, 1, kS, 16 * mt, S.w0, 1, kS, 16 * (warp >> 2));
-            __syncthreads();
             PG_PH(9);
-            store_frags_T<2>(S.y, yacc, 16 * mt, 16 * (warp >> 2), [](float v, int, int) { return v; });
+            store_frags_T<2>(S.dy, yacc, 16 * mt, 16 * (warp >> 2), [](float v, int, int) { return v; });
         }
-        __syncthreads();
+        __syncthreads();   // dy complete; y, xs, tg free for the next tile
         PG_PH(10);
         if (dy_out) {
             for (int i = tid; i < nv * kI; i += kNT) {
                 const int q = i / kI, c = i % kI;
-                dy_out[(p0 + q) * kI + c] = S.y[c * kS + q];
+                dy_out[(p0 + q) * kI + c] = S.dy[c * kS + q];
             }
         }
-        // ---- encode backward ----
-        if (pl < nv) {
+        // ---- stage the next tile's inputs (prefetched into registers) ----
+        const int64_t nxt = tile + gridDim.x;
+        if (tid < kT * D) S.xs[tid] = pf_x;
+        S.tg[tid] = pf_t;
+        fetch(nxt + gridDim.x, pf_x, pf_t);
+        __syncthreads();
+        PG_PH(0);
+        float xn[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) xn[a] = S.xs[pl * D + a];
+        // ---- encode backward of this tile fused with encode forward of the
+        //      next: both use the (sample, level) thread mapping, so one loop
+        //      keeps both tiles' L2 round trips in flight together ----
+        const bool has_next = nxt < ntiles;
 #pragma unroll 1
-            for (int it = 0; it < 4; ++it) {
-                const int l = lsub + 4 * it;
-                encode_level_bwd2<D, NPM, ACC>(g, l, x, S.y[(2 * l) * kS + pl], S.y[(2 * l + 1) * kS + pl],
-                                               feats, conf, gfeat, gconf, touched);
+        for (int it = 0; it < 4; ++it) {
+            const int l = lsub + 4 * it;
+            if (has_next) {
+                const float2 yv = encode_level_fwd2<FT, D>(g, l, xn, feats_fwd, baked);
+                S.y[(2 * l) * kS + pl] = yv.x;
+                S.y[(2 * l + 1) * kS + pl] = yv.y;
             }
+            if (pl < nv)
+                encode_level_bwd2<D, NPM, ACC>(g, l, x, S.dy[(2 * l) * kS + pl], S.dy[(2 * l + 1) * kS + pl],
+                                               feats, conf, gfeat, gconf, touched);
         }
+#pragma unroll
+        for (int a = 0; a < D; ++a) x[a] = xn[a];
+        PG_PH(11);
     }
     PG_PH_FLUSH
     // ---- flush ----
