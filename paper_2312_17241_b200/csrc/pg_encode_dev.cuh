@@ -15,10 +15,6 @@ __device__ __forceinline__ void ld_nc_v8(const float *p, float (&v)[8]) {
         : "l"(p));
 }
 
-struct LevelGeo2 {
-    int res, kind, slot;
-};
-
 // Forward: blended F=2 feature of point x at level l (bit-exact vs _core).
 template <typename FT, int D>
 __device__ __forceinline__ float2 encode_level_fwd2(const pg_grid &g, int l, const float (&x)[D],
@@ -63,67 +59,6 @@ __device__ __forceinline__ float2 encode_level_fwd2(const pg_grid &g, int l, con
         y1 = __fadd_rn(y1, __fmul_rn(w[k], f[k].y));
     }
     return make_float2(y0, y1);
-}
-
-// Forward for NL levels of one point at once (same arithmetic as
-// encode_level_fwd2): phase 1 resolves every corner and issues all baked-
-// index loads of the probed levels, phase 2 issues all feature-row loads,
-// phase 3 blends.  The probed levels' dependent L2 round trip (baked byte ->
-// feature row) is paid once per NL levels instead of once per level.
-template <typename FT, int D, int NL>
-__device__ __forceinline__ void encode_levels_fwd2(const pg_grid &g, const int (&lv)[NL],
-                                                   const float (&x)[D], const FT *__restrict__ feats,
-                                                   const uint8_t *__restrict__ baked, float2 (&y)[NL]) {
-    constexpr int C = 1 << D;
-    const uint32_t nf_mask = (uint32_t)g.n_f - 1u, nc_mask = (uint32_t)g.n_c - 1u;
-    int idx[NL][C];
-    float w[NL][C];
-    uint32_t bv[NL][C];
-#pragma unroll
-    for (int i = 0; i < NL; ++i) {
-        const int l = lv[i], res = g.res[l], kind = g.kind[l];
-        int c[D];
-        float t[D], omt[D];
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-            c[a] = cell_coord(x[a], res, t[a]);
-            omt[a] = __fsub_rn(1.0f, t[a]);
-        }
-#pragma unroll
-        for (int k = 0; k < C; ++k) {
-            w[i][k] = corner_weight<float, D>(k, t, omt);
-            bv[i][k] = 0u;
-            if (kind == PG_LEVEL_DENSE) {
-                idx[i][k] = corner_dense<D>(k, c, res + 1);
-            } else {
-                const uint32_t h = corner_hash<D>(k, c, g.primary);
-                if (kind == PG_LEVEL_HASHED) {
-                    idx[i][k] = (int)(h & nf_mask);
-                } else {
-                    idx[i][k] = (int)((h << g.log2_np) & nf_mask);
-                    const int r = (int)(corner_hash<D>(k, c, g.aux) & nc_mask);
-                    bv[i][k] = __ldg(baked + (int64_t)g.slot[l] * g.n_c + r);
-                }
-            }
-        }
-    }
-    float2 f[NL][C];
-#pragma unroll
-    for (int i = 0; i < NL; ++i) {
-        const FT *tab = feats + (int64_t)lv[i] * g.n_f * 2;
-#pragma unroll
-        for (int k = 0; k < C; ++k) f[i][k] = Feat<FT>::ld2(tab + (int64_t)(idx[i][k] + (int)bv[i][k]) * 2);
-    }
-#pragma unroll
-    for (int i = 0; i < NL; ++i) {
-        float y0 = 0.0f, y1 = 0.0f;
-#pragma unroll
-        for (int k = 0; k < C; ++k) {
-            y0 = __fadd_rn(y0, __fmul_rn(w[i][k], f[i][k].x));
-            y1 = __fadd_rn(y1, __fmul_rn(w[i][k], f[i][k].y));
-        }
-        y[i] = make_float2(y0, y1);
-    }
 }
 
 // Backward for one (point, level), F = 2, fp32: scatter w*up into the
