@@ -604,9 +604,21 @@ int pg_decode_host_f32(const pg_grid *grid, const pg_mlp *mlp, const float *h_xs
     PG_REQUIRE(chunk >= 1, "chunk must be positive");
     const int d = grid->d, od = mlp->widths[mlp->n_layers];
     cudaStream_t st[2] = {as_stream(stream0), as_stream(stream1)};
-    int64_t c = 0;
-    for (int64_t off = 0; off < B; off += chunk, ++c) {
-        const int64_t n = (B - off) < chunk ? (B - off) : chunk;
+    // Chunk sizes ramp up from chunk/8 and back down at the end: the first
+    // H2D and the last D2H are the only transfers nothing overlaps, so they
+    // are kept small (~100 us at C2 instead of ~0.8 ms with uniform chunks).
+    int64_t sizes_head[3] = {chunk / 8, chunk / 4, chunk / 2};
+    int64_t c = 0, n = 0;
+    for (int64_t off = 0; off < B; off += n, ++c) {
+        const int64_t rem = B - off;
+        n = chunk;
+        if (c < 3 && sizes_head[c] > 0) n = sizes_head[c];      // ramp up
+        if (rem <= chunk + chunk / 2 && rem > chunk / 8) {      // ramp down: halve the tail
+            n = rem / 2 > chunk / 8 ? (rem + 1) / 2 : rem;
+            if (n > chunk) n = chunk;
+        }
+        if (n > rem) n = rem;
+        if (n < 1) n = rem;
         const int slot = (int)(c & 1);
         cudaStream_t s = st[slot];
         float *dx = d_xs + (int64_t)slot * chunk * d;
