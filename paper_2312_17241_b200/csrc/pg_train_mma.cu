@@ -381,13 +381,13 @@ int train_mma(const pg_grid *g, int od, const float *xs, const float *targets, i
               const uint8_t *baked, const float *conf, const float *params, float scale, int sig, ACC *gfeat,
               ACC *gconf, uint8_t *touched, ACC *gparams, LACC *loss_sum, float *dy_out, cudaStream_t s) {
     const int smem = (int)sizeof(tm::Smem);
-    static bool configured[4] = {false, false, false, false};
+    static bool configured[6] = {false, false, false, false, false, false};
     int sms = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t ntiles = (B + tm::kT - 1) / tm::kT;
     const int grd = (int)(ntiles < 2 * sms ? ntiles : 2 * sms);
-    const bool np4 = g->log2_np <= 2;
+    const int npm = g->log2_np <= 2 ? 4 : g->log2_np == 3 ? 8 : 16;   // probing range held in registers
 #define PG_TRAIN_MMA(D_, NP_, IDX)                                                                    \
     do {                                                                                              \
         auto kern = train_mma_kernel<float, D_, NP_, ACC, LACC>;                                      \
@@ -399,9 +399,9 @@ int train_mma(const pg_grid *g, int od, const float *xs, const float *targets, i
                                         scale, sig, gfeat, gconf, touched, gparams, loss_sum, dy_out); \
     } while (0)
     if (g->d == 2) {
-        if (np4) PG_TRAIN_MMA(2, 4, 0); else PG_TRAIN_MMA(2, 16, 1);
+        if (npm == 4) PG_TRAIN_MMA(2, 4, 0); else if (npm == 8) PG_TRAIN_MMA(2, 8, 4); else PG_TRAIN_MMA(2, 16, 1);
     } else {
-        if (np4) PG_TRAIN_MMA(3, 4, 2); else PG_TRAIN_MMA(3, 16, 3);
+        if (npm == 4) PG_TRAIN_MMA(3, 4, 2); else if (npm == 8) PG_TRAIN_MMA(3, 8, 5); else PG_TRAIN_MMA(3, 16, 3);
     }
 #undef PG_TRAIN_MMA
     return check_launch("train_mma");
