@@ -286,16 +286,23 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
         umma::mbar_wait(&G.mbar[0], phase);
         umma::fence_after_sync();
         // ------- epilogue 1: bias + ReLU -> layer-2 A operand, two K = 32 blocks -------
+        // With NG > 1 (80-register budget) each column half reads its
+        // accumulators right before its block is written, so no registers
+        // are held across the first block's MMAs; NG = 1 reads both up front.
         float v[32];
-        umma::tmem_ld32(tm_d1 + lane_off + ehalf * 32, v);
+        auto load_h1 = [&]() {
+            umma::tmem_ld32(tm_d1 + lane_off + ehalf * 32, v);
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-            const float z = v[c] + S.bias0[ehalf * 32 + c];
-            v[c] = z < 0.0f ? 0.0f : z;
-        }
+            for (int c = 0; c < 32; ++c) {
+                const float z = v[c] + S.bias0[ehalf * 32 + c];
+                v[c] = z < 0.0f ? 0.0f : z;
+            }
+        };
+        if (NG == 1) load_h1();
 #pragma unroll
         for (int blk = 0; blk < 2; ++blk) {
             if (ehalf == blk) {
+                if (NG > 1) load_h1();
 #pragma unroll
                 for (int c = 0; c < 32; c += 4) {
                     float hi[4], lo[4];
