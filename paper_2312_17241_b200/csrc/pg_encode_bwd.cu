@@ -89,16 +89,16 @@ __global__ void __launch_bounds__(256) encode_bwd_kernel(
                             sg[j] = Ar<T>::exp(cr[j] - mx);
                             sum += sg[j];
                         }
-                    const T inv_sum = T(1) / sum;
+                    // reference rounding: z /= sums; dot and s without FMA
                     T s = T(0);
 #pragma unroll
                     for (int j = 0; j < NPMAX; ++j)
                         if (j < n_p) {
-                            sg[j] = sg[j] * inv_sum;
+                            sg[j] = Ar<T>::div(sg[j], sum);
                             T dot = T(0);
-                            for (int q = 0; q < F; ++q) dot += fb[j * F + q] * gq[q];
+                            for (int q = 0; q < F; ++q) dot = Ar<T>::add(dot, Ar<T>::mul(fb[j * F + q], gq[q]));
                             dots[j] = dot;
-                            s += sg[j] * dot;
+                            s = Ar<T>::add(s, Ar<T>::mul(sg[j], dot));
                         }
                     if constexpr (FC == 2 && sizeof(T) == 4) {
                         // N_p*F contiguous floats, 16B aligned when n_p >= 2
@@ -142,18 +142,17 @@ __global__ void __launch_bounds__(256) encode_bwd_kernel(
                     for (int j = 1; j < n_p; ++j) mx = cr[j] > mx ? cr[j] : mx;
                     T sum = T(0);
                     for (int j = 0; j < n_p; ++j) sum += Ar<T>::exp(cr[j] - mx);
-                    const T inv_sum = T(1) / sum;
                     T s = T(0);
                     for (int j = 0; j < n_p; ++j) {
                         T dot = T(0);
-                        for (int q = 0; q < F; ++q) dot += fb[j * F + q] * gq[q];
-                        s += Ar<T>::exp(cr[j] - mx) * inv_sum * dot;
+                        for (int q = 0; q < F; ++q) dot = Ar<T>::add(dot, Ar<T>::mul(fb[j * F + q], gq[q]));
+                        s = Ar<T>::add(s, Ar<T>::mul(Ar<T>::div(Ar<T>::exp(cr[j] - mx), sum), dot));
                     }
                     for (int j = 0; j < n_p; ++j) {
-                        const T sj = Ar<T>::exp(cr[j] - mx) * inv_sum;
+                        const T sj = Ar<T>::div(Ar<T>::exp(cr[j] - mx), sum);
                         T dot = T(0);
                         for (int q = 0; q < F; ++q) {
-                            dot += fb[j * F + q] * gq[q];
+                            dot = Ar<T>::add(dot, Ar<T>::mul(fb[j * F + q], gq[q]));
                             red_add(gb + j * F + q, sj * gq[q]);
                         }
                         red_add(gc + j, sj * (dot - s));

@@ -175,14 +175,15 @@ __device__ __forceinline__ void encode_level_bwd2(const pg_grid &g, int l, const
                     sg[j] = expf(cv[u][j] - mx);
                     sum += sg[j];
                 }
-            const float inv = 1.0f / sum;
+            // the reference's rounding: z /= sums (numpy_backend.py:128-130);
+            // dot = f0*g0 + f1*g1 and s += sj*dot without FMA (_core.pyx:196-201)
             float s = 0.0f;
 #pragma unroll
             for (int j = 0; j < NPMAX; ++j)
                 if (j < n_p) {
-                    sg[j] *= inv;
-                    dots[j] = fv[u][j][0] * g0 + fv[u][j][1] * g1;
-                    s += sg[j] * dots[j];
+                    sg[j] = __fdiv_rn(sg[j], sum);
+                    dots[j] = __fadd_rn(__fmul_rn(fv[u][j][0], g0), __fmul_rn(fv[u][j][1], g1));
+                    s = __fadd_rn(s, __fmul_rn(sg[j], dots[j]));
                 }
             encode_probe_reds<NPMAX, ACC>(gb, gc, n_p, sg, dots, s, g0, g1);
         }
