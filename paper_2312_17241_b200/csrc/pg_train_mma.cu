@@ -20,6 +20,7 @@
 // (PG_EXACT_MLP / reference-order mode); tests bound this one at 1e-5.
 #include "pg_encode_dev.cuh"
 #include "pg_phase.cuh"
+#include "pg_umma.cuh"
 
 namespace pg {
 namespace tm {
@@ -45,7 +46,24 @@ struct Smem {
     float xs[kT * 3];
     float tg[kT * kO];
     double lred[kNT / 32];
+    uint32_t tmem_base;
 };
+
+// per-thread weight-gradient accumulators live in TMEM between tiles (28
+// columns per warp: dW1 fragment 16, dW0 8, dW2 4), leaving the registers to
+// the encode loops; acc[] is added to the parked values
+template <int N>
+__device__ __forceinline__ void tmem_accumulate(uint32_t taddr, const float *acc) {
+    float v[N];
+    if constexpr (N == 16) umma::tmem_ld16(taddr, v);
+    else if constexpr (N == 8) umma::tmem_ld8(taddr, v);
+    else umma::tmem_ld4(taddr, v);
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] += acc[i];
+    if constexpr (N == 16) umma::tmem_st16(taddr, v);
+    else if constexpr (N == 8) umma::tmem_st8(taddr, v);
+    else umma::tmem_st4(taddr, v);
+}
 
 __device__ __forceinline__ uint32_t to_tf32(float x) {
     uint32_t r;
@@ -149,10 +167,20 @@ __global__ void __launch_bounds__(tm::kNT, 2)
         p += kH * od;
         for (int i = tid; i < 8; i += kNT) S.b2[i] = i < od ? p[i] : 0.0f;
     }
-    // persistent gradient accumulators (fragments of the weight-gradient GEMMs)
-    float gW1[4][4] = {};   // dW1: rows i = 16*(warp&3).., columns j = 32*(warp>>2)..
-    float gW0[2][4] = {};   // dW0: rows f = 16*(warp&1).., columns i = 16*(warp>>1)..
-    float gW2[1][4] = {};   // dW2: rows k = 16*warp (warps 0-3), columns j < 8
+    // weight-gradient fragments (dW1 rows i = 16*(warp&3).., columns j =
+    // 32*(warp>>2)..; dW0 rows f = 16*(warp&1).., columns i = 16*(warp>>1)..;
+    // dW2 rows k = 16*warp (warps 0-3), columns j < 8), parked in TMEM
+    if (warp == 0) umma::tmem_alloc<64>(&S.tmem_base);
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    const uint32_t tm = S.tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 32);
+    {
+        const float z16[16] = {}, z8[8] = {}, z4[4] = {};
+        umma::tmem_st16(tm, z16);
+        umma::tmem_st8(tm + 16, z8);
+        umma::tmem_st4(tm + 24, z4);
+    }
     float gb0 = 0.0f, gb1 = 0.0f, gb2 = 0.0f;   // biases: row tid>>2 (lane%4 == 0); b2: tid < 8
     double lsum = 0.0;
     PG_PH_INIT
@@ -238,7 +266,11 @@ __global__ void __launch_bounds__(tm::kNT, 2)
         __syncthreads();
         PG_PH(4);
         // ---- dW2 += h2^T d3 (warps 0-3), db2; delta2 = (d3 W2^T) * (h2 > 0) ----
-        if (warp < 4) warp_gemm<1, kT>(gW2, S.h2, kS, 1, 16 * warp, S.d3, 8, 1, 0);
+        if (warp < 4) {
+            float t2[1][4] = {};
+            warp_gemm<1, kT>(t2, S.h2, kS, 1, 16 * warp, S.d3, 8, 1, 0);
+            tmem_accumulate<4>(tm + 24, &t2[0][0]);
+        }
         if (tid < 8) {
             float s = 0.0f;
             for (int q = 0; q < kT; ++q) s += S.d3[q * 8 + tid];
@@ -269,7 +301,11 @@ __global__ void __launch_bounds__(tm::kNT, 2)
         }
         // ---- dW1 += h1^T delta2 ; delta1' = delta2 W1^T (kept in registers) ----
         float dacc[4][4] = {};
-        warp_gemm<4, kT>(gW1, S.h1, kS, 1, 16 * (warp & 3), S.h2, 1, kS, 32 * (warp >> 2));
+        {
+            float t1[4][4] = {};
+            warp_gemm<4, kT>(t1, S.h1, kS, 1, 16 * (warp & 3), S.h2, 1, kS, 32 * (warp >> 2));
+            tmem_accumulate<16>(tm, &t1[0][0]);
+        }
         warp_gemm<4, kH>(dacc, S.h2, 1, kS, 16 * mt, S.w1, 1, kS, 32 * (warp >> 2));
         __syncthreads();
         PG_PH(7);
@@ -286,7 +322,11 @@ __global__ void __launch_bounds__(tm::kNT, 2)
         // ---- dW0 += y^T delta1 ; dy = delta1 W0^T ----
         {
             float yacc[2][4] = {};
-            warp_gemm<2, kT>(gW0, S.y, kS, 1, 16 * (warp & 1), S.h1, 1, kS, 16 * (warp >> 1));
+            {
+                float t0[2][4] = {};
+                warp_gemm<2, kT>(t0, S.y, kS, 1, 16 * (warp & 1), S.h1, 1, kS, 16 * (warp >> 1));
+                tmem_accumulate<8>(tm + 16, &t0[0][0]);
+            }
             warp_gemm<2, kH>(yacc, S.h1, 1, kS, 16 * mt, S.w0, 1, kS, 16 * (warp >> 2));
             PG_PH(9);
             store_frags_T<2>(S.dy, yacc, 16 * mt, 16 * (warp >> 2), [](float v, int, int) { return v; });
@@ -334,6 +374,10 @@ __global__ void __launch_bounds__(tm::kNT, 2)
     ACC *gW0p = gparams, *gb0p = gW0p + kI * kH, *gW1p = gb0p + kH, *gb1p = gW1p + kH * kH;
     ACC *gW2p = gb1p + kH, *gb2p = gW2p + kH * od;
     {
+        float gW1[4][4], gW0[2][4], gW2[1][4];
+        umma::tmem_ld16(tm, *reinterpret_cast<float(*)[16]>(&gW1[0][0]));
+        umma::tmem_ld8(tm + 16, *reinterpret_cast<float(*)[8]>(&gW0[0][0]));
+        umma::tmem_ld4(tm + 24, *reinterpret_cast<float(*)[4]>(&gW2[0][0]));
         const int gq = lane >> 2, c = lane & 3;
 #pragma unroll
         for (int t = 0; t < 4; ++t)
@@ -372,6 +416,9 @@ __global__ void __launch_bounds__(tm::kNT, 2)
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (tid == 0 && loss_sum) loss_add(loss_sum, v);
     }
+    umma::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) umma::tmem_free<64>(S.tmem_base);
 }
 
 PG_PH_READER(pg_phase_prof_read_mma)

@@ -118,6 +118,43 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 lanes x N consecutive 32-bit columns <-> N registers per thread
+// (N = 4, 8, 16), for parking per-thread state in TMEM between tiles
+#define PG_TMEM_LDST(N, REGS_OUT, REGS_IN, LIST_LD, LIST_ST)                                           \
+    __device__ __forceinline__ void tmem_ld##N(uint32_t taddr, float (&v)[N]) {                        \
+        uint32_t r[N];                                                                                 \
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x" #N ".b32 " LIST_LD ", [%" #N "];"              \
+                     : REGS_OUT                                                                        \
+                     : "r"(taddr));                                                                    \
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");                                    \
+        for (int i = 0; i < N; ++i) v[i] = __uint_as_float(r[i]);                                      \
+    }                                                                                                  \
+    __device__ __forceinline__ void tmem_st##N(uint32_t taddr, const float (&v)[N]) {                  \
+        uint32_t r[N];                                                                                 \
+        for (int i = 0; i < N; ++i) r[i] = __float_as_uint(v[i]);                                      \
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x" #N ".b32 [%0], " LIST_ST ";"                   \
+                     ::"r"(taddr), REGS_IN                                                             \
+                     : "memory");                                                                      \
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");                                    \
+    }
+#define PG_O4 "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+#define PG_I4 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3])
+#define PG_O8 PG_O4, "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+#define PG_I8 PG_I4, "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+#define PG_O16 PG_O8, "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+#define PG_I16 PG_I8, "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+PG_TMEM_LDST(4, PG_O4, PG_I4, "{%0,%1,%2,%3}", "{%1,%2,%3,%4}")
+PG_TMEM_LDST(8, PG_O8, PG_I8, "{%0,%1,%2,%3,%4,%5,%6,%7}", "{%1,%2,%3,%4,%5,%6,%7,%8}")
+PG_TMEM_LDST(16, PG_O16, PG_I16, "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}",
+             "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16}")
+#undef PG_O4
+#undef PG_I4
+#undef PG_O8
+#undef PG_I8
+#undef PG_O16
+#undef PG_I16
+#undef PG_TMEM_LDST
+
 // fp32 -> (hi, lo) with hi exactly representable in tf32 (round to nearest
 // on the 10-bit mantissa) and lo = x - hi (exact), itself rounded to tf32 by
 // the MMA: hi*w + lo*w carries ~22 significand bits of x.
