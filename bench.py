@@ -361,7 +361,7 @@ def run_gpu(args, rank, world, local_rank):
                    "l2_policy": "inputs (128 MiB coords + 192 MiB outputs per GPU) larger than L2; tables L2-resident"},
         "e2e": {"value": e2e_qps, "unit": "queries/s", "h2d_bytes_per_step": B_INFER * 2 * 4,
                 "d2h_bytes_per_step": B_INFER * hyper.out_dim * 4,
-                "path": "pg_decode_host_f32 (pinned host in/out, 2 streams, 2^21-query chunks)"},
+                "path": "pg_decode_host_f32 (pinned host in/out; H2D, kernel, D2H on 3 event-ordered streams; 2^21-query chunks, ramped)"},
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak,

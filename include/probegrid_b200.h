@@ -209,16 +209,17 @@ int pg_decode_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
                   const float *params, unsigned flags, float *ws, float *out,
                   void *stream);
 
-/* End-to-end decode from HOST memory (pinned for overlap): chunks of
- * `chunk` queries alternate between two streams, H2D copy -> fused decode ->
- * D2H copy, so transfers overlap compute.  d_xs must hold 2*chunk*d floats,
- * d_out 2*chunk*out_dim floats.  Returns after both streams drain. */
+/* End-to-end decode from HOST memory (pinned for overlap): chunks of up to
+ * `chunk` queries, H2D copies on stream_in, fused decodes on stream_compute,
+ * D2H copies on stream_out, two buffer slots ordered by events so both copy
+ * directions overlap the kernels.  d_xs must hold 2*chunk*d floats, d_out
+ * 2*chunk*out_dim floats.  Returns after all three streams drain. */
 int pg_decode_host_f32(const pg_grid *grid, const pg_mlp *mlp,
                        const float *h_xs, int64_t B, const void *feats,
                        const uint8_t *baked, const float *params,
                        unsigned flags, int64_t chunk, float *d_xs,
-                       float *d_out, float *h_out, void *stream0,
-                       void *stream1);
+                       float *d_out, float *h_out, void *stream_in,
+                       void *stream_compute, void *stream_out);
 
 /* Training MLP pass (trainer.py:122-137 + mlp.py:55-85): forward, squared
  * error loss (sum in fp64 into *loss_sum), dpred = diff*scale, backward.

@@ -75,7 +75,7 @@ for _t, _s in (("f32", _F), ("f64", _D)):
 _SIGS.update({
     "pg_dedup_rows": [_P, _I64, _I64, _P, _P, _P, _P, _P],
     "pg_decode_f32": [_G, _M, _P, _I64, _P, _P, _P, ctypes.c_uint, _P, _P, _P],
-    "pg_decode_host_f32": [_G, _M, _P, _I64, _P, _P, _P, ctypes.c_uint, _I64, _P, _P, _P, _P, _P],
+    "pg_decode_host_f32": [_G, _M, _P, _I64, _P, _P, _P, ctypes.c_uint, _I64, _P, _P, _P, _P, _P, _P],
     "pg_touched_to_f32": [_P, _I64, _P, _P],
     "pg_touched_from_f32": [_P, _I64, _P, _P],
     "pg_train_fused_f32": [_G, _M, _P, _P, _I64, _P, _P, _P, _P, _F, ctypes.c_uint, _P, _P, _P,

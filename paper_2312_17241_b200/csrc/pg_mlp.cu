@@ -597,39 +597,62 @@ int pg_decode_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs, int64
 int pg_decode_host_f32(const pg_grid *grid, const pg_mlp *mlp, const float *h_xs, int64_t B,
                        const void *feats, const uint8_t *baked, const float *params,
                        unsigned flags, int64_t chunk, float *d_xs, float *d_out, float *h_out,
-                       void *stream0, void *stream1) {
+                       void *stream_in, void *stream_compute, void *stream_out) {
     if (int e = validate_grid(grid)) return e;
     if (int e = validate_mlp(mlp)) return e;
     PG_REQUIRE(decode_fast_ok(grid, mlp), "host decode needs the fused [32,64,64,<=4] shape");
     PG_REQUIRE(chunk >= 1, "chunk must be positive");
     const int d = grid->d, od = mlp->widths[mlp->n_layers];
-    cudaStream_t st[2] = {as_stream(stream0), as_stream(stream1)};
-    // Chunk sizes ramp up from chunk/8 and back down at the end: the first
-    // H2D and the last D2H are the only transfers nothing overlaps, so they
-    // are kept small (~100 us at C2 instead of ~0.8 ms with uniform chunks).
-    int64_t sizes_head[3] = {chunk / 8, chunk / 4, chunk / 2};
+    cudaStream_t si = as_stream(stream_in), sk = as_stream(stream_compute), so = as_stream(stream_out);
+    // Three streams, two buffer slots: H2D on si, kernels on sk, D2H on so,
+    // ordered by events — copy-in of chunk c+2 needs only kernel c done (its
+    // input slot), kernel c+2 needs only copy-out c done (its output slot), so
+    // both copy directions run under the kernels.
+    cudaEvent_t ev_in[2], ev_k[2], ev_out[2];
+    for (int i = 0; i < 2; ++i) {
+        cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ev_k[i], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming);
+    }
+    // chunk sizes ramp up from chunk/8 and back down at the end: the first
+    // H2D and the last D2H are the only transfers nothing overlaps
+    const int64_t head[3] = {chunk / 8, chunk / 4, chunk / 2};
     int64_t c = 0, n = 0;
+    int err = PG_OK;
     for (int64_t off = 0; off < B; off += n, ++c) {
         const int64_t rem = B - off;
         n = chunk;
-        if (c < 3 && sizes_head[c] > 0) n = sizes_head[c];      // ramp up
-        if (rem <= chunk + chunk / 2 && rem > chunk / 8) {      // ramp down: halve the tail
+        if (c < 3 && head[c] > 0) n = head[c];
+        if (rem <= chunk + chunk / 2 && rem > chunk / 8) {
             n = rem / 2 > chunk / 8 ? (rem + 1) / 2 : rem;
             if (n > chunk) n = chunk;
         }
         if (n > rem) n = rem;
         if (n < 1) n = rem;
         const int slot = (int)(c & 1);
-        cudaStream_t s = st[slot];
         float *dx = d_xs + (int64_t)slot * chunk * d;
         float *dout = d_out + (int64_t)slot * chunk * od;
-        cudaMemcpyAsync(dx, h_xs + off * d, sizeof(float) * n * d, cudaMemcpyHostToDevice, s);
-        if (int e = decode_device(grid, mlp, dx, n, feats, baked, params, flags, nullptr, dout, nullptr, s))
-            return e;
-        cudaMemcpyAsync(h_out + off * od, dout, sizeof(float) * n * od, cudaMemcpyDeviceToHost, s);
+        if (c >= 2) cudaStreamWaitEvent(si, ev_k[slot], 0);     // kernel c-2 has read this input slot
+        cudaMemcpyAsync(dx, h_xs + off * d, sizeof(float) * n * d, cudaMemcpyHostToDevice, si);
+        cudaEventRecord(ev_in[slot], si);
+        cudaStreamWaitEvent(sk, ev_in[slot], 0);
+        if (c >= 2) cudaStreamWaitEvent(sk, ev_out[slot], 0);   // copy-out c-2 has drained this output slot
+        if ((err = decode_device(grid, mlp, dx, n, feats, baked, params, flags, nullptr, dout, nullptr, sk)))
+            break;
+        cudaEventRecord(ev_k[slot], sk);
+        cudaStreamWaitEvent(so, ev_k[slot], 0);
+        cudaMemcpyAsync(h_out + off * od, dout, sizeof(float) * n * od, cudaMemcpyDeviceToHost, so);
+        cudaEventRecord(ev_out[slot], so);
     }
-    cudaStreamSynchronize(st[0]);
-    cudaStreamSynchronize(st[1]);
+    cudaStreamSynchronize(si);
+    cudaStreamSynchronize(sk);
+    cudaStreamSynchronize(so);
+    for (int i = 0; i < 2; ++i) {
+        cudaEventDestroy(ev_in[i]);
+        cudaEventDestroy(ev_k[i]);
+        cudaEventDestroy(ev_out[i]);
+    }
+    if (err) return err;
     return check_launch("decode_host");
 }
 

@@ -181,8 +181,9 @@ def decode_image(inf: InferenceModel, width: int | None = None,
 
 class HostDecoder:
     """End-to-end decode from pinned host memory through the C ABI's
-    pg_decode_host_f32: H2D copy, fused kernel and D2H copy of successive
-    chunks alternate between two streams so transfers overlap compute."""
+    pg_decode_host_f32: H2D copies, fused kernels and D2H copies of
+    successive chunks on three streams (two buffer slots, event-ordered) so
+    both transfer directions overlap compute."""
 
     def __init__(self, inf: InferenceModel, chunk: int = 1 << 21, exact: bool = False):
         if not inf.fast:
@@ -191,8 +192,9 @@ class HostDecoder:
         d, od = inf.hyper.d, inf.out_dim
         self.d_xs = torch.empty(2 * chunk * d, dtype=torch.float32, device=inf.device)
         self.d_out = torch.empty(2 * chunk * od, dtype=torch.float32, device=inf.device)
-        self.s0 = torch.cuda.Stream(device=inf.device)
-        self.s1 = torch.cuda.Stream(device=inf.device)
+        self.s_in = torch.cuda.Stream(device=inf.device)
+        self.s_k = torch.cuda.Stream(device=inf.device)
+        self.s_out = torch.cuda.Stream(device=inf.device)
 
     def __call__(self, h_xs: torch.Tensor, h_out: torch.Tensor) -> torch.Tensor:
         inf = self.inf
@@ -200,6 +202,6 @@ class HostDecoder:
         _lib.call("pg_decode_host_f32", inf.grid, inf.mlp_desc, _lib.ptr(h_xs), h_xs.shape[0],
                   _lib.ptr(inf.feats16), _lib.ptr(inf.baked), _lib.ptr(inf.params),
                   _flags(inf, self.exact), self.chunk, _lib.ptr(self.d_xs), _lib.ptr(self.d_out),
-                  _lib.ptr(h_out), _lib.ctypes.c_void_p(self.s0.cuda_stream),
-                  _lib.ctypes.c_void_p(self.s1.cuda_stream))
+                  _lib.ptr(h_out), _lib.ctypes.c_void_p(self.s_in.cuda_stream),
+                  _lib.ctypes.c_void_p(self.s_k.cuda_stream), _lib.ctypes.c_void_p(self.s_out.cuda_stream))
         return h_out
