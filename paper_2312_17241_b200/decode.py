@@ -135,6 +135,10 @@ def decode_pixels(inf: InferenceModel, xs, counter: TouchCounter | None = None,
         t = torch.from_numpy(a).to(inf.device)
     else:
         t = xs.to(device=inf.device, dtype=torch.float32).contiguous()
+        if t.ndim != 2 or t.shape[1] != d:
+            raise DomainViolation(f"expected (batch, {d}) coordinates, got {tuple(t.shape)}")
+        if t.numel() and bool(((t < 0.0) | (t > 1.0)).any()):   # encoding.py:37-38 (NaN passes, as there)
+            raise DomainViolation("coordinates outside the unit hypercube")
     if counter is not None:
         per = t.shape[0] * (1 << d)
         counter.feature_rows += per * inf.hyper.n_levels

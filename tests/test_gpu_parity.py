@@ -236,6 +236,11 @@ def test_domain_violation():
         pg.encode_forward(m, np.array([[1.2, 0.5]], np.float32))
     with pytest.raises(pg.DomainViolation):
         pg.encode_forward(m, torch.tensor([[0.5, -0.01]], device="cuda"))
+    inf = pg.to_inference(m)
+    for bad in (np.array([[0.5, 1.01]], np.float32), torch.tensor([[0.5, -0.01]], device="cuda"),
+                torch.zeros((3, 3), device="cuda")):
+        with pytest.raises(pg.DomainViolation):
+            pg.decode_pixels(inf, bad)
 
 
 # ------------------------------------------------------------- training
