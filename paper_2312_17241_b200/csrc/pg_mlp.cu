@@ -120,33 +120,81 @@ __device__ __forceinline__ float mac(float acc, float a, float w) {
     return EXACT ? __fadd_rn(acc, __fmul_rn(a, w)) : __fmaf_rn(a, w, acc);
 }
 
+// Paired fp32 FMA (sm_100 FFMA2: two fp32 lanes per instruction) for the
+// non-exact MLP.  The exact (reference-order) MLP stays on scalar
+// __fmul_rn/__fadd_rn: ptxas (12.9) contracts mul.rn.f32x2 + add.rn.f32x2
+// into FFMA2 even with --fmad=false, which would change the rounding.
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float &a, float &b) {
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t acc, uint64_t a, uint64_t w) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(w), "l"(acc));
+    return r;
+}
+
 // 128 x 64 layer: out^T = act(in^T)^T W + b, K = fan_in.
 template <int K, bool EXACT>
 __device__ __forceinline__ void layer_tile(const float *__restrict__ in_t, const float *__restrict__ W,
                                            const float *__restrict__ bias, float *__restrict__ out_t) {
     const int og = threadIdx.x & 15, pg = threadIdx.x >> 4;
     float acc[8][4];
+    if (EXACT) {
+        const float4 bb = *reinterpret_cast<const float4 *>(bias + og * 4);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            acc[i][0] = bb.x;
+            acc[i][1] = bb.y;
+            acc[i][2] = bb.z;
+            acc[i][3] = bb.w;
+        }
+#pragma unroll 8
+        for (int k = 0; k < K; ++k) {
+            const float4 a0 = *reinterpret_cast<const float4 *>(in_t + swz(k, pg * 8));
+            const float4 a1 = *reinterpret_cast<const float4 *>(in_t + swz(k, pg * 8 + 4));
+            const float4 w = *reinterpret_cast<const float4 *>(W + k * kHid + og * 4);
+            const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                acc[i][0] = mac<true>(acc[i][0], a[i], w.x);
+                acc[i][1] = mac<true>(acc[i][1], a[i], w.y);
+                acc[i][2] = mac<true>(acc[i][2], a[i], w.z);
+                acc[i][3] = mac<true>(acc[i][3], a[i], w.w);
+            }
+        }
+    } else {
+    // accumulators as output pairs (j0, j1), (j2, j3): paired fp32 FMA
+    uint64_t acc2[8][2];
     const float4 bb = *reinterpret_cast<const float4 *>(bias + og * 4);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        acc[i][0] = bb.x;
-        acc[i][1] = bb.y;
-        acc[i][2] = bb.z;
-        acc[i][3] = bb.w;
+        acc2[i][0] = f2pack(bb.x, bb.y);
+        acc2[i][1] = f2pack(bb.z, bb.w);
     }
 #pragma unroll 8
     for (int k = 0; k < K; ++k) {
         const float4 a0 = *reinterpret_cast<const float4 *>(in_t + swz(k, pg * 8));
         const float4 a1 = *reinterpret_cast<const float4 *>(in_t + swz(k, pg * 8 + 4));
         const float4 w = *reinterpret_cast<const float4 *>(W + k * kHid + og * 4);
+        const uint64_t w01 = f2pack(w.x, w.y), w23 = f2pack(w.z, w.w);
         const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            acc[i][0] = mac<EXACT>(acc[i][0], a[i], w.x);
-            acc[i][1] = mac<EXACT>(acc[i][1], a[i], w.y);
-            acc[i][2] = mac<EXACT>(acc[i][2], a[i], w.z);
-            acc[i][3] = mac<EXACT>(acc[i][3], a[i], w.w);
+            const uint64_t aa = f2pack(a[i], a[i]);
+            acc2[i][0] = ffma2(acc2[i][0], aa, w01);
+            acc2[i][1] = ffma2(acc2[i][1], aa, w23);
         }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        f2unpack(acc2[i][0], acc[i][0], acc[i][1]);
+        f2unpack(acc2[i][1], acc[i][2], acc[i][3]);
+    }
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
