@@ -309,6 +309,26 @@ def run_gpu(args, rank, world, local_rank):
     l2_stream, l2_gather = measure_l2(None, torch, table_mib=32)
     mlp_flops = 2 * sum(a * b for a, b in zip(inf.widths[:-1], inf.widths[1:]))
 
+    # ---------------- raster-order queries (gigapixel-style image decode) ----------------
+    # the same 2^24 queries as pixel centres of an 8192 x 2048 slab of an
+    # 8192^2 image in raster order: neighbouring lanes share cells on the
+    # coarse levels, the access pattern decode_image / decode_rect produce
+    W_img, H_slab = 8192, B_INFER // 8192
+    yy, xx = torch.meshgrid(torch.arange(H_slab, device=dev), torch.arange(W_img, device=dev),
+                            indexing="ij")
+    xs_r = torch.stack([(xx.reshape(-1).float() + 0.5) / W_img,
+                        (yy.reshape(-1).float() + 0.5) / W_img], dim=1).contiguous()
+    del xx, yy
+    for _ in range(2):
+        decode_device(inf, xs_r, out, exact=exact)
+    e0.record()
+    for _ in range(max(3, args.steps // 4)):
+        decode_device(inf, xs_r, out, exact=exact)
+    e1.record()
+    torch.cuda.synchronize()
+    raster_qps = world * B_INFER * max(3, args.steps // 4) / (e0.elapsed_time(e1) * 1e-3)
+    del xs_r
+
     # ---------------- ablation: same decode, other MLP engines ----------------
     ablation = {}
     for name, kw in (("tcgen05_without_smem_baked_tables", dict(exact=False, smem_tables=False)),
@@ -381,6 +401,7 @@ def run_gpu(args, rank, world, local_rank):
                              "served from shared memory"},
         "clocks": clk,
         "ablation_queries_per_s": ablation,
+        "raster_order_queries_per_s": raster_qps,
         "train": train,
         **extra,
     }
