@@ -345,6 +345,38 @@ def test_step_gradients_vs_oracle(mode):
         close_grad(gc[i], om.levels[lv].cgrad, 1e-10, tc)
 
 
+@pytest.mark.parametrize("B", [1000, 64 * 3 + 1, 37])
+def test_step_gradients_ragged_batch(B):
+    """Batches that are not a multiple of the 64-sample tile (last tile
+    partly padded): tensor-core step gradients vs the oracle."""
+    import paper_2312_17241_b200 as pg
+    img = _smooth()
+    m, om = _models(C1, perturb=False)
+    st = pg.TrainState(m, img, pg.TrainConfig(batch_size=B, seed=3))
+    xs, targets = st.sample_batch()
+    st.loss_sum.zero_()
+    st.compute_grads(xs, targets)
+    ost = O.TrainState(om, img, O.TrainCfg(batch_size=B, seed=3))
+    oxs, otg = ost.sample_batch()
+    eq(xs.cpu().numpy(), oxs)
+    y, traces = O.encode_forward(om, oxs)
+    out, cache = O.mlp_forward(om.W, om.b, y)
+    diff = out - otg
+    oloss = float(np.mean(diff.astype(np.float64) ** 2))
+    ody = O.mlp_backward(om.W, om.Wg, om.bg, cache, diff * np.float32(2.0 / diff.size))
+    O.encode_backward(om, traces, ody)
+    assert abs(float(st.loss_sum.item()) / (B * 3) - oloss) <= 1e-6 * oloss
+    for i in range(3):
+        close_grad(m.mlp.weight_grads[i].cpu().numpy(), om.Wg[i], 1e-9, True)
+        close_grad(m.mlp.bias_grads[i].cpu().numpy(), om.bg[i], 1e-9, True)
+    gf = m.gfeats.cpu().numpy()
+    for L in om.levels:
+        close_grad(gf[L.level], L.fgrad, 1e-10, True)
+    gc = m.gconf.cpu().numpy()
+    for i, lv in enumerate(m.probed):
+        close_grad(gc[i], om.levels[lv].cgrad, 1e-10, True)
+
+
 @pytest.mark.parametrize("od", [3, 2, 4])
 def test_reference_order_mlp_grads_bit_exact(od):
     """reference_order=True: every MLP weight and bias gradient of a batch is
