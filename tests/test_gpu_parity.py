@@ -732,3 +732,49 @@ def test_field_trainer_3d_gradients_vs_oracle(n_p, out_dim, exact):
         close_grad(gc[i], om.levels[lv].cgrad, 1e-10, not exact)
     for i in range(3):
         close_grad(m.mlp.weight_grads[i].cpu().numpy(), om.Wg[i], 1e-9, not exact)
+
+
+# ------------------------------------------------------------- edge cases
+def test_empty_inputs():
+    """Zero-length batches flow through every entry point (the reference's
+    numpy code returns empty arrays)."""
+    import paper_2312_17241_b200 as pg
+    from paper_2312_17241_b200 import backend as cuda
+    from paper_2312_17241_b200.decode import decode_device
+    m = pg.init_model(pg.HyperParams(**C1), seed=0)
+    inf = pg.to_inference(m)
+    z = np.zeros((0, 2), np.float32)
+    assert pg.decode_pixels(inf, z).shape == (0, 3)
+    assert decode_device(inf, torch.zeros((0, 2), device="cuda"), exact=False).shape == (0, 3)
+    y, _ = pg.encode_forward(m, z)
+    assert y.shape == (0, 32)
+    feats = np.zeros((64, 2), np.float32)
+    o, idx, w = cuda.dense_fwd(z, 7, feats)
+    assert o.shape == (0, 2) and idx.shape == (0, 4) and w.shape == (0, 4)
+    o, base, row, w = cuda.probed_fwd(z, 21, 64, 32, 2, feats, np.zeros(32, np.uint8), O.PRIMARY, O.AUX)
+    assert o.shape == (0, 2) and base.shape == (0, 4)
+    rows_u, inv = cuda.dedup_rows(np.zeros((0, 4), np.int32), 32)
+    assert rows_u.shape == (0,) and inv.shape == (0, 4)
+
+
+@pytest.mark.parametrize("n_p", [32, 256])
+def test_long_probing_ranges_vs_oracle(n_p):
+    """N_p beyond the fused kernels' register ranges (up to the 8-bit baked
+    storage limit, model.py:61-62): the generic encode kernels, fwd bit-exact,
+    bwd within 1e-5."""
+    import paper_2312_17241_b200 as pg
+    kw = dict(n_f=2**10, n_c=2**8, n_p=n_p, n_levels=4, n_min=8, n_max=64, n_neurons=16)
+    m, om = _models(kw)
+    xs = _edge_points(777, 2, np.float32, seed=5, res_list=(8, 64))
+    y, traces = pg.encode_forward(m, xs)
+    yo, otr = O.encode_forward(om, xs)
+    eq(y, yo)
+    up = np.random.default_rng(6).standard_normal(y.shape).astype(np.float32)
+    pg.encode_backward(m, traces, up)
+    O.encode_backward(om, otr, up)
+    gf = m.gfeats.cpu().numpy()
+    for L in om.levels:
+        np.testing.assert_allclose(gf[L.level], L.fgrad, rtol=1e-5, atol=1e-6)
+    gc = m.gconf.cpu().numpy()
+    for i, lv in enumerate(m.probed):
+        np.testing.assert_allclose(gc[i], om.levels[lv].cgrad, rtol=1e-5, atol=1e-6)
