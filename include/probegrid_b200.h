@@ -262,6 +262,12 @@ int pg_unpack_indices(const uint8_t *packed, int64_t n_rows, int64_t n_c,
 int pg_pack_indices(const uint8_t *entries, int64_t n_rows, int64_t n_c,
                     int log2_np, uint8_t *packed, void *stream);
 
+/* Pixel centres of the rectangle [x0, x0+w) x [y0, y0+h) of a width x height
+ * image in raster order, (w*h, 2) floats on the device, bit-identical to
+ * model_io.py:321-325 _grid_coords (decode_rect / decode_image input). */
+int pg_raster_coords_f32(int x0, int y0, int w, int h, int width, int height,
+                         float *xs, void *stream);
+
 /* Reference-order MLP gradients (parity mode).  pg_train_fused_ref_f32 is
  * pg_train_fused_f32 except that it leaves gparams untouched and writes, per
  * sample, every layer's input and output delta to acts, laid out as
@@ -283,6 +289,14 @@ int pg_train_fused_ref_f32(const pg_grid *grid, const pg_mlp *mlp, const float *
                            double *loss_sum, float *acts, void *stream);
 int pg_mlp_wgrad_blas_f32(const pg_mlp *mlp, const float *acts, int64_t B,
                           float *gparams, void *stream);
+/* the same with the table gradients and the loss in 64-bit fixed point
+ * (deterministic mode; flush with pg_fx_accumulate_f32 / pg_fx_loss) */
+int pg_train_fused_ref_det_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
+                               const float *targets, int64_t B, const float *feats,
+                               const uint8_t *baked, const float *conf,
+                               const float *params, float scale, unsigned flags,
+                               uint64_t *gfeat_fx, uint64_t *gconf_fx, uint8_t *touched,
+                               uint64_t *loss_fx, float *acts, void *stream);
 
 /* Deterministic mode.  Same passes as pg_encode_bwd_f32 / pg_mlp_train_f32 /
  * pg_train_fused_f32, but every cross-thread sum (table scatters, weight

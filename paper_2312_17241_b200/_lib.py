@@ -83,7 +83,10 @@ _SIGS.update({
     "pg_train_fused_ref_f32": [_G, _M, _P, _P, _I64, _P, _P, _P, _P, _F, ctypes.c_uint, _P, _P,
                                _P, _P, _P, _P],
     "pg_mlp_wgrad_blas_f32": [_M, _P, _I64, _P, _P],
+    "pg_train_fused_ref_det_f32": [_G, _M, _P, _P, _I64, _P, _P, _P, _P, _F, ctypes.c_uint, _P, _P,
+                                   _P, _P, _P, _P],
     "pg_unpack_indices": [_P, _I64, _I64, _I, _P, _P],
+    "pg_raster_coords_f32": [_I, _I, _I, _I, _I, _I, _P, _P],
     "pg_pack_indices": [_P, _I64, _I64, _I, _P, _P],
     "pg_encode_bwd_det_f32": [_G, _P, _I64, _P, _P, _P, _P, _P, _P, _P],
     "pg_mlp_train_det_f32": [_M, _P, _P, _I64, _P, _F, ctypes.c_uint, _P, _P, _P, _P, _P],

@@ -39,9 +39,34 @@ __global__ void pack_indices_kernel(const uint8_t *__restrict__ entries, int64_t
     packed[i] = (uint8_t)(byte & 0xFFu);
 }
 
+// Pixel centres of a rectangle of a W x H image in raster order
+// (model_io.py:321-325 _grid_coords: float32((c + 0.5) / W) with the division
+// in double, as numpy does), so decode_rect / decode_image need no host-side
+// coordinate arrays.
+__global__ void raster_coords_kernel(int x0, int y0, int w, int64_t n, int W, int H, float *__restrict__ xs) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t r = i / w, c = i - r * w;
+    const double u = ((double)(x0 + c) + 0.5) / (double)W;
+    const double v = ((double)(y0 + r) + 0.5) / (double)H;
+    reinterpret_cast<float2 *>(xs)[i] = make_float2(__double2float_rn(u), __double2float_rn(v));
+}
+
 }  // namespace pg
 
 extern "C" {
+
+int pg_raster_coords_f32(int x0, int y0, int w, int h, int width, int height, float *xs, void *stream) {
+    PG_REQUIRE(width >= 1 && height >= 1, "raster_coords: empty image");
+    PG_REQUIRE(0 <= x0 && x0 + w <= width && 0 <= y0 && y0 + h <= height && w >= 0 && h >= 0,
+               "raster_coords: rectangle outside the image");
+    const int64_t n = (int64_t)w * h;
+    if (n == 0) return PG_OK;
+    pg::raster_coords_kernel<<<(unsigned)((n + 255) / 256), 256, 0, pg::as_stream(stream)>>>(x0, y0, w, n, width,
+                                                                                            height, xs);
+    return pg::check_launch("raster_coords");
+}
+
 
 int pg_unpack_indices(const uint8_t *packed, int64_t n_rows, int64_t n_c, int log2_np, uint8_t *entries,
                       void *stream) {

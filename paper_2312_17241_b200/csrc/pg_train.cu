@@ -506,6 +506,19 @@ extern "C" int pg_train_fused_ref_f32(const pg_grid *grid, const pg_mlp *mlp, co
                                           pg::as_stream(stream));
 }
 
+extern "C" int pg_train_fused_ref_det_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
+                                          const float *targets, int64_t B, const float *feats,
+                                          const uint8_t *baked, const float *conf, const float *params,
+                                          float scale, unsigned flags, uint64_t *gfeat_fx,
+                                          uint64_t *gconf_fx, uint8_t *touched, uint64_t *loss_fx,
+                                          float *acts, void *stream) {
+    using pg::fx_t;
+    PG_REQUIRE(acts != nullptr, "pg_train_fused_ref_det_f32: acts is required");
+    return pg::train_fused<fx_t, fx_t>(grid, mlp, xs, targets, B, feats, baked, conf, params, scale, flags,
+                                       (fx_t *)gfeat_fx, (fx_t *)gconf_fx, touched, nullptr, (fx_t *)loss_fx,
+                                       nullptr, acts, pg::as_stream(stream));
+}
+
 extern "C" int pg_train_fused_det_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
                                       const float *targets, int64_t B, const float *feats,
                                       const uint8_t *baked, const float *conf, const float *params,

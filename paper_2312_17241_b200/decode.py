@@ -160,7 +160,7 @@ def grid_coords(width: int, height: int, x0: int, y0: int, x1: int, y1: int) -> 
 
 
 def decode_rect(inf: InferenceModel, rect, width: int | None = None,
-                height: int | None = None) -> np.ndarray:
+                height: int | None = None, exact: bool = True) -> np.ndarray:
     """Decode the half-open pixel rectangle (x0, y0, x1, y1) (model_io.py:327-339)."""
     width = width or inf.width
     height = height or inf.height
@@ -169,18 +169,22 @@ def decode_rect(inf: InferenceModel, rect, width: int | None = None,
     x0, y0, x1, y1 = (int(v) for v in rect)
     if not (0 <= x0 < x1 <= width and 0 <= y0 < y1 <= height):
         raise DomainViolation(f"rect {rect} invalid for {width}x{height} image")
-    out = decode_pixels(inf, grid_coords(width, height, x0, y0, x1, y1))
-    return out.reshape(y1 - y0, x1 - x0, inf.out_dim)
+    # pixel centres generated on the device (bit-identical to grid_coords)
+    w, h = x1 - x0, y1 - y0
+    xs = torch.empty((w * h, 2), dtype=torch.float32, device=inf.device)
+    _lib.call("pg_raster_coords_f32", x0, y0, w, h, width, height, _lib.ptr(xs), _lib.stream_ptr())
+    out = decode_device(inf, xs, exact=exact)
+    return out.cpu().numpy().reshape(h, w, inf.out_dim)
 
 
 def decode_image(inf: InferenceModel, width: int | None = None,
-                 height: int | None = None) -> np.ndarray:
+                 height: int | None = None, exact: bool = True) -> np.ndarray:
     """Decode the full image (model_io.py:342-349)."""
     width = width or inf.width
     height = height or inf.height
     if width < 1 or height < 1:
         raise DomainViolation("model stores no image dimensions; pass them")
-    return decode_rect(inf, (0, 0, width, height), width, height)
+    return decode_rect(inf, (0, 0, width, height), width, height, exact=exact)
 
 
 class HostDecoder:

@@ -136,9 +136,8 @@ class TrainState:
         self.reference_order = reference_order
         self.exact_mlp = exact_mlp or reference_order
         if reference_order:
-            if not self.fused or deterministic:
-                raise InvalidHyperparameter(
-                    "reference_order needs the fused float32 shape and is exclusive with deterministic")
+            if not self.fused:
+                raise InvalidHyperparameter("reference_order needs the fused float32 shape")
             na = int(_lib.lib().pg_mlp_acts_floats(B, model.mlp_desc))
             self.acts = torch.empty(na, dtype=tdt, device=dev)
         if not self.fused:
@@ -233,6 +232,18 @@ class TrainState:
         if self.exact_mlp and self.fused:
             flags |= _lib.PG_EXACT_MLP
         scale = float(np.dtype(m.dtype).type(self.scale))
+        if self.reference_order and self.deterministic:
+            if dy_out is not None:
+                raise InvalidHyperparameter("dy_out is not produced in reference_order mode")
+            gf, gm, gc = m.fx_ptrs()
+            _lib.call("pg_train_fused_ref_det_f32", m.grid, m.mlp_desc, _lib.ptr(xs), _lib.ptr(targets),
+                      xs.shape[0], _lib.ptr(m.feats), _lib.ptr(m.baked), _lib.ptr(m.conf),
+                      _lib.ptr(m.mlp_params), scale, flags, gf, gc, _lib.ptr(m.touched),
+                      _lib.ptr(m.loss_fx), _lib.ptr(self.acts), s)
+            m.fx_flush(loss_sum=self.loss_sum)
+            _lib.call("pg_mlp_wgrad_blas_f32", m.mlp_desc, _lib.ptr(self.acts), xs.shape[0],
+                      _lib.ptr(m.gmlp), s)
+            return
         if self.deterministic:
             gf, gm, gc = m.fx_ptrs()
             if self.fused:
