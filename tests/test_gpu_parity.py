@@ -255,7 +255,8 @@ def test_train_step_parity_c1():
     import paper_2312_17241_b200 as pg
     img = _smooth()
     st = pg.TrainState(pg.init_model(pg.HyperParams(**C1), seed=0), img,
-                       pg.TrainConfig(batch_size=8192, seed=0), reference_order=True)
+                       pg.TrainConfig(batch_size=8192, seed=0), reference_order=True,
+                       deterministic=True)
     ost = O.TrainState(O.init_model(O.Hyper(**C1), seed=0), img, O.TrainCfg(batch_size=8192, seed=0))
     # Confidences: Adam normalises each element's gradient, so an element
     # whose gradient is ~0 moves by up to +-lr per step on rounding noise.
