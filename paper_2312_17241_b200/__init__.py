@@ -9,9 +9,9 @@ libprobegrid_b200.so and fails loudly if it or a CUDA device is missing.
 
 __version__ = "0.1.0"
 
-from .errors import (BadMagic, DomainViolation, InvalidHyperparameter, InvariantViolation,
-                     ModelFileError, ProbeGridError, ShapeMismatch, StaleTrace, TrainingDiverged,
-                     TruncatedFile, UnbakedModel, VersionMismatch)
+from .errors import (BadMagic, DimensionMismatch, DomainViolation, InvalidHyperparameter,
+                     InvariantViolation, ModelFileError, ProbeGridError, ShapeMismatch, StaleTrace,
+                     TargetTooSmall, TrainingDiverged, TruncatedFile, UnbakedModel, VersionMismatch)
 from .hyper import (AUX_PRIMES, PRIMARY_PRIMES, HyperParams, LevelMode, LevelSpec,
                     build_level_specs, level_resolution)
 
@@ -23,7 +23,8 @@ __all__ = [
     "to_inference", "decode_pixels", "decode_at", "decode_rect", "decode_image", "InferenceModel",
     "ModelFileError", "BadMagic", "VersionMismatch", "TruncatedFile", "InvariantViolation",
     "serialize", "deserialize", "read_header", "size_report", "SizeReport", "pack_indices",
-    "unpack_indices", "HEADER_BYTES", "load", "save",
+    "unpack_indices", "HEADER_BYTES", "load", "save", "select_hyperparams",
+    "expand_grid", "run_sweep", "write_csv", "SweepPoint", "psnr", "pareto_front",
 ]
 
 
@@ -35,13 +36,16 @@ def __getattr__(name):
     if name in ("encode_forward", "encode_backward"):
         from . import encoding
         return getattr(encoding, name)
-    if name in ("TrainConfig", "TrainState", "FieldTrainState", "fit", "adam_update"):
+    if name in ("TrainConfig", "TrainState", "FieldTrainState", "fit", "adam_update", "select_hyperparams"):
         from . import train
         return getattr(train, name)
     if name in ("to_inference", "decode_pixels", "decode_at", "decode_rect", "decode_image",
                 "InferenceModel", "TouchCounter", "HostDecoder"):
         from . import decode
         return getattr(decode, name)
+    if name in ("expand_grid", "run_sweep", "write_csv", "SweepPoint", "psnr", "pareto_front", "CSV_COLUMNS"):
+        from . import sweep
+        return getattr(sweep, name)
     if name in ("serialize", "deserialize", "read_header", "size_report", "SizeReport", "pack_indices",
                 "unpack_indices", "HEADER_BYTES", "parse", "load", "save"):
         from . import model_io

@@ -357,6 +357,12 @@ class FitResult:
     ms_per_step: float
     losses: list = field(default_factory=list, repr=False)
 
+    @property
+    def size_report(self):
+        """Exact .cngp byte breakdown of this model (trainer.py FitResult)."""
+        from .model_io import size_report
+        return size_report(self.model.hyper)
+
 
 def psnr(reference, test) -> float:
     """20*log10(1/RMSE) over [0,1] values in fp64 (metrics.py:12-26)."""
@@ -397,3 +403,34 @@ def fit(image, hyper: HyperParams, cfg: TrainConfig, force_probed: bool = False,
     final = psnr(img, np.clip(decoded, 0.0, 1.0))
     return FitResult(model, inf, final, losses[-1] if losses else float("nan"), cfg.steps, wall,
                      float(np.median(step_ms)) if step_ms else 0.0, losses)
+
+
+# size-budgeted hyper-parameters (trainer.py:27-31, 245-281)
+RECIPE_NF_MIN, RECIPE_NF_MAX = 2**6, 2**12
+RECIPE_NC_MIN, RECIPE_NC_MAX = 2**10, 2**16
+RECIPE_NP = 2**1
+
+
+def select_hyperparams(target_size_bytes: int, base: HyperParams | None = None) -> HyperParams:
+    """Largest tables that fit a .cngp byte budget: feature table from the
+    plain-hash lower bound (<= a third of the budget), then the index table
+    toward its ceiling, then the feature table with what remains — the
+    reference's recipe, so both pick the same configuration."""
+    from .errors import TargetTooSmall
+    from .model_io import size_report
+    base = base or HyperParams()
+    hyper = base.with_updates(n_f=RECIPE_NF_MIN, n_c=RECIPE_NC_MIN, n_p=RECIPE_NP)
+    total = lambda h: size_report(h).total_bytes  # noqa: E731
+    minimum = total(hyper)
+    if target_size_bytes < minimum:
+        raise TargetTooSmall(f"target {target_size_bytes} B below the smallest model ({minimum} B)")
+    n_f = RECIPE_NF_MIN
+    while n_f * 2 <= RECIPE_NF_MAX and \
+            total(hyper.with_updates(n_f=n_f * 2, n_p=1)) <= target_size_bytes // 3:
+        n_f *= 2
+    n_c = RECIPE_NC_MIN
+    while n_c * 2 <= RECIPE_NC_MAX and total(hyper.with_updates(n_f=n_f, n_c=n_c * 2)) <= target_size_bytes:
+        n_c *= 2
+    while n_f * 2 <= RECIPE_NF_MAX and total(hyper.with_updates(n_f=n_f * 2, n_c=n_c)) <= target_size_bytes:
+        n_f *= 2
+    return hyper.with_updates(n_f=n_f, n_c=n_c).validate()

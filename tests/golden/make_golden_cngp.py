@@ -72,6 +72,16 @@ def main():
     ex = serialize(to_inference(m, width=3, height=2))
     assert len(ex) == 87, len(ex)
     out["format_example_file"] = np.frombuffer(ex, np.uint8)
+    # trainer.select_hyperparams (size-budgeted configurations)
+    from probegrid.model_io import size_report
+    from probegrid.trainer import select_hyperparams
+    floor = size_report(HyperParams(n_f=2**6, n_c=2**10, n_p=2**1)).total_bytes
+    targets = [floor, floor + 1, 25_000, 60_000, 150_000, 300_000, 1_000_000, 5_000_000, 10**8]
+    sel = []
+    for t in targets:
+        h = select_hyperparams(t)
+        sel.append([t, h.n_f, h.n_c, h.n_p, size_report(h).total_bytes])
+    out["select_hyperparams"] = np.array(sel, np.int64)
     np.savez_compressed(os.path.join(HERE, "cngp_files.npz"), **out)
     print("cngp_files.npz", os.path.getsize(os.path.join(HERE, "cngp_files.npz")))
 

@@ -83,3 +83,24 @@ def test_trained_model_file_round_trip(tmp_path):
     # serialize(Model) downcasts first, as the reference does (no image size)
     raw = pg.serialize(res.model)
     assert raw[:44] == open(path, "rb").read()[:44] and raw[52:] == open(path, "rb").read()[52:]
+
+
+def test_gpu_sweep_small_grid(tmp_path):
+    """run_sweep on the device (sweep.py:61-84): one fit per (configuration,
+    seed), probed vs plain-hash rows, sizes from the file format."""
+    import paper_2312_17241_b200 as pg
+    from paper_2312_17241_b200.model_io import size_report
+    img = np.random.default_rng(0).random((16, 16, 3)).astype(np.float32)
+    base = pg.HyperParams(n_levels=4, n_min=4, n_max=16, n_neurons=16)
+    grid = pg.expand_grid(base, [64], [256], [1, 4])
+    seen = []
+    pts = pg.run_sweep(img, grid, [0, 1], pg.TrainConfig(steps=20, batch_size=128), progress=seen.append)
+    assert len(pts) == 4 and seen == pts
+    assert [p.method for p in pts] == ["baseline", "baseline", "probed", "probed"]
+    for p, (h, s) in zip(pts, [(h, s) for h in grid for s in (0, 1)]):
+        assert p.size_bytes == size_report(h).total_bytes and p.seed == s
+        assert np.isfinite(p.psnr_db) and p.psnr_db > 5.0
+    again = pg.run_sweep(img, grid[:1], [0], pg.TrainConfig(steps=20, batch_size=128))
+    assert abs(again[0].psnr_db - pts[0].psnr_db) < 1e-3   # same seeds (float atomics: not bit-reproducible)
+    pg.write_csv(pts, str(tmp_path / "s.csv"))
+    assert len(pg.pareto_front(pts)) >= 1
