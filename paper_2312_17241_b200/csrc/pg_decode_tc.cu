@@ -80,6 +80,17 @@ template <> struct FeatS<float> {
     }
 };
 
+template <typename FT> struct RangeLoad {
+    static constexpr bool ok = false;
+    static __device__ __forceinline__ float2 widen(uint32_t) { return make_float2(0.f, 0.f); }
+};
+template <> struct RangeLoad<__half> {
+    static constexpr bool ok = true;
+    static __device__ __forceinline__ float2 widen(uint32_t w) {
+        return __half22float2(*reinterpret_cast<const __half2 *>(&w));
+    }
+};
+
 // encode_level_fwd2 (pg_encode_dev.cuh) with optional on-chip tables:
 // identical indices, weights and blend order, so the result is bit-identical.
 template <typename FT, int D>
@@ -116,7 +127,7 @@ __device__ __forceinline__ float2 encode_level_fwd2_tab(const pg_grid &g, int l,
                         const int lg = 5 - __ffs(pbits) + 1;  // log2(32 / pbits)
                         const uint32_t word = reinterpret_cast<const uint32_t *>(tabs + off)[r >> lg];
                         idx[k] += (int)((word >> ((r & ((1u << lg) - 1u)) * pbits)) & ((1u << pbits) - 1u));
-                    } else {
+                    } else if (!(RangeLoad<FT>::ok && g.log2_np == 2)) {
                         idx[k] += (int)__ldg(baked + (int64_t)g.slot[l] * g.n_c + r);
                     }
                 }
@@ -127,6 +138,27 @@ __device__ __forceinline__ float2 encode_level_fwd2_tab(const pg_grid &g, int l,
     if (kind == PG_LEVEL_DENSE && off >= 0) {
 #pragma unroll
         for (int k = 0; k < C; ++k) f[k] = FeatS<FT>::ld2(tabs + off + idx[k] * (int)(2 * sizeof(FT)));
+    } else if (RangeLoad<FT>::ok && kind == PG_LEVEL_PROBED && off < 0 && g.log2_np == 2) {
+        // baked offsets in global memory (N_p = 4): fetch the whole probing
+        // range (4 binary16 rows = 16 B, one sector) together with the baked
+        // byte instead of after it and select the probe in registers — one L2
+        // round trip instead of two.  (A generic N_p = 2/4/8 version of this
+        // measured slower: register pressure at the 80-register budget.)
+        const FT *tab = feats + (int64_t)l * g.n_f * 2;
+        const uint8_t *bt = baked + (int64_t)g.slot[l] * g.n_c;
+        uint4 rng[C];
+        int bk[C];
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            const uint32_t base = (corner_hash<D>(k, c, g.primary) << 2) & nf_mask;
+            rng[k] = __ldg(reinterpret_cast<const uint4 *>(tab + (int64_t)base * 2));
+            bk[k] = (int)__ldg(bt + (corner_hash<D>(k, c, g.aux) & nc_mask));
+        }
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            const uint32_t w = bk[k] == 0 ? rng[k].x : bk[k] == 1 ? rng[k].y : bk[k] == 2 ? rng[k].z : rng[k].w;
+            f[k] = RangeLoad<FT>::widen(w);
+        }
     } else {
         const FT *tab = feats + (int64_t)l * g.n_f * 2;
 #pragma unroll
