@@ -61,6 +61,68 @@ __device__ __forceinline__ float2 encode_level_fwd2(const pg_grid &g, int l, con
     return make_float2(y0, y1);
 }
 
+// encode_level_fwd2 for N_p = 4 probed levels with the probing range fetched
+// whole (4 rows x F = 2: 32 B fp32 / 16 B fp16 — one sector) in parallel
+// with the baked byte, the probe selected in registers: one L2 round trip
+// instead of the dependent baked -> feature pair.  Identical arithmetic.
+template <typename FT, int D>
+__device__ __forceinline__ float2 encode_level_fwd2_rng(const pg_grid &g, int l, const float (&x)[D],
+                                                        const FT *__restrict__ feats,
+                                                        const uint8_t *__restrict__ baked) {
+    if (g.kind[l] != PG_LEVEL_PROBED || g.log2_np != 2) return encode_level_fwd2<FT, D>(g, l, x, feats, baked);
+    constexpr int C = 1 << D;
+    const uint32_t nf_mask = (uint32_t)g.n_f - 1u, nc_mask = (uint32_t)g.n_c - 1u;
+    const int res = g.res[l];
+    int c[D];
+    float t[D], omt[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        c[a] = cell_coord(x[a], res, t[a]);
+        omt[a] = __fsub_rn(1.0f, t[a]);
+    }
+    const FT *tab = feats + (int64_t)l * g.n_f * 2;
+    const uint8_t *bt = baked + (int64_t)g.slot[l] * g.n_c;
+    float2 f[C];
+    int bk[C];
+    if constexpr (sizeof(FT) == 4) {
+        float r[C][8];
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            const uint32_t base = (corner_hash<D>(k, c, g.primary) << 2) & nf_mask;
+            ld_nc_v8(reinterpret_cast<const float *>(tab) + (int64_t)base * 2, r[k]);
+            bk[k] = (int)__ldg(bt + (corner_hash<D>(k, c, g.aux) & nc_mask));
+        }
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            const int j = bk[k];
+            f[k].x = j == 0 ? r[k][0] : j == 1 ? r[k][2] : j == 2 ? r[k][4] : r[k][6];
+            f[k].y = j == 0 ? r[k][1] : j == 1 ? r[k][3] : j == 2 ? r[k][5] : r[k][7];
+        }
+    } else {
+        uint4 r[C];
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            const uint32_t base = (corner_hash<D>(k, c, g.primary) << 2) & nf_mask;
+            r[k] = __ldg(reinterpret_cast<const uint4 *>(tab + (int64_t)base * 2));
+            bk[k] = (int)__ldg(bt + (corner_hash<D>(k, c, g.aux) & nc_mask));
+        }
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            const int j = bk[k];
+            const uint32_t w = j == 0 ? r[k].x : j == 1 ? r[k].y : j == 2 ? r[k].z : r[k].w;
+            f[k] = __half22float2(*reinterpret_cast<const __half2 *>(&w));
+        }
+    }
+    float y0 = 0.0f, y1 = 0.0f;
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+        const float w = corner_weight<float, D>(k, t, omt);
+        y0 = __fadd_rn(y0, __fmul_rn(w, f[k].x));
+        y1 = __fadd_rn(y1, __fmul_rn(w, f[k].y));
+    }
+    return make_float2(y0, y1);
+}
+
 // Backward for one (point, level), F = 2, fp32: scatter w*up into the
 // feature-gradient table (all N_p probes, softmax-weighted, for probed
 // levels), the softmax-Jacobian term into gconf, and flag the row touched.

@@ -3,7 +3,7 @@
 //    the training pass for shapes the fused kernels do not cover);
 //  * the fused decode kernel: all-level encode + [32,64,64,<=4] MLP per
 //    128-query tile, activations resident in shared memory.
-#include "pg_common.cuh"
+#include "pg_encode_dev.cuh"
 
 namespace pg {
 
@@ -234,8 +234,6 @@ __global__ void __launch_bounds__(256, 2)
         p += kHid * out_dim;
         for (int i = tid; i < kOutMax; i += 256) sm.b2[i] = i < out_dim ? p[i] : 0.0f;
     }
-    constexpr int C = 1 << D;
-    const uint32_t nf_mask = (uint32_t)g.n_f - 1u, nc_mask = (uint32_t)g.n_c - 1u;
     const int64_t ntiles = (B + kTP - 1) / kTP;
     const int pl = tid & (kTP - 1);
     const int lhalf = tid >> 7;  // 0/1: which of the two levels per iteration
@@ -257,42 +255,8 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll 2
         for (int it = 0; it < 8; ++it) {
             const int l = 2 * it + lhalf;  // warp-uniform
-            const int res = g.res[l], kind = g.kind[l];
-            int c[D];
-            float t[D], omt[D];
-#pragma unroll
-            for (int a = 0; a < D; ++a) {
-                c[a] = cell_coord(x[a], res, t[a]);
-                omt[a] = __fsub_rn(1.0f, t[a]);
-            }
-            int idx[C];
-            float w[C];
-#pragma unroll
-            for (int k = 0; k < C; ++k) {
-                w[k] = corner_weight<float, D>(k, t, omt);
-                if (kind == PG_LEVEL_DENSE) {
-                    idx[k] = corner_dense<D>(k, c, res + 1);
-                } else {
-                    const uint32_t h = corner_hash<D>(k, c, g.primary);
-                    if (kind == PG_LEVEL_HASHED) {
-                        idx[k] = (int)(h & nf_mask);
-                    } else {
-                        const int r = (int)(corner_hash<D>(k, c, g.aux) & nc_mask);
-                        idx[k] = (int)((h << g.log2_np) & nf_mask) +
-                                 (int)__ldg(baked + (int64_t)g.slot[l] * g.n_c + r);
-                    }
-                }
-            }
-            const FT *tab = feats + (int64_t)l * g.n_f * 2;
-            float2 f[C];
-#pragma unroll
-            for (int k = 0; k < C; ++k) f[k] = Feat<FT>::ld2(tab + (int64_t)idx[k] * 2);
-            float y0 = 0.0f, y1 = 0.0f;  // _core.pyx:53-54 blend order, from zero
-#pragma unroll
-            for (int k = 0; k < C; ++k) {
-                y0 = __fadd_rn(y0, __fmul_rn(w[k], f[k].x));
-                y1 = __fadd_rn(y1, __fmul_rn(w[k], f[k].y));
-            }
+            const float2 yv = encode_level_fwd2_rng<FT, D>(g, l, x, feats, baked);
+            const float y0 = yv.x, y1 = yv.y;
             sm.actA[swz(2 * l, pl)] = y0;
             sm.actA[swz(2 * l + 1, pl)] = y1;
         }
