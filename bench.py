@@ -396,9 +396,11 @@ def run_gpu(args, rank, world, local_rank):
                      "mlp_tflops": qps / world * mlp_flops / 1e12,
                      "note": "table gathers are L2-resident: bytes are algorithmic gather bytes; "
                              "HBM streams only 20 B/query (coords + outputs). The binding limit is "
-                             "the random-gather rate (pg_probe_gather, ~1 per SM per clock): "
-                             "random_gathers_per_query counts feature rows and baked bytes not "
-                             "served from shared memory"},
+                             "the random-gather rate (pg_probe_gather, ~1 per SM per clock, measured "
+                             "with 4-32 MiB tables, i.e. every gather an L1 miss): "
+                             "random_gathers_per_query counts feature rows / probing ranges and baked "
+                             "bytes not served from shared memory; the decode's coarse levels hit in "
+                             "L1, so this fraction can exceed 1"},
         "clocks": clk,
         "ablation_queries_per_s": ablation,
         "raster_order_queries_per_s": raster_qps,
