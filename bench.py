@@ -314,6 +314,8 @@ def run_gpu(args, rank, world, local_rank):
     # 8192^2 image in raster order: neighbouring lanes share cells on the
     # coarse levels, the access pattern decode_image / decode_rect produce
     W_img, H_slab = 8192, B_INFER // 8192
+    if os.environ.get("PG_BENCH_NO_RASTER"):
+        W_img, H_slab = 8192, 1
     yy, xx = torch.meshgrid(torch.arange(H_slab, device=dev), torch.arange(W_img, device=dev),
                             indexing="ij")
     xs_r = torch.stack([(xx.reshape(-1).float() + 0.5) / W_img,
