@@ -793,3 +793,29 @@ def test_long_probing_ranges_vs_oracle(n_p):
     gc = m.gconf.cpu().numpy()
     for i, lv in enumerate(m.probed):
         np.testing.assert_allclose(gc[i], om.levels[lv].cgrad, rtol=1e-5, atol=1e-6)
+
+
+def test_c_abi_rejects_bad_arguments():
+    """Invalid descriptors and sizes come back as a non-zero status with a
+    message (pg_last_error), raised as ValueError by the binding — no launch,
+    no crash (SURVEY 8b error behaviour)."""
+    import ctypes
+    import paper_2312_17241_b200 as pg
+    from paper_2312_17241_b200 import _lib
+    m = pg.init_model(pg.HyperParams(**C1), seed=0)
+    xs = torch.rand((128, 2), device="cuda")
+    y = torch.empty((128, 32), device="cuda")
+    bad = _lib.PgGrid.from_buffer_copy(bytes(m.grid))
+    bad.n_f = 1000                                   # not a power of two
+    with pytest.raises(ValueError, match="power"):
+        _lib.call("pg_encode_fwd_f32", ctypes.byref(bad), _lib.ptr(xs), 128, _lib.ptr(m.feats), _lib.ptr(m.baked),
+                  None, 0, _lib.ptr(y), None, _lib.stream_ptr())
+    with pytest.raises(ValueError):
+        _lib.call("pg_unpack_indices", None, 1, 16, 9, None, _lib.stream_ptr())   # 9-bit offsets
+    with pytest.raises(ValueError):
+        _lib.call("pg_raster_coords_f32", 0, 0, 10, 10, 5, 5, None, _lib.stream_ptr())   # rect outside
+    inf = pg.to_inference(m)
+    with pytest.raises(ValueError):
+        _lib.call("pg_decode_host_f32", inf.grid, inf.mlp_desc, None, 10, _lib.ptr(inf.feats16), _lib.ptr(inf.baked),
+                  _lib.ptr(inf.params), 0, 0, None, None, None, None, None, None)        # chunk 0
+    torch.cuda.synchronize()    # the context is still healthy
