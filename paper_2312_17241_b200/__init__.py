@@ -18,7 +18,8 @@ from .hyper import (AUX_PRIMES, PRIMARY_PRIMES, HyperParams, LevelMode, LevelSpe
 __all__ = [
     "AUX_PRIMES", "PRIMARY_PRIMES", "HyperParams", "LevelMode", "LevelSpec", "build_level_specs",
     "level_resolution", "ProbeGridError", "InvalidHyperparameter", "DomainViolation",
-    "ShapeMismatch", "StaleTrace", "TrainingDiverged", "UnbakedModel",
+    "ShapeMismatch", "StaleTrace", "TrainingDiverged", "UnbakedModel", "DimensionMismatch",
+    "TargetTooSmall",
     "init_model", "Model", "encode_forward", "encode_backward", "TrainConfig", "TrainState", "fit",
     "to_inference", "decode_pixels", "decode_at", "decode_rect", "decode_image", "InferenceModel",
     "ModelFileError", "BadMagic", "VersionMismatch", "TruncatedFile", "InvariantViolation",

@@ -1,4 +1,4 @@
-import os, sys, torch, numpy as np
+import os, sys, torch
 sys.path.insert(0, os.getcwd())
 from paper_2312_17241_b200 import _lib
 _lib._LIB = _lib.load(sys.argv[1])
