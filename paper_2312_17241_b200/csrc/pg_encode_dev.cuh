@@ -131,7 +131,7 @@ template <int NPMAX, typename ACC>
 __device__ __forceinline__ void encode_probe_reds(ACC *gb, ACC *gc, int n_p, const float (&sg)[NPMAX],
                                                   const float (&dots)[NPMAX], float s, float g0, float g1);
 
-template <int D, int NPMAX, typename ACC = float>
+template <int D, int NPMAX, typename ACC = float, bool LAZY = false>
 __device__ __forceinline__ void encode_level_bwd2(const pg_grid &g, int l, const float (&x)[D],
                                                   float up0, float up1,
                                                   const float *__restrict__ feats,
@@ -221,7 +221,7 @@ __device__ __forceinline__ void encode_level_bwd2(const pg_grid &g, int l, const
 #pragma unroll
         for (int u = 0; u < PF; ++u) {
             const int k = k0 + u;
-            touched[crow[k]] = 1;
+            if (!LAZY) touched[crow[k]] = 1;
             const float g0 = __fmul_rn(wk[k], up0), g1 = __fmul_rn(wk[k], up1);
             ACC *gc = gconf + crow[k] * n_p;
             ACC *gb = gtab + (int64_t)bs[k] * 2;
@@ -247,6 +247,19 @@ __device__ __forceinline__ void encode_level_bwd2(const pg_grid &g, int l, const
                     dots[j] = __fadd_rn(__fmul_rn(fv[u][j][0], g0), __fmul_rn(fv[u][j][1], g1));
                     s = __fadd_rn(s, __fmul_rn(sg[j], dots[j]));
                 }
+            if (LAZY) {
+                // A lookup that adds a normal (non-zero, non-subnormal: the
+                // vector reductions flush subnormals) value to its gconf row
+                // needs no flag: the lazy Adam also visits every row whose
+                // gradient is non-zero.  Only all-zero contributions (zero
+                // corner weight or upstream, equal dots, exp underflow) are
+                // flagged -- a byte store on ~0% of lookups instead of all.
+                bool live = false;
+#pragma unroll
+                for (int j = 0; j < NPMAX; ++j)
+                    if (j < n_p) live |= fabsf(sg[j] * (dots[j] - s)) >= 1.17549435e-38f;
+                if (!live) touched[crow[k]] = 1;
+            }
             encode_probe_reds<NPMAX, ACC>(gb, gc, n_p, sg, dots, s, g0, g1);
         }
     }

@@ -74,8 +74,15 @@ __global__ void lazy_adam_rebake_kernel(T *conf, T *m, T *v, uint8_t *baked, T *
     const bool skip = guard && !isfinite(*guard);
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
          r += (int64_t)gridDim.x * blockDim.x) {
-        if (!touched[r]) continue;
+        // a row is due when flagged or when its gradient is non-zero (the
+        // fused fp32 training pass flags only all-zero lookups,
+        // encode_level_bwd2<..., LAZY>); every lookup of a flagged-or-
+        // non-zero row is exactly the reference's touched set up to an
+        // exact cancellation of its summed gradient
         T *gp = gconf + r * n_p;
+        bool due = touched[r] != 0;
+        for (int j = 0; j < n_p && !due; ++j) due = gp[j] != T(0);
+        if (!due) continue;
         if (!skip)
             adam_row<T>(conf + r * n_p, m + r * n_p, v + r * n_p, gp, n_p, b1, nb1, b2, nb2, ic1,
                         ic2, lr, eps, baked + r);

@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(tm::kNT, 2)
                 S.y[(2 * l + 1) * kS + pl] = yv.y;
             }
             if (pl < nv)
-                encode_level_bwd2<D, NPM, ACC>(g, l, x, S.dy[(2 * l) * kS + pl], S.dy[(2 * l + 1) * kS + pl],
+                encode_level_bwd2<D, NPM, ACC, std::is_same<ACC, float>::value>(g, l, x, S.dy[(2 * l) * kS + pl], S.dy[(2 * l + 1) * kS + pl],
                                                feats, conf, gfeat, gconf, touched);
         }
 #pragma unroll

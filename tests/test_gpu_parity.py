@@ -297,6 +297,16 @@ def test_train_step_parity_c1():
             assert frac <= conf_bar and bfrac <= baked_bar
 
 
+def _assert_due_rows(m, traces):
+    """The confidence rows the lazy Adam will visit (touched flag OR non-zero
+    gradient row, pg_optim.cu lazy_adam_rebake_kernel) are exactly the rows
+    the reference looked up (trainer.py:162-167 via encoding.py:111)."""
+    gc = m.gconf.cpu().numpy()
+    due = m.touched.cpu().numpy().reshape(gc.shape[:2]).astype(bool) | (gc != 0).any(axis=-1)
+    for i, lv in enumerate(m.probed):
+        eq(np.nonzero(due[i])[0], np.unique(traces[lv].row))
+
+
 @pytest.mark.parametrize("mode", ["fused_exact", "generic", "fused_tensor"])
 def test_step_gradients_vs_oracle(mode):
     """Gradients of one batch (no optimizer) against numpy/OpenBLAS.  The
@@ -344,6 +354,7 @@ def test_step_gradients_vs_oracle(mode):
         close_grad(gf[L.level], L.fgrad, 1e-10, tc)
     for i, lv in enumerate(m.probed):
         close_grad(gc[i], om.levels[lv].cgrad, 1e-10, tc)
+    _assert_due_rows(m, traces)
 
 
 @pytest.mark.parametrize("B", [1000, 64 * 3 + 1, 37])
@@ -376,6 +387,27 @@ def test_step_gradients_ragged_batch(B):
     gc = m.gconf.cpu().numpy()
     for i, lv in enumerate(m.probed):
         close_grad(gc[i], om.levels[lv].cgrad, 1e-10, True)
+    _assert_due_rows(m, traces)
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_touched_rows_with_zero_weight_corners(exact):
+    """Lookups whose gradient contribution is exactly zero (samples on cell
+    boundaries: zero corner weights; a zero upstream) must still mark their
+    rows: the fused tensor-core pass flags only those, the exact pass flags
+    every lookup; both must give the reference's touched set."""
+    import paper_2312_17241_b200 as pg
+    img = _smooth()
+    m, om = _models(C1, perturb=False)
+    st = pg.TrainState(m, img, pg.TrainConfig(batch_size=4096, seed=0), exact_mlp=exact)
+    xs = _edge_points(4096, 2, np.float32, seed=4)
+    xs[100:1100] = np.round(xs[100:1100] * 16) / 16          # on level-0 grid lines
+    xs[1100:1200] = 0.0
+    tg = np.random.default_rng(9).random((4096, 3)).astype(np.float32)
+    st.loss_sum.zero_()
+    st.compute_grads(torch.from_numpy(xs).cuda(), torch.from_numpy(tg).cuda())
+    _, traces = O.encode_forward(om, xs)
+    _assert_due_rows(m, traces)
 
 
 @pytest.mark.parametrize("od", [3, 2, 4])

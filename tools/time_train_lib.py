@@ -9,6 +9,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2312_17241_b200 import _lib  # noqa: E402
 
+import ctypes  # noqa: E402
+_raw = ctypes.CDLL(sys.argv[1])
+_lib._SIGS = {k: v for k, v in _lib._SIGS.items() if hasattr(_raw, k)}   # older builds lack newer entries
 _lib._LIB = _lib.load(sys.argv[1])
 import paper_2312_17241_b200 as pg  # noqa: E402
 from tests.golden_util import smooth_image  # noqa: E402
