@@ -239,10 +239,17 @@ int pg_mlp_train_f64(const pg_mlp *mlp, const double *y, const double *targets,
 /* Fused training pass (trainer.py:118-148): per 64-sample tile one kernel
  * runs encode fwd -> MLP fwd -> squared error -> MLP bwd -> encode bwd with
  * activations in shared memory.  Shape: F = 2, 16 levels, N_p <= 16, MLP
- * [32, 64, 64, out_dim <= 4].  Forward and data-gradient GEMMs follow
- * numpy/OpenBLAS's FMA-chain order, so y, the loss terms and dL/dy equal the
- * reference's bit for bit; weight/bias gradients (into gparams) and table
- * gradients (gfeat, gconf, touched) are accumulated as pg_encode_bwd does.
+ * [32, 64, 64, out_dim <= 4].
+ * Default: every MLP GEMM on tensor cores (mma.sync tf32, 3-term split,
+ * fp32-level accuracy), the next tile's encode fwd fused with this tile's
+ * encode bwd.  Table gradients (gfeat, gconf) are accumulated as
+ * pg_encode_bwd does; touched[] is set only for lookups whose gconf
+ * contribution is all zero/subnormal -- pg_lazy_adam_rebake_f32 also visits
+ * every row with a non-zero gradient, which together is the reference's
+ * touched set.
+ * flags & PG_EXACT_MLP: CUDA-core MLP in numpy/OpenBLAS's FMA-chain order, so
+ * y, the loss terms and dL/dy equal the reference's bit for bit; touched[]
+ * is set for every lookup.
  * loss_sum += sum of squared errors (fp64).  dy_out (optional, B x 32)
  * receives dL/dy for parity checks. */
 int pg_train_fused_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
@@ -352,8 +359,9 @@ int pg_adam_f64(double *param, double *grad, double *m, double *v, int64_t n,
                 const double *d_guard, void *stream);
 
 /* Lazy Adam + incremental re-bake over every confidence row whose touched
- * flag is set (trainer.py:162-167 with _core.pyx:224-272 arithmetic), then
- * clears that row's gradient and flag.  rows = n_probed*n_c. */
+ * flag is set or whose gradient row is non-zero (trainer.py:162-167 with
+ * _core.pyx:224-272 arithmetic), then clears that row's gradient and flag.
+ * rows = n_probed*n_c. */
 int pg_lazy_adam_rebake_f32(float *conf, float *m, float *v, uint8_t *baked,
                             float *gconf, uint8_t *touched, int64_t rows,
                             int n_p, int64_t t, double lr, double beta1,
