@@ -20,8 +20,9 @@ from tests.golden_util import smooth_image  # noqa: E402
 EXACT = len(sys.argv) > 1 and sys.argv[1] == "exact"
 NAMES = (["tile load", "encode fwd", "layer 1", "layer 2", "output+loss", "dW2", "delta2", "dW1",
           "delta1", "dW0", "dy", "encode bwd (+next-tile wait)"] if EXACT else
-         ["tile load", "encode fwd", "layer 1", "layer 2", "output+loss", "dW2 + delta2", "delta2 store",
-          "dW1 + dgrad2", "delta1 mask", "dW0 + dgrad1", "dy store + db0", "encode bwd (+next-tile wait)"])
+         ["stage next tile", "tile barrier (encode stragglers)", "layer 1", "layer 2", "output+loss",
+          "dW2 + delta2", "delta2 store", "dW1 + dgrad2", "delta1 mask", "dW0 + dgrad1", "dy store",
+          "fused encode bwd(t) + fwd(t+1)"])
 READ = "pg_phase_prof_read" if EXACT else "pg_phase_prof_read_mma"
 st = pg.TrainState(pg.init_model(pg.HyperParams(n_f=2**12, n_c=2**14, n_p=4), seed=0),
                    smooth_image(256, 256), pg.TrainConfig(batch_size=1 << 18, seed=0), sampler="device",
