@@ -365,6 +365,7 @@ def run_gpu(args, rank, world, local_rank):
     if not args.quick:
         extra["train_c3"] = run_train_field(args, pg, torch, dist, rank, world, barrier, max_over_ranks, "c3")
         extra["train_c4"] = run_train_field(args, pg, torch, dist, rank, world, barrier, max_over_ranks, "c4")
+        extra["train_c4_nerf"] = run_train_nerf(args, pg, torch, dist, rank, world, barrier, max_over_ranks)
         if world == 1:
             extra["sweep_inference_c2_c5"] = run_sweep(args, pg, torch, decode_device)
 
@@ -515,6 +516,41 @@ def run_train_field(args, pg, torch, dist, rank, world, barrier, max_over_ranks,
                        "samples_per_gpu_per_step": B, "mlp": hyper.mlp_widths(),
                        "probed_levels": len(model.probed), "parallelism": f"dp{world}"},
             "encode_bytes_per_sample": bps, "encode_algorithmic_gbs": B * bps / (ms * 1e-3) / 1e9,
+            "last_loss": st.loss_value()}
+
+
+def run_train_nerf(args, pg, torch, dist, rank, world, barrier, max_over_ranks):
+    """C4 with the volume-compositing head: 2^12 rays x 64
+    samples per GPU per step (2^18 samples), C4 encoding (N_p=8, out 4);
+    targets rendered from an analytic field (soft ball of density, colour =
+    position) through the same compositing.  Step = ray sampling, encode
+    fwd, MLP + compositing + loss + backward, encode bwd, Adam, lazy Adam."""
+    from paper_2312_17241_b200 import nerf
+    hk = dict(d=3, n_f=2**8, n_c=2**16, n_p=8, n_max=2048, out_dim=4)
+    R, S = 1 << 12, 64
+    hyper = pg.HyperParams(**hk)
+    model = pg.init_model(hyper, seed=0)
+    o, d = nerf.orbit_rays(2 * R * world, seed=1)
+    pts, deltas = nerf.sample_points(o, d, S)
+    r = (pts - 0.5).norm(dim=1, keepdim=True)
+    raw = torch.cat([12.0 * (0.3 - r) / 0.05, 4.0 * (pts - 0.5)], dim=1).contiguous()
+    tgt = nerf.composite(raw, deltas, S)
+    st = nerf.NerfTrainState(model, o, d, tgt, pg.TrainConfig(batch_size=R, seed=rank), n_samples=S)
+    dp = None
+    if world > 1:
+        from paper_2312_17241_b200.dist import DataParallel
+        dp = DataParallel(st, dist)
+    steps = max(3, args.steps // 4)
+    ms = _time_steps(torch, dp.launch_step if dp else st.launch_step, steps, args.warmup, barrier,
+                     max_over_ranks)
+    return {"metric": "train rays/s", "value": world * R / (ms * 1e-3), "unit": "rays/s",
+            "samples_per_s": world * R * S / (ms * 1e-3), "ms_per_step": ms, "steps": steps,
+            "config": {"workload": "C4 NeRF-style step with volume compositing", **hk,
+                       "rays_per_gpu_per_step": R, "samples_per_ray": S, "mlp": hyper.mlp_widths(),
+                       "probed_levels": len(model.probed), "parallelism": f"dp{world}",
+                       "path": ("fused tensor-core step, one ray per 64-sample tile composited in-kernel "
+                                "(pg_train_fused_f32 + PG_COMPOSITE)" if st.nerf_fused else
+                                "generic encode kernels + pg_nerf_train_f32")},
             "last_loss": st.loss_value()}
 
 

@@ -54,6 +54,9 @@ extern "C" {
 #define PG_SMEM_TABLES 32u    /* decode: force the shared-memory baked-index
                                * variant (default: automatic, N_p = 2 or 4) */
 #define PG_NO_SMEM_TABLES 64u /* decode: never use it                       */
+#define PG_COMPOSITE 128u     /* fused training: volume compositing, one ray
+                               * of 64 samples per tile; targets (B, 4) =
+                               * (segment length, ray r, g, b) per sample */
 
 /* Geometry of one multiresolution grid (HyperParams + build_level_specs,
  * model.py:35-87, indexing.py:93-101).  Feature tables of all levels are one
@@ -259,6 +262,31 @@ int pg_train_fused_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
                        float *gfeat, float *gconf, uint8_t *touched,
                        float *gparams, double *loss_sum, float *dy_out,
                        void *stream);
+
+/* Volume-compositing head (the reference has no
+ * renderer, so these are checked against the numpy restatement in
+ * oracle/oracle.py and finite differences).  raw (R*S, 4) = per-sample MLP
+ * outputs (sigma_raw, r, g, b) of R rays x S samples in ray-major order;
+ * sigma = softplus(sigma_raw), colour = logistic(rgb_raw),
+ * alpha_i = 1 - exp(-sigma_i * deltas_i), T_i = prod_{j<i}(1 - alpha_j),
+ * rgb = sum_i T_i alpha_i c_i.  weights (optional, R*S) = T_i alpha_i. */
+int pg_composite_fwd_f32(const float *raw, const float *deltas, int64_t R,
+                         int S, float *rgb, float *weights, void *stream);
+/* S midpoint samples per ray inside [0,1]^3 (slab entry/exit; a ray that
+ * misses gets zero-length segments): pts (R*S, 3) clamped to [0,1],
+ * deltas (R*S) = segment length.  origins/dirs (R, 3). */
+int pg_ray_samples_f32(const float *origins, const float *dirs, int64_t R,
+                       int S, float *pts, float *deltas, void *stream);
+/* NeRF-style training pass over R rays x S samples: y (R*S, widths[0]) are
+ * the samples' encodings (pg_encode_fwd_f32); MLP forward (widths[-1] = 4),
+ * compositing, loss = sum (rgb - target_rgb)^2 into *loss_sum (fp64),
+ * dL/drgb = scale * (rgb - target), backward through compositing and the
+ * MLP: gparams += parameter grads, dy (R*S, widths[0]) = dL/dy for
+ * pg_encode_bwd_f32.  ws: pg_mlp_train_workspace_floats(R*S, mlp). */
+int pg_nerf_train_f32(const pg_mlp *mlp, const float *y, const float *deltas,
+                      const float *target_rgb, int64_t R, int S,
+                      const float *params, float scale, float *gparams,
+                      float *dy, double *loss_sum, float *ws, void *stream);
 
 /* .cngp index blocks (model_io.py:150-165, FORMAT.md "Index block packing"):
  * n_rows blocks of n_c probe offsets at w = log2_np bits each, entry k in

@@ -681,3 +681,83 @@ def grid_coords(width, height, x0, y0, x1, y1):
     cols, rows = np.meshgrid(np.arange(x0, x1), np.arange(y0, y1))
     return np.stack([(cols.ravel() + 0.5) / width, (rows.ravel() + 0.5) / height],
                     axis=1).astype(np.float32)
+
+
+# --------------------------------------------------------------------------
+# volume compositing head.  NOT in the reference (no
+# renderer there): this is the definitional restatement the CUDA kernels
+# (pg_composite_fwd_f32 / pg_nerf_train_f32) are checked against, itself
+# checked by finite differences (tests/test_nerf_oracle.py).  "parity
+# unpinned" for this row: no reference outputs exist to pin it to.
+# --------------------------------------------------------------------------
+def _softplus(x):
+    return np.where(x > 20, x, np.log1p(np.exp(np.minimum(x, 20))))
+
+
+def _logistic(x):
+    return 1.0 / (1.0 + np.exp(-x))
+
+
+def composite_forward(raw, deltas):
+    """raw (R, S, 4) = (sigma_raw, r, g, b) per sample, deltas (R, S) ->
+    rgb (R, 3), weights (R, S): sigma = softplus, c = logistic,
+    alpha = 1 - exp(-sigma delta), T_i = prod_{j<i}(1 - alpha_j)."""
+    raw = np.asarray(raw)
+    tr = np.exp(-_softplus(raw[..., 0]) * deltas)
+    T = np.cumprod(np.concatenate([np.ones_like(tr[:, :1]), tr[:, :-1]], axis=1), axis=1)
+    w = T * (1 - tr)
+    c = _logistic(raw[..., 1:])
+    return (w[..., None] * c).sum(axis=1), w
+
+
+def composite_backward(raw, deltas, g_rgb):
+    """dL/draw (R, S, 4) for dL/drgb = g_rgb (R, 3): dC/dc_i = w_i,
+    dC/dsigma_i = delta_i (T_{i+1} c_i - sum_{k>i} w_k c_k)."""
+    raw = np.asarray(raw)
+    tr = np.exp(-_softplus(raw[..., 0]) * deltas)
+    T = np.cumprod(np.concatenate([np.ones_like(tr[:, :1]), tr[:, :-1]], axis=1), axis=1)
+    w = T * (1 - tr)
+    c = _logistic(raw[..., 1:])
+    cg = (c * g_rgb[:, None, :]).sum(-1)                         # c_i . g
+    wcg = w * cg
+    after = np.cumsum(wcg[:, ::-1], axis=1)[:, ::-1] - wcg       # sum_{k>i} w_k c_k . g
+    dsig = deltas * (T * tr * cg - after)
+    out = np.empty_like(raw)
+    out[..., 0] = dsig * _logistic(raw[..., 0])
+    out[..., 1:] = w[..., None] * g_rgb[:, None, :] * c * (1 - c)
+    return out
+
+
+def nerf_step_grads(model: OModel, pts, deltas, target_rgb, n_samples, scale, kern=CBackend):
+    """One NeRF-style gradient pass on the numpy side: encode fwd, MLP fwd,
+    compositing, loss sum, dL/draw, MLP bwd, encode bwd (accumulates into
+    model.W grads / level grads).  Returns (loss_sum, dy)."""
+    y, traces = encode_forward(model, pts, kern)
+    raw, cache = mlp_forward(model.W, model.b, y)
+    R = target_rgb.shape[0]
+    rgb, _ = composite_forward(raw.reshape(R, n_samples, 4), deltas.reshape(R, n_samples))
+    diff = rgb - target_rgb
+    loss = float((diff.astype(np.float64) ** 2).sum())
+    draw = composite_backward(raw.reshape(R, n_samples, 4), deltas.reshape(R, n_samples),
+                              diff * np.float32(scale)).reshape(-1, 4).astype(raw.dtype)
+    dy = mlp_backward(model.W, model.Wg, model.bg, cache, draw)
+    encode_backward(model, traces, dy, kern)
+    return loss, dy
+
+
+def ray_samples(origins, dirs, n_samples):
+    """Midpoint samples inside [0,1]^3 (slab entry/exit), float32 like the
+    kernel: points (R*S, 3) clamped to [0,1], deltas (R*S)."""
+    o = np.asarray(origins, np.float32)
+    d = np.asarray(dirs, np.float32)
+    dd = np.where(np.abs(d) < np.float32(1e-12), np.float32(1e-12), d)
+    inv = np.float32(1) / dd
+    t0, t1 = (np.float32(0) - o) * inv, (np.float32(1) - o) * inv
+    near = np.maximum(np.minimum(t0, t1).max(axis=1), np.float32(0))
+    far = np.maximum(t0, t1).min(axis=1)
+    hit = far > near
+    near, far = np.where(hit, near, 0).astype(np.float32), np.where(hit, far, 0).astype(np.float32)
+    step = (far - near) / np.float32(n_samples)
+    t = near[:, None] + (np.arange(n_samples, dtype=np.float32) + np.float32(0.5))[None, :] * step[:, None]
+    pts = np.clip(o[:, None, :] + t[..., None] * d[:, None, :], 0, 1).astype(np.float32)
+    return pts.reshape(-1, 3), np.repeat(step, n_samples)

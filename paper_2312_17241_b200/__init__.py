@@ -26,6 +26,7 @@ __all__ = [
     "serialize", "deserialize", "read_header", "size_report", "SizeReport", "pack_indices",
     "unpack_indices", "HEADER_BYTES", "load", "save", "select_hyperparams",
     "expand_grid", "run_sweep", "write_csv", "SweepPoint", "psnr", "pareto_front",
+    "NerfTrainState", "render", "composite", "orbit_rays", "sample_points",
 ]
 
 
@@ -44,6 +45,9 @@ def __getattr__(name):
                 "InferenceModel", "TouchCounter", "HostDecoder"):
         from . import decode
         return getattr(decode, name)
+    if name in ("NerfTrainState", "render", "composite", "orbit_rays", "sample_points"):
+        from . import nerf
+        return getattr(nerf, name)
     if name in ("expand_grid", "run_sweep", "write_csv", "SweepPoint", "psnr", "pareto_front", "CSV_COLUMNS"):
         from . import sweep
         return getattr(sweep, name)

@@ -18,6 +18,7 @@ PG_MAX_LEVELS, PG_MAX_FEATURE, PG_MAX_PROBES, PG_MAX_LAYERS = 64, 16, 256, 17
 PG_LEVEL_DENSE, PG_LEVEL_HASHED, PG_LEVEL_PROBED = 0, 1, 2
 PG_EXACT_MLP, PG_SIGMOID, PG_SURROGATE, PG_HALF_FEATS, PG_NO_TENSOR = 1, 2, 4, 8, 16
 PG_SMEM_TABLES, PG_NO_SMEM_TABLES = 32, 64
+PG_COMPOSITE = 128
 
 
 class PgGrid(ctypes.Structure):
@@ -77,6 +78,9 @@ _SIGS.update({
     "pg_decode_f32": [_G, _M, _P, _I64, _P, _P, _P, ctypes.c_uint, _P, _P, _P],
     "pg_decode_host_f32": [_G, _M, _P, _I64, _P, _P, _P, ctypes.c_uint, _I64, _P, _P, _P, _P, _P, _P],
     "pg_touched_to_f32": [_P, _I64, _P, _P],
+    "pg_composite_fwd_f32": [_P, _P, _I64, _I, _P, _P, _P],
+    "pg_ray_samples_f32": [_P, _P, _I64, _I, _P, _P, _P],
+    "pg_nerf_train_f32": [_M, _P, _P, _P, _I64, _I, _P, _F, _P, _P, _P, _P, _P],
     "pg_touched_from_f32": [_P, _I64, _P, _P],
     "pg_train_fused_f32": [_G, _M, _P, _P, _I64, _P, _P, _P, _P, _F, ctypes.c_uint, _P, _P, _P,
                            _P, _P, _P, _P],

@@ -457,10 +457,11 @@ __global__ void train_dgrad_kernel(const T *__restrict__ delta, int64_t B, int f
     out[i] = acc;
 }
 
-template <typename T, typename ACC = T, typename LACC = double>
-int mlp_train_generic(const pg_mlp *m, const T *y, const T *targets, int64_t B, const T *params,
-                      T scale, unsigned flags, ACC *gparams, T *dy, LACC *loss_sum, T *ws,
-                      cudaStream_t s) {
+// forward layers -> loss(z_out, delta) -> backward layers; the loss stage
+// writes dL/d(output pre-activation) for all B rows into delta
+template <typename T, typename ACC, typename LossFn>
+int mlp_train_core(const pg_mlp *m, const T *y, int64_t B, const T *params, ACC *gparams, T *dy,
+                   T *ws, cudaStream_t s, LossFn loss) {
     if (int e = validate_mlp(m)) return e;
     if (B == 0) return PG_OK;
     PG_REQUIRE(ws != nullptr, "mlp_train needs workspace");
@@ -490,9 +491,7 @@ int mlp_train_generic(const pg_mlp *m, const T *y, const T *targets, int64_t B, 
             const T *a = l == 0 ? y : z[l - 1];
             train_linear_fwd_kernel<T><<<grid_for(B * fo, 256), 256, 0, s>>>(a, l > 0, B, fi, Wp[l], bp[l], fo, z[l]);
         }
-        const int od = m->widths[nl];
-        train_loss_kernel<T, LACC><<<grid_for(B * od, 256), 256, 0, s>>>(
-            z[nl - 1], targets, B * od, scale, (flags & PG_SIGMOID) ? 1 : 0, d0, loss_sum);
+        loss(z[nl - 1], d0);
         // backward
         T *dcur = d0, *dnext = d1;
         for (int l = nl - 1; l >= 0; --l) {
@@ -510,6 +509,135 @@ int mlp_train_generic(const pg_mlp *m, const T *y, const T *targets, int64_t B, 
         }
     }
     return check_launch("mlp_train");
+}
+
+template <typename T, typename ACC = T, typename LACC = double>
+int mlp_train_generic(const pg_mlp *m, const T *y, const T *targets, int64_t B, const T *params,
+                      T scale, unsigned flags, ACC *gparams, T *dy, LACC *loss_sum, T *ws,
+                      cudaStream_t s) {
+    const int od = m->widths[m->n_layers];
+    return mlp_train_core<T, ACC>(m, y, B, params, gparams, dy, ws, s, [&](const T *zout, T *delta) {
+        train_loss_kernel<T, LACC><<<grid_for(B * od, 256), 256, 0, s>>>(
+            zout, targets, B * od, scale, (flags & PG_SIGMOID) ? 1 : 0, delta, loss_sum);
+    });
+}
+
+// =========================================================================
+// Volume compositing head (beyond the reference, which has
+// no renderer): per ray, S samples of raw MLP outputs (sigma_raw, r, g, b),
+// density sigma = softplus(sigma_raw), colour c = logistic(rgb_raw),
+// alpha_i = 1 - exp(-sigma_i delta_i), T_i = prod_{j<i} (1 - alpha_j),
+// C = sum_i T_i alpha_i c_i.  One thread per ray, samples in order.
+// Backward (derivation in DESIGN.md 4): with w_i = T_i alpha_i and the
+// prefix C_<=i, dC/dc_i = w_i and dC/dsigma_i = delta_i (T_{i+1} c_i -
+// (C - C_<=i)).
+// =========================================================================
+// midpoint samples along each ray inside the unit cube (slab test); rays
+// that miss get zero-length segments at their clamped origin
+__global__ void ray_samples_kernel(const float *__restrict__ o, const float *__restrict__ dir, int64_t R,
+                                   int S, float *__restrict__ pts, float *__restrict__ deltas) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= R * S) return;
+    const int64_t r = i / S;
+    const int k = (int)(i - r * S);
+    float ov[3], dv[3], nr = 0.0f, fr = 3.4e38f;
+    for (int a = 0; a < 3; ++a) {
+        ov[a] = o[r * 3 + a];
+        dv[a] = dir[r * 3 + a];
+        const float inv = 1.0f / (fabsf(dv[a]) < 1e-12f ? 1e-12f : dv[a]);
+        const float t0 = (0.0f - ov[a]) * inv, t1 = (1.0f - ov[a]) * inv;
+        nr = fmaxf(nr, fminf(t0, t1));
+        fr = fminf(fr, fmaxf(t0, t1));
+    }
+    if (!(fr > nr)) nr = fr = 0.0f;
+    const float step = (fr - nr) / (float)S;
+    const float t = nr + ((float)k + 0.5f) * step;
+    for (int a = 0; a < 3; ++a) pts[i * 3 + a] = fminf(fmaxf(ov[a] + t * dv[a], 0.0f), 1.0f);
+    deltas[i] = step;
+}
+
+__device__ __forceinline__ float softplus_f(float x) { return x > 20.0f ? x : log1pf(expf(x)); }
+__device__ __forceinline__ float logistic_f(float x) { return 1.0f / (1.0f + expf(-x)); }
+
+__global__ void composite_fwd_kernel(const float *__restrict__ raw, const float *__restrict__ deltas,
+                                     int64_t R, int S, float *__restrict__ rgb, float *__restrict__ wts) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= R) return;
+    float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
+    for (int i = 0; i < S; ++i) {
+        const int64_t q = r * S + i;
+        const float4 v = *reinterpret_cast<const float4 *>(raw + q * 4);
+        const float tr = expf(-softplus_f(v.x) * deltas[q]);
+        const float w = T * (1.0f - tr);
+        c0 += w * logistic_f(v.y);
+        c1 += w * logistic_f(v.z);
+        c2 += w * logistic_f(v.w);
+        if (wts) wts[q] = w;
+        T *= tr;
+    }
+    rgb[r * 3 + 0] = c0;
+    rgb[r * 3 + 1] = c1;
+    rgb[r * 3 + 2] = c2;
+}
+
+// loss = sum over rays and channels of (C - target)^2 (fp64, into loss_sum);
+// delta (R*S, 4) = dL/d(raw) with dL/dC = scale * (C - target)
+template <typename LACC>
+__global__ void composite_loss_kernel(const float *__restrict__ raw, const float *__restrict__ deltas,
+                                      const float *__restrict__ target, int64_t R, int S, float scale,
+                                      float *__restrict__ draw, LACC *__restrict__ loss_sum) {
+    __shared__ double red[32];
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double sq = 0.0;
+    if (r < R) {
+        float T = 1.0f, C[3] = {0.0f, 0.0f, 0.0f};
+        for (int i = 0; i < S; ++i) {
+            const int64_t q = r * S + i;
+            const float4 v = *reinterpret_cast<const float4 *>(raw + q * 4);
+            const float tr = expf(-softplus_f(v.x) * deltas[q]);
+            const float w = T * (1.0f - tr);
+            C[0] += w * logistic_f(v.y);
+            C[1] += w * logistic_f(v.z);
+            C[2] += w * logistic_f(v.w);
+            T *= tr;
+        }
+        float gC[3];
+        for (int k = 0; k < 3; ++k) {
+            const float diff = C[k] - target[r * 3 + k];
+            sq += (double)diff * (double)diff;
+            gC[k] = diff * scale;
+        }
+        const float cg = C[0] * gC[0] + C[1] * gC[1] + C[2] * gC[2];
+        float Tc = 1.0f, pre = 0.0f;   // T_i and (C_<=i . gC)
+        for (int i = 0; i < S; ++i) {
+            const int64_t q = r * S + i;
+            const float4 v = *reinterpret_cast<const float4 *>(raw + q * 4);
+            const float dl = deltas[q];
+            const float tr = expf(-softplus_f(v.x) * dl);
+            const float w = Tc * (1.0f - tr);
+            const float l0 = logistic_f(v.y), l1 = logistic_f(v.z), l2 = logistic_f(v.w);
+            const float ci_g = l0 * gC[0] + l1 * gC[1] + l2 * gC[2];
+            pre += w * ci_g;
+            Tc *= tr;                                   // now T_{i+1}
+            const float dsig = dl * (Tc * ci_g - (cg - pre));
+            float4 d;
+            d.x = dsig * logistic_f(v.x);               // softplus' = logistic
+            d.y = w * gC[0] * l0 * (1.0f - l0);
+            d.z = w * gC[1] * l1 * (1.0f - l1);
+            d.w = w * gC[2] * l2 * (1.0f - l2);
+            *reinterpret_cast<float4 *>(draw + q * 4) = d;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0 && loss_sum) loss_add(loss_sum, v);
+    }
 }
 
 
@@ -682,6 +810,34 @@ int pg_mlp_train_det_f32(const pg_mlp *mlp, const float *y, const float *targets
     return mlp_train_generic<float, fx_t, fx_t>(mlp, y, targets, B, params, scale, flags,
                                                 (fx_t *)gparams_fx, dy, (fx_t *)loss_fx, ws,
                                                 as_stream(stream));
+}
+int pg_ray_samples_f32(const float *origins, const float *dirs, int64_t R, int S, float *pts,
+                       float *deltas, void *stream) {
+    PG_REQUIRE(R >= 0 && S >= 1, "ray_samples: R >= 0 and S >= 1");
+    if (R == 0) return PG_OK;
+    ray_samples_kernel<<<grid_for(R * S, 256), 256, 0, as_stream(stream)>>>(origins, dirs, R, S, pts, deltas);
+    return check_launch("ray_samples");
+}
+int pg_composite_fwd_f32(const float *raw, const float *deltas, int64_t R, int S, float *rgb,
+                         float *weights, void *stream) {
+    PG_REQUIRE(R >= 0 && S >= 1, "composite: R >= 0 and S >= 1");
+    PG_REQUIRE(R == 0 || (raw && deltas && rgb), "composite: null buffer");
+    if (R == 0) return PG_OK;
+    composite_fwd_kernel<<<grid_for(R, 128), 128, 0, as_stream(stream)>>>(raw, deltas, R, S, rgb, weights);
+    return check_launch("composite_fwd");
+}
+int pg_nerf_train_f32(const pg_mlp *mlp, const float *y, const float *deltas, const float *target_rgb,
+                      int64_t R, int S, const float *params, float scale, float *gparams, float *dy,
+                      double *loss_sum, float *ws, void *stream) {
+    PG_REQUIRE(R >= 0 && S >= 1, "nerf_train: R >= 0 and S >= 1");
+    PG_REQUIRE(mlp && mlp->n_layers >= 1 && mlp->widths[mlp->n_layers] == 4,
+               "nerf_train: the MLP must output (sigma, r, g, b)");
+    if (R == 0) return PG_OK;
+    cudaStream_t s = as_stream(stream);
+    return mlp_train_core<float, float>(mlp, y, R * S, params, gparams, dy, ws, s, [&](const float *zout, float *delta) {
+        composite_loss_kernel<double><<<grid_for(R, 128), 128, 0, s>>>(zout, deltas, target_rgb, R, S, scale,
+                                                                      delta, loss_sum);
+    });
 }
 int64_t pg_mlp_acts_floats(int64_t B, const pg_mlp *mlp) { return mlp_acts_floats(B, mlp); }
 int pg_mlp_wgrad_blas_f32(const pg_mlp *mlp, const float *acts, int64_t B, float *gparams, void *stream) {

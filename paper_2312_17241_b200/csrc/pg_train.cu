@@ -448,6 +448,13 @@ int train_fused(const pg_grid *g, const pg_mlp *m, const float *xs, const float 
     if (B == 0) return PG_OK;
     const int od = m->widths[3];
     const int sig = (flags & PG_SIGMOID) ? 1 : 0;
+    if (flags & PG_COMPOSITE) {
+        // one 64-sample tile = one ray of 64 samples (pg_train_mma.cu)
+        PG_REQUIRE(od == 4 && !sig && !(flags & PG_EXACT_MLP) && !acts && B % 64 == 0,
+                   "PG_COMPOSITE: out_dim 4, no sigmoid, tensor-core MLP, B a multiple of 64 samples");
+        return train_mma<ACC, LACC>(g, od, xs, targets, B, feats, baked, conf, params, scale, 2, gfeat, gconf,
+                                    touched, gparams, loss_sum, dy_out, s);
+    }
     // fast path: tensor-core MLP (pg_train_mma.cu); this file's FFMA kernel is
     // the OpenBLAS-order path (PG_EXACT_MLP, reference-order mode)
     if (!acts && !(flags & PG_EXACT_MLP))

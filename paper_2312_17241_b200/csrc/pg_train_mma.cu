@@ -138,12 +138,92 @@ __device__ __forceinline__ float row_sum4(const float *srcT, int r, int qq) {
 }
 }  // namespace tm
 
+// Volume compositing of one ray = one 64-sample tile (PG_COMPOSITE, the
+// NeRF-style head of SURVEY 8f row 4): S.d3[q*8 + 0..3] holds the raw MLP
+// outputs (sigma_raw, r, g, b) of sample q, S.tg[q*4] its segment length and
+// S.tg[1..3] the ray's target colour.  One warp: lane l owns samples 2l and
+// 2l+1; transmittance by a multiplicative warp scan, the colour by a warp
+// sum, the backward's "colour behind sample i" by an additive scan (same
+// equations as pg_mlp.cu composite_loss_kernel).  Overwrites S.d3 with
+// dL/d(raw); returns the ray's squared error (lane 0).
+__device__ __forceinline__ float tile_softplus(float x) { return x > 20.0f ? x : log1pf(expf(x)); }
+__device__ __forceinline__ float tile_logistic(float x) { return 1.0f / (1.0f + expf(-x)); }
+
+__device__ __forceinline__ double composite_tile(float *d3, const float *tg, float scale, int lane) {
+    float raw[2][4], tr[2], c[2][3], dl[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const int q = 2 * lane + u;
+        const float4 v = *reinterpret_cast<const float4 *>(d3 + q * 8);
+        raw[u][0] = v.x; raw[u][1] = v.y; raw[u][2] = v.z; raw[u][3] = v.w;
+        dl[u] = tg[q * 4];
+        tr[u] = expf(-tile_softplus(v.x) * dl[u]);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) c[u][k] = tile_logistic(raw[u][k + 1]);
+    }
+    // exclusive prefix product of the transmittances over the 64 samples
+    float p = tr[0] * tr[1], incl = p;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const float t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl *= t;
+    }
+    float T0 = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) T0 = 1.0f;
+    const float T[2] = {T0, T0 * tr[0]};
+    const float w[2] = {T[0] * (1.0f - tr[0]), T[1] * (1.0f - tr[1])};
+    float C[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        float v = w[0] * c[0][k] + w[1] * c[1][k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        C[k] = v;
+    }
+    double sq = 0.0;
+    float gC[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float diff = C[k] - tg[1 + k];
+        sq += (double)diff * (double)diff;
+        gC[k] = diff * scale;
+    }
+    const float cg = C[0] * gC[0] + C[1] * gC[1] + C[2] * gC[2];
+    float ci_g[2], v[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        ci_g[u] = c[u][0] * gC[0] + c[u][1] * gC[1] + c[u][2] * gC[2];
+        v[u] = w[u] * ci_g[u];
+    }
+    float s = v[0] + v[1];   // inclusive prefix sum over lanes
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const float t = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += t;
+    }
+    const float pre[2] = {s - v[1], s};             // prefix through samples 2l, 2l+1
+    const float Tn[2] = {T[1], T[1] * tr[1]};        // T_{i+1}
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const int q = 2 * lane + u;
+        const float dsig = dl[u] * (Tn[u] * ci_g[u] - (cg - pre[u]));
+        float4 d;
+        d.x = dsig * tile_logistic(raw[u][0]);
+        d.y = w[u] * gC[0] * c[u][0] * (1.0f - c[u][0]);
+        d.z = w[u] * gC[1] * c[u][1] * (1.0f - c[u][1]);
+        d.w = w[u] * gC[2] * c[u][2] * (1.0f - c[u][2]);
+        *reinterpret_cast<float4 *>(d3 + q * 8) = d;
+    }
+    return lane == 0 ? sq : 0.0;
+}
+
 template <typename FT, int D, int NPM, typename ACC, typename LACC>
 __global__ void __launch_bounds__(tm::kNT, 2)
     train_mma_kernel(const pg_grid g, const float *__restrict__ xs, const float *__restrict__ targets,
                      int64_t B, const FT *__restrict__ feats_fwd, const float *__restrict__ feats,
                      const uint8_t *__restrict__ baked, const float *__restrict__ conf,
-                     const float *__restrict__ params, int od, float scale, int sigmoid,
+                     const float *__restrict__ params, int od, float scale,
+                     int sigmoid,   // 1: logistic output; 2: volume compositing (one ray per tile)
                      ACC *__restrict__ gfeat, ACC *__restrict__ gconf, uint8_t *__restrict__ touched,
                      ACC *__restrict__ gparams, LACC *__restrict__ loss_sum, float *__restrict__ dy_out) {
     using namespace tm;
@@ -252,18 +332,24 @@ __global__ void __launch_bounds__(tm::kNT, 2)
             for (int e = 0; e < 4; ++e) {
                 const int q = 16 * warp + gq + (e >> 1) * 8, j = 2 * c + (e & 1);
                 float d = 0.0f;
-                if (j < od && q < nv) {
+                if (sigmoid == 2) {
+                    d = j < od ? acc[0][e] + S.b2[j] : 0.0f;   // raw output, composited below
+                } else if (j < od && q < nv) {
                     const float o = acc[0][e] + S.b2[j];
-                    const float pred = sigmoid ? 1.0f / (1.0f + expf(-o)) : o;
+                    const float pred = sigmoid == 1 ? 1.0f / (1.0f + expf(-o)) : o;
                     const float diff = pred - S.tg[q * kO + j];
                     lsum += (double)diff * (double)diff;
                     d = diff * scale;
-                    if (sigmoid) d *= pred * (1.0f - pred);
+                    if (sigmoid == 1) d *= pred * (1.0f - pred);
                 }
                 S.d3[q * 8 + j] = d;
             }
         }
         __syncthreads();
+        if (sigmoid == 2) {
+            if (warp == 0) lsum += composite_tile(S.d3, S.tg, scale, lane);
+            __syncthreads();
+        }
         PG_PH(4);
         // ---- dW2 += h2^T d3 (warps 0-3), db2; delta2 = (d3 W2^T) * (h2 > 0) ----
         if (warp < 4) {
