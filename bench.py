@@ -626,9 +626,19 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # code-path check of the multi-rank bench on a one-GPU box (NOT a
+    # measurement): PG_BENCH_SHARE_GPU=1 maps every rank to the visible GPUs
+    # round-robin and PG_BENCH_DIST_BACKEND=gloo replaces NCCL (which refuses
+    # two ranks on one device); the driver's N-GPU runs use neither
+    if os.environ.get("PG_BENCH_SHARE_GPU") == "1":
+        local_rank = local_rank % torch.cuda.device_count()
     if world > 1:
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("PG_BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     line, _ = run_gpu(args, rank, world, local_rank)
     if rank == 0:
         if not args.no_cpu_baseline and world == 1:
