@@ -357,7 +357,7 @@ def run_gpu(args, rank, world, local_rank):
         hd(hx, ho)
     el = max_over_ranks(time.perf_counter() - t0)
     e2e_qps = world * B_INFER * args.steps / el
-    e2e_launches = args.steps * math.ceil(B_INFER / hd.chunk)
+    e2e_launches = args.steps * (1 if hd.streaming else math.ceil(B_INFER / hd.chunk))
 
     # ---------------- training (C1, data parallel) ----------------
     train = run_train(args, pg, torch, dist, rank, world, dev, barrier, max_over_ranks, l2_stream)
@@ -383,7 +383,11 @@ def run_gpu(args, rank, world, local_rank):
                    "l2_policy": "inputs (128 MiB coords + 192 MiB outputs per GPU) larger than L2; tables L2-resident"},
         "e2e": {"value": e2e_qps, "unit": "queries/s", "h2d_bytes_per_step": B_INFER * 2 * 4,
                 "d2h_bytes_per_step": B_INFER * hyper.out_dim * 4,
-                "path": "pg_decode_host_f32 (pinned host in/out; H2D, kernel, D2H on 3 event-ordered streams; 2^21-query chunks, ramped)"},
+                "path": ("pg_decode_host_stream_f32 (pinned host in/out; ONE decode launch fed 2^18-query "
+                         "pieces by the copy engine through device flags, D2H of each piece on a stream wait "
+                         "for its tile counter; 3 streams)" if hd.streaming else
+                         "pg_decode_host_f32 (pinned host in/out; H2D, kernel, D2H on 3 event-ordered streams; "
+                         "2^21-query chunks, ramped)")},
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak,

@@ -224,6 +224,26 @@ int pg_decode_host_f32(const pg_grid *grid, const pg_mlp *mlp,
                        float *d_out, float *h_out, void *stream_in,
                        void *stream_compute, void *stream_out);
 
+/* Streaming end-to-end decode from HOST memory: one tcgen05 decode launch
+ * over the whole batch consumes `chunk`-query pieces as
+ * the copy engine lands them (flag written by the stream after each H2D
+ * copy), and the D2H copy of each piece starts as soon as the kernel has
+ * counted all of its tiles done (stream wait on a device counter).  chunk:
+ * a power of two >= 128.  d_xs
+ * holds B*d floats, d_out B*out_dim floats, d_flags 2*ceil(B/chunk) uint32.
+ * Needs the fused shape, the tensor-core MLP and stream memory operations:
+ * pg_decode_stream_supported() says whether this call can run.  The kernel
+ * traps (an error, not a hang) if a chunk does not arrive within 20 s. */
+int pg_decode_stream_supported(const pg_grid *grid, const pg_mlp *mlp,
+                               unsigned flags);
+int pg_decode_host_stream_f32(const pg_grid *grid, const pg_mlp *mlp,
+                              const float *h_xs, int64_t B, const void *feats,
+                              const uint8_t *baked, const float *params,
+                              unsigned flags, int64_t chunk, float *d_xs,
+                              float *d_out, uint32_t *d_flags, float *h_out,
+                              void *stream_in, void *stream_compute,
+                              void *stream_out);
+
 /* Training MLP pass (trainer.py:122-137 + mlp.py:55-85): forward, squared
  * error loss (sum in fp64 into *loss_sum), dpred = diff*scale, backward.
  * Accumulates parameter grads into gparams (same layout as params) and

@@ -190,4 +190,43 @@ struct LevelTab {
 
 int validate_grid(const pg_grid *g);
 
+// Streaming decode (pg_decode_host_stream_f32): one kernel over the whole
+// batch consumes chunks as the copy engine lands them.  ready[c] is written
+// non-zero (cuStreamWriteValue32) after chunk c's H2D copy; the kernel bumps
+// done[c] once per finished tile, and the D2H stream waits (cuStreamWaitValue32
+// GEQ) for done[c] == tiles of chunk c.  Null pointers: ordinary launch.
+struct DecodeStream {
+    const uint32_t *ready = nullptr;
+    uint32_t *done = nullptr;
+    int chunk_tiles_log2 = 0;   // chunks are 2^k tiles of 128 queries
+    uint64_t timeout_ns = 0;
+};
+
+// poll a flag written by the stream front end after a copy; traps (a launch
+// error, not a hang) if it does not arrive within timeout_ns.  Relaxed
+// polling: an acquire would invalidate L1 (the tables' cache) on every
+// check; the data behind the flag is then read with L2-coherent ld.cg loads
+// issued after the flag was observed (control dependency + group barrier).
+__device__ __forceinline__ void wait_flag(const uint32_t *f, uint64_t timeout_ns) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    if (v) return;
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        __nanosleep(128);
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if (v) return;
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > timeout_ns) __trap();
+    }
+}
+
+// count n finished tiles; the caller has fenced every thread's output
+// stores (gpu scope: the copy engine reads through L2) and synchronised
+__device__ __forceinline__ void signal_done(uint32_t *f, uint32_t n) {
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(f), "r"(n) : "memory");
+}
+
 }  // namespace pg

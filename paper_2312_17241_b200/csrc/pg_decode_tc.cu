@@ -47,6 +47,8 @@ struct Group {
     alignas(128) float opA[2 * kTP * 32];
     float xs[kTP * 3];
     uint64_t mbar[3];
+    int seen;            // streaming: chunk of the group's current tile
+    uint32_t pending;    // streaming: finished tiles of chunk `seen` not yet counted
 };
 template <int NG>
 struct Smem {
@@ -66,6 +68,9 @@ struct TabPlan {
     int32_t pbits;               // packed bits per baked index; 0 when N_p == 1
     int32_t bytes;
 };
+using Stream = DecodeStream;
+using pg::wait_flag;
+using pg::signal_done;
 }  // namespace tc
 
 template <typename FT> struct FeatS;
@@ -177,11 +182,12 @@ __device__ __forceinline__ void group_sync(int grp) {
     asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(tc::kGT) : "memory");
 }
 
-template <typename FT, int D, int NG, int MINB>
+template <typename FT, int D, int NG, int MINB, bool STREAM>
 __global__ void __launch_bounds__(tc::kGT *NG, MINB)
     decode_umma_kernel(const pg_grid g, const tc::TabPlan plan, const float *__restrict__ xs, int64_t B,
                         const FT *__restrict__ feats, const uint8_t *__restrict__ baked,
-                        const float *__restrict__ params, int od, int sigmoid, float *__restrict__ out) {
+                        const float *__restrict__ params, int od, int sigmoid, float *__restrict__ out,
+                        tc::Stream st) {
     using namespace tc;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     constexpr int kThreads = kGT * NG, kGroups = NG;
@@ -244,6 +250,10 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
             }
         }
     }
+    if (STREAM && tid < kGroups) {
+        S.grp[tid].seen = -1;
+        S.grp[tid].pending = 0;
+    }
     if ((tid >> 5) == 0) umma::tmem_alloc<(NG == 1 ? 128 : NG == 2 ? 256 : 512)>(&S.tmem_base);
     if (tid == 0) {
         for (int gi = 0; gi < kGroups; ++gi)
@@ -274,7 +284,26 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
          tile += (int64_t)gridDim.x * kGroups, phase ^= 1u) {
         const int64_t p0 = tile * kTP;
         const int nv = (int)((B - p0) < kTP ? (B - p0) : kTP);
-        for (int i = gt; i < kTP * D; i += kGT) G.xs[i] = i < nv * D ? xs[p0 * D + i] : 0.5f;
+        if (STREAM && (int)(tile >> st.chunk_tiles_log2) != G.seen) {
+            // streaming, entering a new chunk: publish the finished tiles of
+            // the previous one (fence each thread's output stores, then one
+            // counter add per group and chunk), then wait for this chunk's
+            // inputs to land.  The bookkeeping lives in shared memory: the
+            // 3-pipeline variant is at its register cap.
+            __threadfence();
+            group_sync(grp);
+            if (gt == 0) {
+                if (G.pending) tc::signal_done(st.done + G.seen, G.pending);
+                G.pending = 0;
+                G.seen = (int)(tile >> st.chunk_tiles_log2);
+                tc::wait_flag(st.ready + G.seen, st.timeout_ns);
+            }
+            group_sync(grp);
+        }
+        // streaming: L2-coherent loads (the copy engine writes xs while the
+        // kernel runs, so the non-coherent path must not be used)
+        for (int i = gt; i < kTP * D; i += kGT)
+            G.xs[i] = i < nv * D ? (STREAM ? __ldcg(xs + p0 * D + i) : xs[p0 * D + i]) : 0.5f;
         group_sync(grp);
         // ---------------- encode -> layer-1 A operand (hi | lo) ----------------
         {
@@ -392,6 +421,12 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
                 dst[i] = o;
             }
         }
+        if (STREAM && gt == 0) ++G.pending;
+    }
+    if (STREAM) {
+        __threadfence();
+        group_sync(grp);
+        if (gt == 0 && G.pending) tc::signal_done(st.done + G.seen, G.pending);
     }
     umma::fence_after_sync();
     __syncthreads();
@@ -428,25 +463,26 @@ static tc::TabPlan plan_tables(const pg_grid *g, size_t feat_bytes, int budget, 
     return p;
 }
 
-template <typename FT, int D, int NG, int MINB>
+template <typename FT, int D, int NG, int MINB, bool STREAM>
 static void launch_umma(const pg_grid *g, const tc::TabPlan &plan, int smem, int grd, const float *xs,
                          int64_t B, const void *feats, const uint8_t *baked, const float *params, int od,
-                         int sig, float *out, cudaStream_t s) {
+                         int sig, float *out, const tc::Stream &st, cudaStream_t s) {
     static bool configured = false;
     if (!configured) {
         int dev = 0, optin = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        cudaFuncSetAttribute(decode_umma_kernel<FT, D, NG, MINB>,
+        cudaFuncSetAttribute(decode_umma_kernel<FT, D, NG, MINB, STREAM>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
         configured = true;
     }
-    decode_umma_kernel<FT, D, NG, MINB><<<grd, tc::kGT * NG, smem, s>>>(*g, plan, xs, B, (const FT *)feats,
-                                                                           baked, params, od, sig, out);
+    decode_umma_kernel<FT, D, NG, MINB, STREAM><<<grd, tc::kGT * NG, smem, s>>>(*g, plan, xs, B, (const FT *)feats,
+                                                                           baked, params, od, sig, out, st);
 }
 
 int decode_umma(const pg_grid *g, int od, const float *xs, int64_t B, const void *feats, bool half,
-                const uint8_t *baked, const float *params, int sig, int table_flags, float *out, cudaStream_t s) {
+                const uint8_t *baked, const float *params, int sig, int table_flags, float *out, cudaStream_t s,
+                const tc::Stream &st) {
     static int sms = 0, optin = 0, env_budget = -1, env_kinds = 2;
     if (!sms) {
         int dev = 0;
@@ -480,13 +516,22 @@ int decode_umma(const pg_grid *g, int od, const float *xs, int64_t B, const void
     const int64_t want = (ntiles + ng - 1) / ng;
     const int64_t cap = (int64_t)sms * per_sm;
     const int grd = (int)(want < cap ? want : cap);
-#define PG_DEC_TC2(FT_, D_)                                                                        \
-    (ng == 3 ? launch_umma<FT_, D_, 3, 1>(g, plan, smem, grd, xs, B, feats, baked, params, od, sig, out, s) \
-             : launch_umma<FT_, D_, 1, 3>(g, plan, smem, grd, xs, B, feats, baked, params, od, sig, out, s))
+    // streaming (pg_decode_host_stream_f32) is its own instantiation, so the
+    // ordinary kernel carries none of its registers; fp16 tables only (the
+    // inference model's storage)
+    const bool stream = st.ready != nullptr;
+    PG_REQUIRE(!stream || half, "streaming decode runs on fp16 tables");
+#define PG_DEC_TC2(FT_, D_, S_)                                                                       \
+    (ng == 3 ? launch_umma<FT_, D_, 3, 1, S_>(g, plan, smem, grd, xs, B, feats, baked, params, od, sig, out, st, s) \
+             : launch_umma<FT_, D_, 1, 3, S_>(g, plan, smem, grd, xs, B, feats, baked, params, od, sig, out, st, s))
     if (half) {
-        if (g->d == 2) PG_DEC_TC2(__half, 2); else PG_DEC_TC2(__half, 3);
+        if (stream) {
+            if (g->d == 2) PG_DEC_TC2(__half, 2, true); else PG_DEC_TC2(__half, 3, true);
+        } else {
+            if (g->d == 2) PG_DEC_TC2(__half, 2, false); else PG_DEC_TC2(__half, 3, false);
+        }
     } else {
-        if (g->d == 2) PG_DEC_TC2(float, 2); else PG_DEC_TC2(float, 3);
+        if (g->d == 2) PG_DEC_TC2(float, 2, false); else PG_DEC_TC2(float, 3, false);
     }
 #undef PG_DEC_TC2
     return check_launch("decode_umma");

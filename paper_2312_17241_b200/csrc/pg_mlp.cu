@@ -3,6 +3,8 @@
 //    the training pass for shapes the fused kernels do not cover);
 //  * the fused decode kernel: all-level encode + [32,64,64,<=4] MLP per
 //    128-query tile, activations resident in shared memory.
+#include <cuda.h>
+
 #include "pg_encode_dev.cuh"
 
 namespace pg {
@@ -327,7 +329,8 @@ static void launch_decode(const pg_grid *g, const float *xs, int64_t B, const vo
 }
 
 int decode_umma(const pg_grid *g, int od, const float *xs, int64_t B, const void *feats, bool half,
-                const uint8_t *baked, const float *params, int sig, int table_flags, float *out, cudaStream_t s);
+                const uint8_t *baked, const float *params, int sig, int table_flags, float *out, cudaStream_t s,
+                const DecodeStream &st = DecodeStream());
 
 int decode_device(const pg_grid *g, const pg_mlp *m, const float *xs, int64_t B,
                   const void *feats, const uint8_t *baked, const float *params, unsigned flags,
@@ -794,6 +797,112 @@ int pg_decode_host_f32(const pg_grid *grid, const pg_mlp *mlp, const float *h_xs
     }
     if (err) return err;
     return check_launch("decode_host");
+}
+
+// Streaming end-to-end decode: ONE tcgen05 decode launch over the whole
+// batch, fed chunk by chunk by the copy engine (see DecodeStream): removes
+// the per-launch prologue (weights, shared-memory tables, TMEM) and tail
+// that chunked launches pay (~35 us each), and lets the first tiles start
+// as soon as the first chunk lands.
+typedef CUresult (*pg_write_value_fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*pg_wait_value_fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static pg_write_value_fn g_write_value = nullptr;
+static pg_wait_value_fn g_wait_value = nullptr;
+static bool stream_memops() {
+    // stream memory operations (CUDA >= 12: always available; the v1
+    // capability attribute is deprecated), resolved through the runtime's
+    // driver entry-point query so the library needs no link against libcuda
+    static int state = 0;   // 0 unknown, 1 ok, -1 unavailable
+    if (state == 0) {
+        cudaDriverEntryPointQueryResult q1 = cudaDriverEntryPointSymbolNotFound, q2 = q1;
+        cudaGetDriverEntryPoint("cuStreamWriteValue32", (void **)&g_write_value, cudaEnableDefault, &q1);
+        cudaGetDriverEntryPoint("cuStreamWaitValue32", (void **)&g_wait_value, cudaEnableDefault, &q2);
+        state = (q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess && g_write_value &&
+                 g_wait_value)
+                    ? 1
+                    : -1;
+        if (getenv("PG_DEBUG_MEMOPS"))
+            fprintf(stderr, "pg: stream memops q1=%d q2=%d write=%p wait=%p\n", (int)q1, (int)q2,
+                    (void *)g_write_value, (void *)g_wait_value);
+        cudaGetLastError();
+    }
+    return state == 1;
+}
+
+int pg_decode_stream_supported(const pg_grid *grid, const pg_mlp *mlp, unsigned flags) {
+    return grid && mlp && decode_fast_ok(grid, mlp) && !(flags & (PG_EXACT_MLP | PG_NO_TENSOR)) && stream_memops();
+}
+
+int pg_decode_host_stream_f32(const pg_grid *grid, const pg_mlp *mlp, const float *h_xs, int64_t B,
+                              const void *feats, const uint8_t *baked, const float *params, unsigned flags,
+                              int64_t chunk, float *d_xs, float *d_out, uint32_t *d_flags, float *h_out,
+                              void *stream_in, void *stream_compute, void *stream_out) {
+    if (int e = validate_grid(grid)) return e;
+    if (int e = validate_mlp(mlp)) return e;
+    PG_REQUIRE(pg_decode_stream_supported(grid, mlp, flags),
+               "streaming decode needs the tcgen05 [32,64,64,<=4] path and stream memory operations");
+    PG_REQUIRE(chunk >= 128 && (chunk & (chunk - 1)) == 0, "chunk must be a power of two >= 128 queries");
+    PG_REQUIRE(B >= 0 && (B == 0 || (h_xs && d_xs && d_out && d_flags && h_out)), "null buffer");
+    if (B == 0) return PG_OK;
+    const int d = grid->d, od = mlp->widths[3];
+    const int64_t nch = (B + chunk - 1) / chunk;
+    cudaStream_t si = as_stream(stream_in), sk = as_stream(stream_compute), so = as_stream(stream_out);
+    uint32_t *ready = d_flags, *done = d_flags + nch;
+    cudaEvent_t ev0;
+    cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
+    const bool dbg_nocopy = getenv("PG_DEBUG_STREAM_NOCOPY") != nullptr;   // kernel-only probe
+    cudaMemsetAsync(d_flags, 0, sizeof(uint32_t) * 2 * nch, sk);
+    if (dbg_nocopy) cudaMemsetAsync(d_flags, 1, sizeof(uint32_t) * nch, sk);
+    cudaEventRecord(ev0, sk);
+    cudaStreamWaitEvent(si, ev0, 0);
+    cudaStreamWaitEvent(so, ev0, 0);
+    DecodeStream st;
+    st.ready = ready;
+    st.done = done;
+    while ((128ll << st.chunk_tiles_log2) < chunk) ++st.chunk_tiles_log2;
+    st.timeout_ns = 20ull * 1000 * 1000 * 1000;
+    const bool half = (flags & PG_HALF_FEATS) != 0;
+    static const bool dbg = getenv("PG_DEBUG_STREAM") != nullptr;
+    cudaEvent_t dk0 = nullptr, dk1 = nullptr, dend = nullptr;
+    if (dbg) {
+        cudaEventCreate(&dk0);
+        cudaEventCreate(&dk1);
+        cudaEventCreate(&dend);
+        cudaEventRecord(dk0, sk);
+    }
+    int err = decode_umma(grid, od, d_xs, B, feats, half, baked, params, (flags & PG_SIGMOID) ? 1 : 0,
+                          (int)(flags & (PG_SMEM_TABLES | PG_NO_SMEM_TABLES)), d_out, sk, st);
+    if (dbg) cudaEventRecord(dk1, sk);
+    for (int64_t c = 0; c < nch && !err && !dbg_nocopy; ++c) {
+        const int64_t off = c * chunk, n = B - off < chunk ? B - off : chunk;
+        cudaMemcpyAsync(d_xs + off * d, h_xs + off * d, sizeof(float) * n * d, cudaMemcpyHostToDevice, si);
+        CUresult r1 = g_write_value((CUstream)si, (CUdeviceptr)(ready + c), 1u, 0);
+        CUresult r2 = g_wait_value((CUstream)so, (CUdeviceptr)(done + c), (cuuint32_t)((n + 127) / 128),
+                                   CU_STREAM_WAIT_VALUE_GEQ);
+        if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS) {
+            // cannot feed the running kernel: it would time out; report instead
+            set_error("stream memory operation failed (" + std::to_string((int)r1) + ", " +
+                      std::to_string((int)r2) + ")");
+            err = PG_ERR_CUDA;
+        }
+        cudaMemcpyAsync(h_out + off * od, d_out + off * od, sizeof(float) * n * od, cudaMemcpyDeviceToHost, so);
+    }
+    if (dbg) cudaEventRecord(dend, so);
+    cudaStreamSynchronize(si);
+    cudaStreamSynchronize(sk);
+    cudaStreamSynchronize(so);
+    cudaEventDestroy(ev0);
+    if (dbg) {
+        float k = 0, t = 0;
+        cudaEventElapsedTime(&k, dk0, dk1);
+        cudaEventElapsedTime(&t, dk0, dend);
+        fprintf(stderr, "pg stream decode: kernel %.3f ms, kernel start -> last D2H %.3f ms\n", k, t);
+        cudaEventDestroy(dk0);
+        cudaEventDestroy(dk1);
+        cudaEventDestroy(dend);
+    }
+    if (err) return err;
+    return check_launch("decode_host_stream");
 }
 
 int64_t pg_mlp_train_workspace_floats(int64_t B, const pg_mlp *mlp) { return mlp_train_ws(B, mlp); }

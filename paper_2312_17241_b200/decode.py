@@ -188,28 +188,63 @@ def decode_image(inf: InferenceModel, width: int | None = None,
 
 
 class HostDecoder:
-    """End-to-end decode from pinned host memory through the C ABI's
-    pg_decode_host_f32: H2D copies, fused kernels and D2H copies of
-    successive chunks on three streams (two buffer slots, event-ordered) so
-    both transfer directions overlap compute."""
+    """End-to-end decode from pinned host memory through the C ABI.
 
-    def __init__(self, inf: InferenceModel, chunk: int = 1 << 21, exact: bool = False):
+    Streaming mode (default when the device supports stream memory
+    operations and the tensor-core path applies): pg_decode_host_stream_f32
+    — ONE decode launch over the whole batch, fed `stream_chunk`-query pieces
+    by the copy engine and draining its outputs piece by piece, so H2D, the
+    kernel and D2H overlap without per-chunk launch costs.  Needs device
+    buffers for the whole batch (20 B/query for 2-D, 3 outputs).
+    Chunked mode (stream=False, or the exact / FFMA engines):
+    pg_decode_host_f32 — successive chunks on three streams, two buffer
+    slots, event-ordered."""
+
+    def __init__(self, inf: InferenceModel, chunk: int = 1 << 21, exact: bool = False,
+                 stream: bool | None = None, stream_chunk: int = 1 << 18):
         if not inf.fast:
             raise ValueError("host decode needs the fused [32,64,64,<=4] shape")
-        self.inf, self.chunk, self.exact = inf, chunk, exact
+        if stream_chunk < 128 or stream_chunk & (stream_chunk - 1):
+            raise ValueError("stream_chunk must be a power of two >= 128")
+        self.inf, self.chunk, self.exact, self.stream_chunk = inf, chunk, exact, stream_chunk
         d, od = inf.hyper.d, inf.out_dim
-        self.d_xs = torch.empty(2 * chunk * d, dtype=torch.float32, device=inf.device)
-        self.d_out = torch.empty(2 * chunk * od, dtype=torch.float32, device=inf.device)
+        ok = bool(_lib.lib().pg_decode_stream_supported(inf.grid, inf.mlp_desc, _flags(inf, exact)))
+        if stream and not ok:
+            raise ValueError("streaming host decode is not available for this model / device")
+        self.streaming = ok if stream is None else bool(stream)
         self.s_in = torch.cuda.Stream(device=inf.device)
         self.s_k = torch.cuda.Stream(device=inf.device)
         self.s_out = torch.cuda.Stream(device=inf.device)
+        self._cap = 0
+        if not self.streaming:
+            self.d_xs = torch.empty(2 * chunk * d, dtype=torch.float32, device=inf.device)
+            self.d_out = torch.empty(2 * chunk * od, dtype=torch.float32, device=inf.device)
+
+    def _reserve(self, B: int) -> None:
+        if B <= self._cap:
+            return
+        inf = self.inf
+        self.d_xs = torch.empty(B * inf.hyper.d, dtype=torch.float32, device=inf.device)
+        self.d_out = torch.empty(B * inf.out_dim, dtype=torch.float32, device=inf.device)
+        n = -(-B // self.stream_chunk)
+        self.d_flags = torch.empty(2 * n, dtype=torch.int32, device=inf.device)
+        self._cap = B
 
     def __call__(self, h_xs: torch.Tensor, h_out: torch.Tensor) -> torch.Tensor:
         inf = self.inf
         assert h_xs.is_pinned() and h_out.is_pinned(), "host buffers must be pinned"
+        streams = (_lib.ctypes.c_void_p(self.s_in.cuda_stream), _lib.ctypes.c_void_p(self.s_k.cuda_stream),
+                   _lib.ctypes.c_void_p(self.s_out.cuda_stream))
+        if self.streaming:
+            B = h_xs.shape[0]
+            self._reserve(B)
+            _lib.call("pg_decode_host_stream_f32", inf.grid, inf.mlp_desc, _lib.ptr(h_xs), B,
+                      _lib.ptr(inf.feats16), _lib.ptr(inf.baked), _lib.ptr(inf.params),
+                      _flags(inf, self.exact), self.stream_chunk, _lib.ptr(self.d_xs), _lib.ptr(self.d_out),
+                      _lib.ptr(self.d_flags), _lib.ptr(h_out), *streams)
+            return h_out
         _lib.call("pg_decode_host_f32", inf.grid, inf.mlp_desc, _lib.ptr(h_xs), h_xs.shape[0],
                   _lib.ptr(inf.feats16), _lib.ptr(inf.baked), _lib.ptr(inf.params),
                   _flags(inf, self.exact), self.chunk, _lib.ptr(self.d_xs), _lib.ptr(self.d_out),
-                  _lib.ptr(h_out), _lib.ctypes.c_void_p(self.s_in.cuda_stream),
-                  _lib.ctypes.c_void_p(self.s_k.cuda_stream), _lib.ctypes.c_void_p(self.s_out.cuda_stream))
+                  _lib.ptr(h_out), *streams)
         return h_out

@@ -583,17 +583,24 @@ def test_decode_smem_tables_bit_identical(n_p, d):
     np.testing.assert_allclose(b[:20000], ref, rtol=1e-5, atol=1e-6)
 
 
-def test_host_decoder_matches_device():
+@pytest.mark.parametrize("stream", [False, True])
+def test_host_decoder_matches_device(stream):
+    """End-to-end host decode (chunked launches, or ONE streaming launch fed
+    chunk by chunk through device flags) equals the device decode bit for
+    bit, for batches below one chunk, ragged and multi-chunk, and on reuse
+    of the same decoder (flags re-armed per call)."""
     import paper_2312_17241_b200 as pg
     from paper_2312_17241_b200.decode import HostDecoder, decode_device
     m, _ = _trained_pair(1)
     inf = pg.to_inference(m)
-    n = (1 << 20) + 12345
-    hx = torch.rand((n, 2), generator=torch.Generator().manual_seed(0)).pin_memory()
-    ho = torch.empty((n, 3)).pin_memory()
-    HostDecoder(inf, chunk=1 << 18)(hx, ho)
-    dev = decode_device(inf, hx.cuda(), exact=False).cpu()
-    eq(ho.numpy(), dev.numpy())
+    hd = HostDecoder(inf, chunk=1 << 18, stream=stream, stream_chunk=1 << 16)
+    assert hd.streaming == stream
+    for n in ((1 << 20) + 12345, 1, 1000, 1 << 16, (1 << 18) + 128):
+        hx = torch.rand((n, 2), generator=torch.Generator().manual_seed(n)).pin_memory()
+        ho = torch.full((n, 3), float("nan")).pin_memory()
+        hd(hx, ho)
+        dev = decode_device(inf, hx.cuda(), exact=False).cpu()
+        eq(ho.numpy(), dev.numpy())
 
 
 def test_decode_generic_shape_matches_oracle():
