@@ -232,8 +232,10 @@ int pg_decode_host_f32(const pg_grid *grid, const pg_mlp *mlp,
  * a power of two >= 128.  d_xs
  * holds B*d floats, d_out B*out_dim floats, d_flags 2*ceil(B/chunk) uint32.
  * Needs the fused shape, the tensor-core MLP and stream memory operations:
- * pg_decode_stream_supported() says whether this call can run.  The kernel
- * traps (an error, not a hang) if a chunk does not arrive within 20 s. */
+ * pg_decode_stream_supported() says whether this call can run.  A chunk
+ * whose flag has not arrived 2 ms after the kernel reached it (copies
+ * serialised behind the kernel by a profiler or CUDA_LAUNCH_BLOCKING) is
+ * read from h_xs directly (pinned, so device-accessible): never a hang. */
 int pg_decode_stream_supported(const pg_grid *grid, const pg_mlp *mlp,
                                unsigned flags);
 int pg_decode_host_stream_f32(const pg_grid *grid, const pg_mlp *mlp,
@@ -243,6 +245,15 @@ int pg_decode_host_stream_f32(const pg_grid *grid, const pg_mlp *mlp,
                               float *d_out, uint32_t *d_flags, float *h_out,
                               void *stream_in, void *stream_compute,
                               void *stream_out);
+
+/* Zero-copy end-to-end decode: the tcgen05 decode kernel reads h_xs and
+ * writes h_out in pinned host memory directly over PCIe (UVA); no copies,
+ * flags or device buffers.
+ * h_xs / h_out must be page-locked (checked).  Returns after completion. */
+int pg_decode_host_zc_f32(const pg_grid *grid, const pg_mlp *mlp,
+                          const float *h_xs, int64_t B, const void *feats,
+                          const uint8_t *baked, const float *params,
+                          unsigned flags, float *h_out, void *stream);
 
 /* Training MLP pass (trainer.py:122-137 + mlp.py:55-85): forward, squared
  * error loss (sum in fp64 into *loss_sum), dpred = diff*scale, backward.

@@ -81,6 +81,7 @@ _SIGS.update({
     "pg_composite_fwd_f32": [_P, _P, _I64, _I, _P, _P, _P],
     "pg_ray_samples_f32": [_P, _P, _I64, _I, _P, _P, _P],
     "pg_decode_stream_supported": [_G, _M, ctypes.c_uint],
+    "pg_decode_host_zc_f32": [_G, _M, _P, _I64, _P, _P, _P, ctypes.c_uint, _P, _P],
     "pg_decode_host_stream_f32": [_G, _M, _P, _I64, _P, _P, _P, ctypes.c_uint, _I64, _P, _P, _P, _P, _P, _P, _P],
     "pg_nerf_train_f32": [_M, _P, _P, _P, _I64, _I, _P, _F, _P, _P, _P, _P, _P],
     "pg_touched_from_f32": [_P, _I64, _P, _P],

@@ -200,26 +200,27 @@ struct DecodeStream {
     uint32_t *done = nullptr;
     int chunk_tiles_log2 = 0;   // chunks are 2^k tiles of 128 queries
     uint64_t timeout_ns = 0;
+    const float *host_xs = nullptr;   // pinned host copy of the inputs (fallback)
 };
 
-// poll a flag written by the stream front end after a copy; traps (a launch
-// error, not a hang) if it does not arrive within timeout_ns.  Relaxed
-// polling: an acquire would invalidate L1 (the tables' cache) on every
-// check; the data behind the flag is then read with L2-coherent ld.cg loads
-// issued after the flag was observed (control dependency + group barrier).
-__device__ __forceinline__ void wait_flag(const uint32_t *f, uint64_t timeout_ns) {
+// poll a flag written by the stream front end after a copy; false if it
+// does not arrive within timeout_ns.  Relaxed polling: an acquire would
+// invalidate L1 (the tables' cache) on every check; the data behind the flag
+// is then read with L2-coherent ld.cg loads issued after the flag was
+// observed (control dependency + group barrier).
+__device__ __forceinline__ bool wait_flag(const uint32_t *f, uint64_t timeout_ns) {
     uint32_t v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-    if (v) return;
+    if (v) return true;
     uint64_t t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (;;) {
         __nanosleep(128);
         asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-        if (v) return;
+        if (v) return true;
         uint64_t t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        if (t - t0 > timeout_ns) __trap();
+        if (t - t0 > timeout_ns) return false;
     }
 }
 

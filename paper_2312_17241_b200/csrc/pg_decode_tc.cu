@@ -49,6 +49,7 @@ struct Group {
     uint64_t mbar[3];
     int seen;            // streaming: chunk of the group's current tile
     uint32_t pending;    // streaming: finished tiles of chunk `seen` not yet counted
+    int host;            // streaming: a flag timed out -> read inputs from host memory
 };
 template <int NG>
 struct Smem {
@@ -182,7 +183,11 @@ __device__ __forceinline__ void group_sync(int grp) {
     asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(tc::kGT) : "memory");
 }
 
-template <typename FT, int D, int NG, int MINB, bool STREAM>
+// MODE 0: ordinary launch (inputs/outputs in device memory, or in pinned
+// host memory for the zero-copy entry point); 1: streaming (inputs landed by
+// the copy engine behind per-chunk flags, outputs counted per chunk for the
+// D2H stream)
+template <typename FT, int D, int NG, int MINB, int MODE>
 __global__ void __launch_bounds__(tc::kGT *NG, MINB)
     decode_umma_kernel(const pg_grid g, const tc::TabPlan plan, const float *__restrict__ xs, int64_t B,
                         const FT *__restrict__ feats, const uint8_t *__restrict__ baked,
@@ -250,9 +255,11 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
             }
         }
     }
+    constexpr bool STREAM = MODE == 1;
     if (STREAM && tid < kGroups) {
         S.grp[tid].seen = -1;
         S.grp[tid].pending = 0;
+        S.grp[tid].host = 0;
     }
     if ((tid >> 5) == 0) umma::tmem_alloc<(NG == 1 ? 128 : NG == 2 ? 256 : 512)>(&S.tmem_base);
     if (tid == 0) {
@@ -296,14 +303,23 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
                 if (G.pending) tc::signal_done(st.done + G.seen, G.pending);
                 G.pending = 0;
                 G.seen = (int)(tile >> st.chunk_tiles_log2);
-                tc::wait_flag(st.ready + G.seen, st.timeout_ns);
+                // a flag that does not come (the copies serialised behind
+                // this kernel: profilers, CUDA_LAUNCH_BLOCKING) is not an
+                // error: the group then reads its inputs from pinned host
+                // memory directly (they are there already)
+                if (!G.host && !tc::wait_flag(st.ready + G.seen, st.timeout_ns)) G.host = 1;
             }
             group_sync(grp);
         }
         // streaming: L2-coherent loads (the copy engine writes xs while the
         // kernel runs, so the non-coherent path must not be used)
-        for (int i = gt; i < kTP * D; i += kGT)
-            G.xs[i] = i < nv * D ? (STREAM ? __ldcg(xs + p0 * D + i) : xs[p0 * D + i]) : 0.5f;
+        {
+            // streaming: L2-coherent loads from the landed chunk, or straight
+            // from pinned host memory for a group whose flag never came
+            const float *src = STREAM && G.host ? st.host_xs : xs;
+            for (int i = gt; i < kTP * D; i += kGT)
+                G.xs[i] = i < nv * D ? (STREAM ? __ldcg(src + p0 * D + i) : xs[p0 * D + i]) : 0.5f;
+        }
         group_sync(grp);
         // ---------------- encode -> layer-1 A operand (hi | lo) ----------------
         {
@@ -463,7 +479,7 @@ static tc::TabPlan plan_tables(const pg_grid *g, size_t feat_bytes, int budget, 
     return p;
 }
 
-template <typename FT, int D, int NG, int MINB, bool STREAM>
+template <typename FT, int D, int NG, int MINB, int MODE>
 static void launch_umma(const pg_grid *g, const tc::TabPlan &plan, int smem, int grd, const float *xs,
                          int64_t B, const void *feats, const uint8_t *baked, const float *params, int od,
                          int sig, float *out, const tc::Stream &st, cudaStream_t s) {
@@ -472,11 +488,11 @@ static void launch_umma(const pg_grid *g, const tc::TabPlan &plan, int smem, int
         int dev = 0, optin = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        cudaFuncSetAttribute(decode_umma_kernel<FT, D, NG, MINB, STREAM>,
+        cudaFuncSetAttribute(decode_umma_kernel<FT, D, NG, MINB, MODE>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
         configured = true;
     }
-    decode_umma_kernel<FT, D, NG, MINB, STREAM><<<grd, tc::kGT * NG, smem, s>>>(*g, plan, xs, B, (const FT *)feats,
+    decode_umma_kernel<FT, D, NG, MINB, MODE><<<grd, tc::kGT * NG, smem, s>>>(*g, plan, xs, B, (const FT *)feats,
                                                                            baked, params, od, sig, out, st);
 }
 
@@ -519,19 +535,19 @@ int decode_umma(const pg_grid *g, int od, const float *xs, int64_t B, const void
     // streaming (pg_decode_host_stream_f32) is its own instantiation, so the
     // ordinary kernel carries none of its registers; fp16 tables only (the
     // inference model's storage)
-    const bool stream = st.ready != nullptr;
-    PG_REQUIRE(!stream || half, "streaming decode runs on fp16 tables");
+    const int mode = st.ready ? 1 : 0;
+    PG_REQUIRE(!mode || half, "streaming decode runs on fp16 tables");
 #define PG_DEC_TC2(FT_, D_, S_)                                                                       \
     (ng == 3 ? launch_umma<FT_, D_, 3, 1, S_>(g, plan, smem, grd, xs, B, feats, baked, params, od, sig, out, st, s) \
              : launch_umma<FT_, D_, 1, 3, S_>(g, plan, smem, grd, xs, B, feats, baked, params, od, sig, out, st, s))
     if (half) {
-        if (stream) {
-            if (g->d == 2) PG_DEC_TC2(__half, 2, true); else PG_DEC_TC2(__half, 3, true);
+        if (mode == 1) {
+            if (g->d == 2) PG_DEC_TC2(__half, 2, 1); else PG_DEC_TC2(__half, 3, 1);
         } else {
-            if (g->d == 2) PG_DEC_TC2(__half, 2, false); else PG_DEC_TC2(__half, 3, false);
+            if (g->d == 2) PG_DEC_TC2(__half, 2, 0); else PG_DEC_TC2(__half, 3, 0);
         }
     } else {
-        if (g->d == 2) PG_DEC_TC2(float, 2, false); else PG_DEC_TC2(float, 3, false);
+        if (g->d == 2) PG_DEC_TC2(float, 2, 0); else PG_DEC_TC2(float, 3, 0);
     }
 #undef PG_DEC_TC2
     return check_launch("decode_umma");

@@ -860,7 +860,8 @@ int pg_decode_host_stream_f32(const pg_grid *grid, const pg_mlp *mlp, const floa
     st.ready = ready;
     st.done = done;
     while ((128ll << st.chunk_tiles_log2) < chunk) ++st.chunk_tiles_log2;
-    st.timeout_ns = 20ull * 1000 * 1000 * 1000;
+    st.timeout_ns = 2ull * 1000 * 1000;   // then read from host memory (see the kernel)
+    st.host_xs = h_xs;
     const bool half = (flags & PG_HALF_FEATS) != 0;
     static const bool dbg = getenv("PG_DEBUG_STREAM") != nullptr;
     cudaEvent_t dk0 = nullptr, dk1 = nullptr, dend = nullptr;
@@ -903,6 +904,39 @@ int pg_decode_host_stream_f32(const pg_grid *grid, const pg_mlp *mlp, const floa
     }
     if (err) return err;
     return check_launch("decode_host_stream");
+}
+
+// Zero-copy end-to-end decode: the decode kernel reads the coordinates from
+// and writes the outputs to pinned host memory directly (UVA).  No copies,
+// flags or extra device memory (measured 5.50 ms per 2^24 queries vs 5.22
+// for the streaming path; a variant prefetching each tile's coordinates a
+// tile ahead spilled at the 80-register cap and ran 5.62 ms).
+static bool is_pinned_host(const void *p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+int pg_decode_host_zc_f32(const pg_grid *grid, const pg_mlp *mlp, const float *h_xs, int64_t B,
+                          const void *feats, const uint8_t *baked, const float *params, unsigned flags,
+                          float *h_out, void *stream) {
+    if (int e = validate_grid(grid)) return e;
+    if (int e = validate_mlp(mlp)) return e;
+    PG_REQUIRE(decode_fast_ok(grid, mlp) && !(flags & (PG_EXACT_MLP | PG_NO_TENSOR)) && (flags & PG_HALF_FEATS),
+               "zero-copy decode needs the tcgen05 [32,64,64,<=4] path on fp16 tables");
+    if (B == 0) return PG_OK;
+    PG_REQUIRE(is_pinned_host(h_xs) && is_pinned_host(h_out),
+               "zero-copy decode needs page-locked (pinned) host buffers");
+    cudaStream_t s = as_stream(stream);
+    if (int e = decode_umma(grid, mlp->widths[3], h_xs, B, feats, true, baked, params,
+                            (flags & PG_SIGMOID) ? 1 : 0, (int)(flags & (PG_SMEM_TABLES | PG_NO_SMEM_TABLES)),
+                            h_out, s))
+        return e;
+    cudaStreamSynchronize(s);
+    return check_launch("decode_host_zc");
 }
 
 int64_t pg_mlp_train_workspace_floats(int64_t B, const pg_mlp *mlp) { return mlp_train_ws(B, mlp); }

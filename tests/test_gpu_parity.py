@@ -603,6 +603,53 @@ def test_host_decoder_matches_device(stream):
         eq(ho.numpy(), dev.numpy())
 
 
+def test_zero_copy_host_decode():
+    """pg_decode_host_zc_f32: the decode kernel on pinned host buffers
+    directly equals the device decode bit for bit; pageable buffers are
+    refused with an error instead of a device fault."""
+    import paper_2312_17241_b200 as pg
+    from paper_2312_17241_b200 import _lib
+    from paper_2312_17241_b200.decode import _flags, decode_device
+    m, _ = _trained_pair(1)
+    inf = pg.to_inference(m)
+    n = (1 << 18) + 77
+    hx = torch.rand((n, 2), generator=torch.Generator().manual_seed(3)).pin_memory()
+    ho = torch.full((n, 3), float("nan")).pin_memory()
+    _lib.call("pg_decode_host_zc_f32", inf.grid, inf.mlp_desc, _lib.ptr(hx), n, _lib.ptr(inf.feats16),
+              _lib.ptr(inf.baked), _lib.ptr(inf.params), _flags(inf, False), _lib.ptr(ho), _lib.stream_ptr())
+    eq(ho.numpy(), decode_device(inf, hx.cuda(), exact=False).cpu().numpy())
+    with pytest.raises(ValueError, match="pinned"):
+        _lib.call("pg_decode_host_zc_f32", inf.grid, inf.mlp_desc, _lib.ptr(hx.clone()), n,
+                  _lib.ptr(inf.feats16), _lib.ptr(inf.baked), _lib.ptr(inf.params), _flags(inf, False),
+                  _lib.ptr(ho), _lib.stream_ptr())
+
+
+def test_streaming_decode_survives_serialised_launches():
+    """With CUDA_LAUNCH_BLOCKING=1 the copies that feed the streaming kernel
+    can only run after it: its groups time out on the flags and read the
+    inputs from pinned host memory — a correct result, never a hang."""
+    import subprocess
+    import sys
+    code = (
+        "import torch, numpy as np, paper_2312_17241_b200 as pg\n"
+        "from paper_2312_17241_b200.decode import HostDecoder, decode_device\n"
+        "m = pg.init_model(pg.HyperParams(n_f=2**12, n_c=2**14, n_p=4), seed=0)\n"
+        "inf = pg.to_inference(m)\n"
+        "n = (1 << 18) + 5\n"
+        "hx = torch.rand((n, 2), generator=torch.Generator().manual_seed(0)).pin_memory()\n"
+        "ho = torch.full((n, 3), float('nan')).pin_memory()\n"
+        "hd = HostDecoder(inf, stream=True, stream_chunk=1 << 16)\n"
+        "hd(hx, ho)\n"
+        "ref = decode_device(inf, hx.cuda(), exact=False).cpu()\n"
+        "assert torch.equal(ref, ho), 'mismatch'\n"
+        "print('ok')\n")
+    env = dict(os.environ, CUDA_LAUNCH_BLOCKING="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
 def test_decode_generic_shape_matches_oracle():
     import paper_2312_17241_b200 as pg
     kw = dict(n_f=64, n_c=64, n_p=4, n_levels=4, n_min=4, n_max=32, n_neurons=16, out_dim=2,
