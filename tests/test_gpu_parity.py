@@ -603,6 +603,27 @@ def test_host_decoder_matches_device(stream):
         eq(ho.numpy(), dev.numpy())
 
 
+@pytest.mark.parametrize("kw", [dict(d=3, n_f=2**12, n_c=2**12, n_p=4, out_dim=1),
+                                dict(d=3, n_f=2**10, n_c=2**10, n_p=8, out_dim=4, out_sigmoid=True),
+                                dict(n_f=2**14, n_c=2**14, n_p=2, out_dim=3, out_sigmoid=True),
+                                dict(n_f=2**12, n_c=2**14, n_p=1, out_dim=2)])
+def test_streaming_host_decode_shapes(kw):
+    """Streaming host decode across dimensions, probing ranges (smem-table
+    and global-baked variants), output widths and the logistic head: equal
+    to the device decode bit for bit."""
+    import paper_2312_17241_b200 as pg
+    from paper_2312_17241_b200.decode import HostDecoder, decode_device
+    m = pg.init_model(pg.HyperParams(**kw), seed=1)
+    inf = pg.to_inference(m)
+    d = inf.hyper.d
+    n = 3 * (1 << 16) + 1000
+    hx = torch.rand((n, d), generator=torch.Generator().manual_seed(7)).pin_memory()
+    ho = torch.full((n, inf.out_dim), float("nan")).pin_memory()
+    hd = HostDecoder(inf, stream=True, stream_chunk=1 << 16)
+    hd(hx, ho)
+    eq(ho.numpy(), decode_device(inf, hx.cuda(), exact=False).cpu().numpy())
+
+
 def test_zero_copy_host_decode():
     """pg_decode_host_zc_f32: the decode kernel on pinned host buffers
     directly equals the device decode bit for bit; pageable buffers are
