@@ -363,9 +363,12 @@ def run_gpu(args, rank, world, local_rank):
     train = run_train(args, pg, torch, dist, rank, world, dev, barrier, max_over_ranks, l2_stream)
     extra = {}
     if not args.quick:
-        extra["train_c3"] = run_train_field(args, pg, torch, dist, rank, world, barrier, max_over_ranks, "c3")
-        extra["train_c4"] = run_train_field(args, pg, torch, dist, rank, world, barrier, max_over_ranks, "c4")
-        extra["train_c4_nerf"] = run_train_nerf(args, pg, torch, dist, rank, world, barrier, max_over_ranks)
+        extra["train_c3"] = run_train_field(args, pg, torch, dist, rank, world, barrier, max_over_ranks, "c3",
+                                            l2_stream)
+        extra["train_c4"] = run_train_field(args, pg, torch, dist, rank, world, barrier, max_over_ranks, "c4",
+                                            l2_stream)
+        extra["train_c4_nerf"] = run_train_nerf(args, pg, torch, dist, rank, world, barrier, max_over_ranks,
+                                                l2_stream)
         if world == 1:
             extra["sweep_inference_c2_c5"] = run_sweep(args, pg, torch, decode_device)
 
@@ -493,7 +496,7 @@ def field_points(kind, n, seed):
     return x, v
 
 
-def run_train_field(args, pg, torch, dist, rank, world, barrier, max_over_ranks, kind):
+def run_train_field(args, pg, torch, dist, rank, world, barrier, max_over_ranks, kind, l2_stream=None):
     """C3 (3-D SDF, 2^22 points/step) or C4 (NeRF-style, N_p=8, out 4, 2^18
     samples/step) training step; data parallel under torchrun."""
     if kind == "c3":
@@ -520,10 +523,11 @@ def run_train_field(args, pg, torch, dist, rank, world, barrier, max_over_ranks,
                        "samples_per_gpu_per_step": B, "mlp": hyper.mlp_widths(),
                        "probed_levels": len(model.probed), "parallelism": f"dp{world}"},
             "encode_bytes_per_sample": bps, "encode_algorithmic_gbs": B * bps / (ms * 1e-3) / 1e9,
+            "encode_frac_of_l2_stream": (B * bps / (ms * 1e-3) / 1e9 / l2_stream) if l2_stream else None,
             "last_loss": st.loss_value()}
 
 
-def run_train_nerf(args, pg, torch, dist, rank, world, barrier, max_over_ranks):
+def run_train_nerf(args, pg, torch, dist, rank, world, barrier, max_over_ranks, l2_stream=None):
     """C4 with the volume-compositing head: 2^12 rays x 64
     samples per GPU per step (2^18 samples), C4 encoding (N_p=8, out 4);
     targets rendered from an analytic field (soft ball of density, colour =
@@ -547,8 +551,12 @@ def run_train_nerf(args, pg, torch, dist, rank, world, barrier, max_over_ranks):
     steps = max(3, args.steps // 4)
     ms = _time_steps(torch, dp.launch_step if dp else st.launch_step, steps, args.warmup, barrier,
                      max_over_ranks)
+    bps = train_bytes_per_sample(hyper, len(model.probed))
+    gbs = R * S * bps / (ms * 1e-3) / 1e9
     return {"metric": "train rays/s", "value": world * R / (ms * 1e-3), "unit": "rays/s",
             "samples_per_s": world * R * S / (ms * 1e-3), "ms_per_step": ms, "steps": steps,
+            "encode_bytes_per_sample": bps, "encode_algorithmic_gbs": gbs,
+            "encode_frac_of_l2_stream": gbs / l2_stream if l2_stream else None,
             "config": {"workload": "C4 NeRF-style step with volume compositing", **hk,
                        "rays_per_gpu_per_step": R, "samples_per_ray": S, "mlp": hyper.mlp_widths(),
                        "probed_levels": len(model.probed), "parallelism": f"dp{world}",
