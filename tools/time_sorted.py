@@ -8,6 +8,13 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+if len(sys.argv) > 1:   # A/B: the library at argv[1]
+    import ctypes
+    from paper_2312_17241_b200 import _lib
+    _raw = ctypes.CDLL(sys.argv[1])
+    _lib._SIGS = {k: v for k, v in _lib._SIGS.items() if hasattr(_raw, k)}
+    _lib._LIB = _lib.load(sys.argv[1])
+    print("lib", sys.argv[1])
 import paper_2312_17241_b200 as pg  # noqa: E402
 from tests.golden_util import smooth_image  # noqa: E402
 
