@@ -33,11 +33,13 @@ constexpr int kS = 72;    // row stride (floats) of [feature][sample] tiles and 
                           // 72 = 8 mod 32 makes the A/B fragment loads of the
                           // feature-indexed GEMMs bank-conflict free
 
-struct Smem {
+struct SmemW {            // weights: shared by the tile pipelines of a CTA
     float w0[kI * kS];    // W0 [in f][out i]
     float w1[kH * kS];    // W1 [in i][out j]
     float w2[kH * 8];     // W2 [in k][out j], columns >= od zero
     float b0[kH], b1[kH], b2[8];
+};
+struct SmemG {            // one tile pipeline's activations
     float y[kI * kS];     // y^T [f][q] of the current tile, then of the next
     float dy[kI * kS];    // dL/dy^T [f][q]
     float h1[kH * kS];    // relu(z1)^T [i][q], later delta1^T
@@ -46,8 +48,14 @@ struct Smem {
     float xs[kT * 3];
     float tg[kT * kO];
     double lred[kNT / 32];
+};
+template <int NG>
+struct SmemT {
+    SmemW w;
+    SmemG g[NG];
     uint32_t tmem_base;
 };
+using Smem = SmemT<1>;
 
 // per-thread weight-gradient accumulators live in TMEM between tiles (28
 // columns per warp: dW1 fragment 16, dW0 8, dW2 4), leaving the registers to
@@ -139,12 +147,12 @@ __device__ __forceinline__ float row_sum4(const float *srcT, int r, int qq) {
 }  // namespace tm
 
 // Volume compositing of one ray = one 64-sample tile (PG_COMPOSITE, the
-// NeRF-style head of SURVEY 8f row 4): S.d3[q*8 + 0..3] holds the raw MLP
-// outputs (sigma_raw, r, g, b) of sample q, S.tg[q*4] its segment length and
-// S.tg[1..3] the ray's target colour.  One warp: lane l owns samples 2l and
+// NeRF-style head of SURVEY 8f row 4): G.d3[q*8 + 0..3] holds the raw MLP
+// outputs (sigma_raw, r, g, b) of sample q, G.tg[q*4] its segment length and
+// G.tg[1..3] the ray's target colour.  One warp: lane l owns samples 2l and
 // 2l+1; transmittance by a multiplicative warp scan, the colour by a warp
 // sum, the backward's "colour behind sample i" by an additive scan (same
-// equations as pg_mlp.cu composite_loss_kernel).  Overwrites S.d3 with
+// equations as pg_mlp.cu composite_loss_kernel).  Overwrites G.d3 with
 // dL/d(raw); returns the ray's squared error (lane 0).
 __device__ __forceinline__ float tile_softplus(float x) { return x > 20.0f ? x : log1pf(expf(x)); }
 __device__ __forceinline__ float tile_logistic(float x) { return 1.0f / (1.0f + expf(-x)); }
@@ -217,8 +225,13 @@ __device__ __forceinline__ double composite_tile(float *d3, const float *tg, flo
     return lane == 0 ? sq : 0.0;
 }
 
-template <typename FT, int D, int NPM, typename ACC, typename LACC>
-__global__ void __launch_bounds__(tm::kNT, 2)
+// NG = 1: one 8-warp tile pipeline per CTA, two CTAs per SM.  NG = 2: one
+// CTA per SM running two 8-warp pipelines that share the weights and are
+// held in anti-phase by a CTA-wide barrier at every phase switch, so one
+// pipeline's MLP (shared memory + tensor pipe) always runs beside the
+// other's table gathers/scatters (L1/L2).
+template <typename FT, int D, int NPM, typename ACC, typename LACC, int NG>
+__global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
     train_mma_kernel(const pg_grid g, const float *__restrict__ xs, const float *__restrict__ targets,
                      int64_t B, const FT *__restrict__ feats_fwd, const float *__restrict__ feats,
                      const uint8_t *__restrict__ baked, const float *__restrict__ conf,
@@ -228,33 +241,48 @@ __global__ void __launch_bounds__(tm::kNT, 2)
                      ACC *__restrict__ gparams, LACC *__restrict__ loss_sum, float *__restrict__ dy_out) {
     using namespace tm;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    Smem &S = *reinterpret_cast<Smem *>(smem_raw);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    SmemT<NG> &S = *reinterpret_cast<SmemT<NG> *>(smem_raw);
+    const int gid = NG == 1 ? 0 : (int)(threadIdx.x >> 8);   // tile pipeline
+    const int tid = threadIdx.x & (kNT - 1), warp = tid >> 5, lane = tid & 31;
+    SmemW &W = S.w;
+    SmemG &G = S.g[gid];
+    // barrier of this pipeline's 256 threads / of the whole CTA
+    auto gsync = [&]() {
+        if constexpr (NG == 1) __syncthreads();
+        else asm volatile("bar.sync %0, %1;" ::"r"(1 + gid), "r"(kNT) : "memory");
+    };
+    auto xsync = [&]() {
+#ifndef PG_X_NOXSYNC
+        if constexpr (NG > 1) __syncthreads();
+#endif
+    };
     {
         const float *p = params;
-        for (int i = tid; i < kI * kH; i += kNT) S.w0[(i / kH) * kS + i % kH] = p[i];
+        const int nt = kNT * NG, t0 = threadIdx.x;
+        for (int i = t0; i < kI * kH; i += nt) W.w0[(i / kH) * kS + i % kH] = p[i];
         p += kI * kH;
-        for (int i = tid; i < kH; i += kNT) S.b0[i] = p[i];
+        for (int i = t0; i < kH; i += nt) W.b0[i] = p[i];
         p += kH;
-        for (int i = tid; i < kH * kH; i += kNT) S.w1[(i / kH) * kS + i % kH] = p[i];
+        for (int i = t0; i < kH * kH; i += nt) W.w1[(i / kH) * kS + i % kH] = p[i];
         p += kH * kH;
-        for (int i = tid; i < kH; i += kNT) S.b1[i] = p[i];
+        for (int i = t0; i < kH; i += nt) W.b1[i] = p[i];
         p += kH;
-        for (int i = tid; i < kH * 8; i += kNT) {
+        for (int i = t0; i < kH * 8; i += nt) {
             const int k = i / 8, j = i % 8;
-            S.w2[i] = j < od ? p[k * od + j] : 0.0f;
+            W.w2[i] = j < od ? p[k * od + j] : 0.0f;
         }
         p += kH * od;
-        for (int i = tid; i < 8; i += kNT) S.b2[i] = i < od ? p[i] : 0.0f;
+        for (int i = t0; i < 8; i += nt) W.b2[i] = i < od ? p[i] : 0.0f;
     }
     // weight-gradient fragments (dW1 rows i = 16*(warp&3).., columns j =
     // 32*(warp>>2)..; dW0 rows f = 16*(warp&1).., columns i = 16*(warp>>1)..;
     // dW2 rows k = 16*warp (warps 0-3), columns j < 8), parked in TMEM
-    if (warp == 0) umma::tmem_alloc<64>(&S.tmem_base);
+    if (threadIdx.x < 32) umma::tmem_alloc<64 * NG>(&S.tmem_base);
     umma::fence_before_sync();
     __syncthreads();
     umma::fence_after_sync();
-    const uint32_t tm = S.tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 32);
+    const uint32_t tm = S.tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 32) +
+                        (uint32_t)(64 * gid);
     {
         const float z16[16] = {}, z8[8] = {}, z4[4] = {};
         umma::tmem_st16(tm, z16);
@@ -278,131 +306,144 @@ __global__ void __launch_bounds__(tm::kNT, 2)
     const int pl = tid & (kT - 1), lsub = tid >> 6;
     const int mt = warp & 3;           // 16-sample m-tile of the sample-major GEMMs
     const int rr = tid >> 2, qq = tid & 3;  // bias row-sum role
+    // tiles of this pipeline: first, first + stride, ...; every pipeline of
+    // a CTA runs as many iterations as its first one (the most), so the
+    // CTA-wide phase barriers match up
+    const int64_t first = (int64_t)blockIdx.x * NG + gid, stride = (int64_t)gridDim.x * NG;
+    const int64_t base0 = (int64_t)blockIdx.x * NG;
+    const int64_t n_iter = base0 < ntiles ? (ntiles - base0 + stride - 1) / stride : 0;
+    if (gid == 1) xsync();   // pipeline 1 starts one phase behind pipeline 0
     // prologue: the first tile's inputs and encode forward
     float x[D];
-    fetch(blockIdx.x, pf_x, pf_t);
-    if (tid < kT * D) S.xs[tid] = pf_x;
-    S.tg[tid] = pf_t;
-    fetch(blockIdx.x + gridDim.x, pf_x, pf_t);
-    __syncthreads();
+    fetch(first, pf_x, pf_t);
+    if (tid < kT * D) G.xs[tid] = pf_x;
+    G.tg[tid] = pf_t;
+    fetch(first + stride, pf_x, pf_t);
+    gsync();
 #pragma unroll
-    for (int a = 0; a < D; ++a) x[a] = S.xs[pl * D + a];
-    if (blockIdx.x < ntiles) {
+    for (int a = 0; a < D; ++a) x[a] = G.xs[pl * D + a];
+    if (first < ntiles) {
 #pragma unroll 2
         for (int it = 0; it < 4; ++it) {
             const int l = lsub + 4 * it;
             const float2 yv = encode_level_fwd2<FT, D>(g, l, x, feats_fwd, baked);
-            S.y[(2 * l) * kS + pl] = yv.x;
-            S.y[(2 * l + 1) * kS + pl] = yv.y;
+            G.y[(2 * l) * kS + pl] = yv.x;
+            G.y[(2 * l + 1) * kS + pl] = yv.y;
         }
     }
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int64_t iter = 0; iter < n_iter; ++iter) {
+        const int64_t tile = first + iter * stride;
+        xsync();   // phase switch: MLP here, the other pipeline's encode there
+        if (tile >= ntiles) {   // (only pipeline 1's last iteration) keep the barriers
+            xsync();
+            continue;
+        }
         const int64_t p0 = tile * kT;
         const int nv = (int)((B - p0) < kT ? (B - p0) : kT);
-        __syncthreads();
+        gsync();
         PG_PH(1);
         // ---- layer 1: h1 = relu(y W0 + b0) ----
         {
             float acc[4][4] = {};
-            warp_gemm<4, kI>(acc, S.y, 1, kS, 16 * mt, S.w0, kS, 1, 32 * (warp >> 2));
-            store_frags_T<4>(S.h1, acc, 16 * mt, 32 * (warp >> 2), [&](float v, int n, int) {
-                const float z = v + S.b0[n];
+            warp_gemm<4, kI>(acc, G.y, 1, kS, 16 * mt, W.w0, kS, 1, 32 * (warp >> 2));
+            store_frags_T<4>(G.h1, acc, 16 * mt, 32 * (warp >> 2), [&](float v, int n, int) {
+                const float z = v + W.b0[n];
                 return z > 0.0f ? z : 0.0f;
             });
         }
-        __syncthreads();
+        gsync();
         PG_PH(2);
         // ---- layer 2: h2 = relu(h1 W1 + b1) ----
         {
             float acc[4][4] = {};
-            warp_gemm<4, kH>(acc, S.h1, 1, kS, 16 * mt, S.w1, kS, 1, 32 * (warp >> 2));
-            store_frags_T<4>(S.h2, acc, 16 * mt, 32 * (warp >> 2), [&](float v, int n, int) {
-                const float z = v + S.b1[n];
+            warp_gemm<4, kH>(acc, G.h1, 1, kS, 16 * mt, W.w1, kS, 1, 32 * (warp >> 2));
+            store_frags_T<4>(G.h2, acc, 16 * mt, 32 * (warp >> 2), [&](float v, int n, int) {
+                const float z = v + W.b1[n];
                 return z > 0.0f ? z : 0.0f;
             });
         }
-        __syncthreads();
+        gsync();
         PG_PH(3);
         // ---- output layer, loss, dL/dout (warps 0-3: one 16-sample tile each) ----
         if (warp < 4) {
             float acc[1][4] = {};
-            warp_gemm<1, kH>(acc, S.h2, 1, kS, 16 * warp, S.w2, 8, 1, 0);
+            warp_gemm<1, kH>(acc, G.h2, 1, kS, 16 * warp, W.w2, 8, 1, 0);
             const int gq = lane >> 2, c = lane & 3;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int q = 16 * warp + gq + (e >> 1) * 8, j = 2 * c + (e & 1);
                 float d = 0.0f;
                 if (sigmoid == 2) {
-                    d = j < od ? acc[0][e] + S.b2[j] : 0.0f;   // raw output, composited below
+                    d = j < od ? acc[0][e] + W.b2[j] : 0.0f;   // raw output, composited below
                 } else if (j < od && q < nv) {
-                    const float o = acc[0][e] + S.b2[j];
+                    const float o = acc[0][e] + W.b2[j];
                     const float pred = sigmoid == 1 ? 1.0f / (1.0f + expf(-o)) : o;
-                    const float diff = pred - S.tg[q * kO + j];
+                    const float diff = pred - G.tg[q * kO + j];
                     lsum += (double)diff * (double)diff;
                     d = diff * scale;
                     if (sigmoid == 1) d *= pred * (1.0f - pred);
                 }
-                S.d3[q * 8 + j] = d;
+                G.d3[q * 8 + j] = d;
             }
         }
-        __syncthreads();
+        gsync();
         if (sigmoid == 2) {
-            if (warp == 0) lsum += composite_tile(S.d3, S.tg, scale, lane);
-            __syncthreads();
+            if (warp == 0) lsum += composite_tile(G.d3, G.tg, scale, lane);
+            gsync();
         }
         PG_PH(4);
         // ---- dW2 += h2^T d3 (warps 0-3), db2; delta2 = (d3 W2^T) * (h2 > 0) ----
         if (warp < 4) {
             float t2[1][4] = {};
-            warp_gemm<1, kT>(t2, S.h2, kS, 1, 16 * warp, S.d3, 8, 1, 0);
+            warp_gemm<1, kT>(t2, G.h2, kS, 1, 16 * warp, G.d3, 8, 1, 0);
             tmem_accumulate<4>(tm + 24, &t2[0][0]);
         }
         if (tid < 8) {
             float s = 0.0f;
-            for (int q = 0; q < kT; ++q) s += S.d3[q * 8 + tid];
+            for (int q = 0; q < kT; ++q) s += G.d3[q * 8 + tid];
             gb2 += s;
         }
         {
             // thread (sample q = tid & 63, 16 hidden units k = 16*(tid>>6)..)
             const int q = tid & (kT - 1), k0 = 16 * (tid >> 6);
-            const float4 dq = *reinterpret_cast<const float4 *>(S.d3 + q * 8);
+            const float4 dq = *reinterpret_cast<const float4 *>(G.d3 + q * 8);
             float dl[16];
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
                 const int k = k0 + u;
-                const float4 w = *reinterpret_cast<const float4 *>(S.w2 + k * 8);
+                const float4 w = *reinterpret_cast<const float4 *>(W.w2 + k * 8);
                 const float s = dq.x * w.x + dq.y * w.y + dq.z * w.z + dq.w * w.w;
-                dl[u] = S.h2[k * kS + q] > 0.0f ? s : 0.0f;
+                dl[u] = G.h2[k * kS + q] > 0.0f ? s : 0.0f;
             }
-            __syncthreads();  // dW2 reads h2 above
+            gsync();  // dW2 reads h2 above
             PG_PH(5);
 #pragma unroll
-            for (int u = 0; u < 16; ++u) S.h2[(k0 + u) * kS + q] = dl[u];
+            for (int u = 0; u < 16; ++u) G.h2[(k0 + u) * kS + q] = dl[u];
         }
-        __syncthreads();
+        gsync();
         PG_PH(6);
         {
-            const float s = row_sum4(S.h2, rr, qq);
+            const float s = row_sum4(G.h2, rr, qq);
             if (qq == 0) gb1 += s;
         }
         // ---- dW1 += h1^T delta2 ; delta1' = delta2 W1^T (kept in registers) ----
         float dacc[4][4] = {};
         {
             float t1[4][4] = {};
-            warp_gemm<4, kT>(t1, S.h1, kS, 1, 16 * (warp & 3), S.h2, 1, kS, 32 * (warp >> 2));
+            warp_gemm<4, kT>(t1, G.h1, kS, 1, 16 * (warp & 3), G.h2, 1, kS, 32 * (warp >> 2));
             tmem_accumulate<16>(tm, &t1[0][0]);
         }
-        warp_gemm<4, kH>(dacc, S.h2, 1, kS, 16 * mt, S.w1, 1, kS, 32 * (warp >> 2));
-        __syncthreads();
+        warp_gemm<4, kH>(dacc, G.h2, 1, kS, 16 * mt, W.w1, 1, kS, 32 * (warp >> 2));
+        gsync();
         PG_PH(7);
         // delta1 = delta1' * (h1 > 0), in place over h1
-        store_frags_T<4>(S.h1, dacc, 16 * mt, 32 * (warp >> 2), [&](float v, int n, int m) {
-            return S.h1[n * kS + m] > 0.0f ? v : 0.0f;
+        store_frags_T<4>(G.h1, dacc, 16 * mt, 32 * (warp >> 2), [&](float v, int n, int m) {
+            return G.h1[n * kS + m] > 0.0f ? v : 0.0f;
         });
-        __syncthreads();
+        gsync();
         PG_PH(8);
         {
-            const float s = row_sum4(S.h1, rr, qq);
+            const float s = row_sum4(G.h1, rr, qq);
             if (qq == 0) gb0 += s;
         }
         // ---- dW0 += y^T delta1 ; dy = delta1 W0^T ----
@@ -410,31 +451,32 @@ __global__ void __launch_bounds__(tm::kNT, 2)
             float yacc[2][4] = {};
             {
                 float t0[2][4] = {};
-                warp_gemm<2, kT>(t0, S.y, kS, 1, 16 * (warp & 1), S.h1, 1, kS, 16 * (warp >> 1));
+                warp_gemm<2, kT>(t0, G.y, kS, 1, 16 * (warp & 1), G.h1, 1, kS, 16 * (warp >> 1));
                 tmem_accumulate<8>(tm + 16, &t0[0][0]);
             }
-            warp_gemm<2, kH>(yacc, S.h1, 1, kS, 16 * mt, S.w0, 1, kS, 16 * (warp >> 2));
+            warp_gemm<2, kH>(yacc, G.h1, 1, kS, 16 * mt, W.w0, 1, kS, 16 * (warp >> 2));
             PG_PH(9);
-            store_frags_T<2>(S.dy, yacc, 16 * mt, 16 * (warp >> 2), [](float v, int, int) { return v; });
+            store_frags_T<2>(G.dy, yacc, 16 * mt, 16 * (warp >> 2), [](float v, int, int) { return v; });
         }
-        __syncthreads();   // dy complete; y, xs, tg free for the next tile
+        gsync();   // dy complete; y, xs, tg free for the next tile
         PG_PH(10);
         if (dy_out) {
             for (int i = tid; i < nv * kI; i += kNT) {
                 const int q = i / kI, c = i % kI;
-                dy_out[(p0 + q) * kI + c] = S.dy[c * kS + q];
+                dy_out[(p0 + q) * kI + c] = G.dy[c * kS + q];
             }
         }
         // ---- stage the next tile's inputs (prefetched into registers) ----
-        const int64_t nxt = tile + gridDim.x;
-        if (tid < kT * D) S.xs[tid] = pf_x;
-        S.tg[tid] = pf_t;
-        fetch(nxt + gridDim.x, pf_x, pf_t);
-        __syncthreads();
+        const int64_t nxt = tile + stride;
+        if (tid < kT * D) G.xs[tid] = pf_x;
+        G.tg[tid] = pf_t;
+        fetch(nxt + stride, pf_x, pf_t);
+        gsync();
+        xsync();   // phase switch: encode here, the other pipeline's MLP there
         PG_PH(0);
         float xn[D];
 #pragma unroll
-        for (int a = 0; a < D; ++a) xn[a] = S.xs[pl * D + a];
+        for (int a = 0; a < D; ++a) xn[a] = G.xs[pl * D + a];
         // ---- encode backward of this tile fused with encode forward of the
         //      next: both use the (sample, level) thread mapping, so one loop
         //      keeps both tiles' L2 round trips in flight together ----
@@ -444,17 +486,18 @@ __global__ void __launch_bounds__(tm::kNT, 2)
             const int l = lsub + 4 * it;
             if (has_next) {
                 const float2 yv = encode_level_fwd2<FT, D>(g, l, xn, feats_fwd, baked);
-                S.y[(2 * l) * kS + pl] = yv.x;
-                S.y[(2 * l + 1) * kS + pl] = yv.y;
+                G.y[(2 * l) * kS + pl] = yv.x;
+                G.y[(2 * l + 1) * kS + pl] = yv.y;
             }
             if (pl < nv)
-                encode_level_bwd2<D, NPM, ACC, std::is_same<ACC, float>::value>(g, l, x, S.dy[(2 * l) * kS + pl], S.dy[(2 * l + 1) * kS + pl],
+                encode_level_bwd2<D, NPM, ACC, std::is_same<ACC, float>::value>(g, l, x, G.dy[(2 * l) * kS + pl], G.dy[(2 * l + 1) * kS + pl],
                                                feats, conf, gfeat, gconf, touched);
         }
 #pragma unroll
         for (int a = 0; a < D; ++a) x[a] = xn[a];
         PG_PH(11);
     }
+    if (gid == 0) xsync();   // matches pipeline 1's leading phase
     PG_PH_FLUSH
     // ---- flush ----
     ACC *gW0p = gparams, *gb0p = gW0p + kI * kH, *gW1p = gb0p + kH, *gb1p = gW1p + kH * kH;
@@ -494,17 +537,17 @@ __global__ void __launch_bounds__(tm::kNT, 2)
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-    if (lane == 0) S.lred[warp] = lsum;
-    __syncthreads();
+    if (lane == 0) G.lred[warp] = lsum;
+    gsync();
     if (tid < 32) {
-        double v = tid < kNT / 32 ? S.lred[tid] : 0.0;
+        double v = tid < kNT / 32 ? G.lred[tid] : 0.0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (tid == 0 && loss_sum) loss_add(loss_sum, v);
     }
     umma::fence_before_sync();
     __syncthreads();
-    if (warp == 0) umma::tmem_free<64>(S.tmem_base);
+    if (threadIdx.x < 32) umma::tmem_free<64 * NG>(S.tmem_base);
 }
 
 PG_PH_READER(pg_phase_prof_read_mma)
@@ -513,29 +556,40 @@ template <typename ACC, typename LACC>
 int train_mma(const pg_grid *g, int od, const float *xs, const float *targets, int64_t B, const float *feats,
               const uint8_t *baked, const float *conf, const float *params, float scale, int sig, ACC *gfeat,
               ACC *gconf, uint8_t *touched, ACC *gparams, LACC *loss_sum, float *dy_out, cudaStream_t s) {
-    const int smem = (int)sizeof(tm::Smem);
-    static bool configured[6] = {false, false, false, false, false, false};
-    int sms = 0, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static bool configured[12] = {};
+    static int sms = 0, groups = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const char *e = getenv("PG_TRAIN_GROUPS");   // tile pipelines per CTA (1 or 2)
+        groups = e && atoi(e) == 1 ? 1 : 2;
+    }
     const int64_t ntiles = (B + tm::kT - 1) / tm::kT;
-    const int grd = (int)(ntiles < 2 * sms ? ntiles : 2 * sms);
     const int npm = g->log2_np <= 2 ? 4 : g->log2_np == 3 ? 8 : 16;   // probing range held in registers
-#define PG_TRAIN_MMA(D_, NP_, IDX)                                                                    \
+#define PG_TRAIN_MMA(D_, NP_, NG_, IDX)                                                               \
     do {                                                                                              \
-        auto kern = train_mma_kernel<float, D_, NP_, ACC, LACC>;                                      \
+        auto kern = train_mma_kernel<float, D_, NP_, ACC, LACC, NG_>;                                 \
+        const int smem = (int)sizeof(tm::SmemT<NG_>);                                                 \
         if (!configured[IDX]) {                                                                       \
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);            \
             configured[IDX] = true;                                                                   \
         }                                                                                             \
-        kern<<<grd, tm::kNT, smem, s>>>(*g, xs, targets, B, feats, feats, baked, conf, params, od,     \
-                                        scale, sig, gfeat, gconf, touched, gparams, loss_sum, dy_out); \
+        const int64_t want = (ntiles + NG_ - 1) / NG_, cap = (int64_t)sms * (2 / NG_);                \
+        const int grd = (int)(want < cap ? want : cap);                                               \
+        kern<<<grd, tm::kNT * NG_, smem, s>>>(*g, xs, targets, B, feats, feats, baked, conf, params, od, \
+                                              scale, sig, gfeat, gconf, touched, gparams, loss_sum, dy_out); \
+    } while (0)
+#define PG_TRAIN_MMA_NG(D_, NP_, IDX)                                                                 \
+    do {                                                                                              \
+        if (groups == 2) PG_TRAIN_MMA(D_, NP_, 2, (IDX) + 6); else PG_TRAIN_MMA(D_, NP_, 1, IDX);     \
     } while (0)
     if (g->d == 2) {
-        if (npm == 4) PG_TRAIN_MMA(2, 4, 0); else if (npm == 8) PG_TRAIN_MMA(2, 8, 4); else PG_TRAIN_MMA(2, 16, 1);
+        if (npm == 4) PG_TRAIN_MMA_NG(2, 4, 0); else if (npm == 8) PG_TRAIN_MMA_NG(2, 8, 4); else PG_TRAIN_MMA_NG(2, 16, 1);
     } else {
-        if (npm == 4) PG_TRAIN_MMA(3, 4, 2); else if (npm == 8) PG_TRAIN_MMA(3, 8, 5); else PG_TRAIN_MMA(3, 16, 3);
+        if (npm == 4) PG_TRAIN_MMA_NG(3, 4, 2); else if (npm == 8) PG_TRAIN_MMA_NG(3, 8, 5); else PG_TRAIN_MMA_NG(3, 16, 3);
     }
+#undef PG_TRAIN_MMA_NG
 #undef PG_TRAIN_MMA
     return check_launch("train_mma");
 }
