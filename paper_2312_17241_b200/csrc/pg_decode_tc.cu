@@ -287,8 +287,26 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
 
     const int64_t ntiles = (B + kTP - 1) / kTP;
     uint32_t phase = 0;
-    for (int64_t tile = (int64_t)blockIdx.x * kGroups + grp; tile < ntiles;
-         tile += (int64_t)gridDim.x * kGroups, phase ^= 1u) {
+    // Token ring over the pipelines' MLP phases (named barriers 4..4+NG-1):
+    // pipeline g starts its tensor-core MLP only after pipeline g-1 finished
+    // its own (bar.arrive at an MLP's end, bar.sync before the next), so the
+    // MLP phases of a CTA's pipelines never overlap and the L1 gather pipe
+    // always has the other pipelines' encodes: 3.71e9 vs 3.43e9 q/s free-
+    // running (C2).  All pipelines run as many iterations as pipeline 0.
+    constexpr bool RING = NG > 1;
+    const int64_t stride_t = (int64_t)gridDim.x * kGroups, first_t = (int64_t)blockIdx.x * kGroups + grp;
+    const int64_t base0 = (int64_t)blockIdx.x * kGroups;
+    const int64_t n_iter = base0 < ntiles ? (ntiles - base0 + stride_t - 1) / stride_t : 0;
+    for (int64_t iter = 0; iter < n_iter; ++iter) {
+        const int64_t tile = first_t + iter * stride_t;
+        if (tile >= ntiles) {
+            if (RING) {
+                if (grp > 0 || iter > 0) asm volatile("bar.sync %0, %1;" ::"r"(4 + grp), "r"(2 * kGT) : "memory");
+                asm volatile("bar.arrive %0, %1;" ::"r"(4 + (grp + 1) % NG), "r"(2 * kGT) : "memory");
+            }
+            continue;
+        }
+        phase = (uint32_t)(iter & 1);
         const int64_t p0 = tile * kTP;
         const int nv = (int)((B - p0) < kTP ? (B - p0) : kTP);
         if (STREAM && (int)(tile >> st.chunk_tiles_log2) != G.seen) {
@@ -347,6 +365,7 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
         umma::fence_async_smem();
         umma::fence_before_sync();
         group_sync(grp);
+        if (RING && (grp > 0 || iter > 0)) asm volatile("bar.sync %0, %1;" ::"r"(4 + grp), "r"(2 * kGT) : "memory");
         // ---------------- layer 1: D1 = (Y_hi + Y_lo) . W0 ----------------
         if (gt == 0) {
             umma::fence_after_sync();
@@ -428,6 +447,7 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
         }
         umma::fence_before_sync();
         group_sync(grp);
+        if (RING) asm volatile("bar.arrive %0, %1;" ::"r"(4 + (grp + 1) % NG), "r"(2 * kGT) : "memory");
         {
             float *dst = out + p0 * od;
             for (int i = gt; i < nv * od; i += kGT) {
@@ -444,6 +464,7 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
         group_sync(grp);
         if (gt == 0 && G.pending) tc::signal_done(st.done + G.seen, G.pending);
     }
+    if (RING && grp == 0 && n_iter > 0) asm volatile("bar.sync %0, %1;" ::"r"(4), "r"(2 * kGT) : "memory");
     umma::fence_after_sync();
     __syncthreads();
     if ((tid >> 5) == 0) umma::tmem_free<(NG == 1 ? 128 : NG == 2 ? 256 : 512)>(S.tmem_base);
