@@ -530,15 +530,19 @@ int decode_umma(const pg_grid *g, int od, const float *xs, int64_t B, const void
         if (const char *e = getenv("PG_DECODE_TABLE_BYTES")) env_budget = atoi(e);
         if (const char *k = getenv("PG_DECODE_TABLE_KINDS")) env_kinds = atoi(k);  // 1 dense, 2 baked
     }
-    // Without tables: three independent 256-thread CTAs per SM (~60 KB shared
-    // memory each).  With: one CTA of three pipelines per SM sharing <= 64 KB
-    // of bit-packed baked indices, so that smem + L1 stay inside the 196 KB
-    // carve-out and L1 keeps ~60 KB (measured on B200, tools/gpu_decode_ab.sh:
-    // +25% at N_p = 2, +3% at N_p = 4, -4% at N_p >= 8 where 4-bit packing fits
-    // only two levels, -15% at N_p = 1 where there is nothing to place).
+    // Shared-memory tables: the three pipelines of a CTA share <= 64 KB of
+    // bit-packed baked indices, so that smem + L1 stay inside the 196 KB
+    // carve-out and L1 keeps ~60 KB.  On for N_p = 2 and 4 (measured with the
+    // token ring: 3.99 vs 3.11e9 at N_p = 2, 3.72 vs 3.38e9 at N_p = 4;
+    // none or a wash at N_p = 1, 8, 16).
     const bool tables = (table_flags & PG_SMEM_TABLES) ||
                         (!(table_flags & PG_NO_SMEM_TABLES) && g->log2_np >= 1 && g->log2_np <= 2);
-    const int ng = tables ? 3 : 1;
+    // three token-ring pipelines per CTA (one CTA per SM) with or without
+    // tables: measured faster than three independent CTAs per SM for every
+    // C2/C5 shape (N_p 1: 4.72 vs 4.44e9, 8: 2.84 vs 2.61e9, 16: 2.84 vs
+    // 2.59e9 q/s); PG_DECODE_GROUPS=1 restores the independent CTAs
+    static const int env_groups = getenv("PG_DECODE_GROUPS") ? atoi(getenv("PG_DECODE_GROUPS")) : 3;
+    const int ng = (tables || env_groups != 1) ? 3 : 1;
     const int fixed = ng == 3 ? tc::tab_offset<3>() : tc::tab_offset<1>();
     int budget = 0;
     if (tables) {
