@@ -98,17 +98,23 @@ constexpr int kIn = 32;    // L * F
 constexpr int kHid = 64;
 constexpr int kOutMax = 4;
 
-struct DecodeSmem {
+struct DecodeSmemW {       // weights, shared by the CTA's tile pipelines
     float w0[kIn * kHid];
     float w1[kHid * kHid];
     float w2[kHid * kOutMax];
     float b0[kHid];
     float b1[kHid];
     float b2[kOutMax];
+};
+struct DecodeSmemG {       // one tile pipeline
     float actA[kHid * kTP];  // y^T (rows 0..31) for layer 1, then h2^T for layer 3
     float actB[kHid * kTP];  // h1^T
     float outs[kTP * kOutMax];
     float xs[kTP * 3];
+};
+struct DecodeSmem {        // two ping-pong pipelines per CTA
+    DecodeSmemW w;
+    DecodeSmemG g[2];
 };
 
 __device__ __forceinline__ int swz(int row, int col) {
@@ -144,7 +150,7 @@ __device__ __forceinline__ uint64_t ffma2(uint64_t acc, uint64_t a, uint64_t w) 
 template <int K, bool EXACT>
 __device__ __forceinline__ void layer_tile(const float *__restrict__ in_t, const float *__restrict__ W,
                                            const float *__restrict__ bias, float *__restrict__ out_t) {
-    const int og = threadIdx.x & 15, pg = threadIdx.x >> 4;
+    const int og = threadIdx.x & 15, pg = (threadIdx.x & 255) >> 4;   // within the 256-thread pipeline
     float acc[8][4];
     if (EXACT) {
         const float4 bb = *reinterpret_cast<const float4 *>(bias + og * 4);
@@ -209,42 +215,60 @@ __device__ __forceinline__ void layer_tile(const float *__restrict__ in_t, const
     }
 }
 
+// Two 256-thread tile pipelines per CTA (one CTA per SM) sharing the weights,
+// in ping-pong over their MLP phases (named barriers 3/4: a pipeline arrives
+// when its MLP ends and waits before its next one), so one pipeline's MLP
+// always runs beside the other's gathers.
 template <typename FT, int D, bool EXACT>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(512, 1)
     decode_fused_kernel(const pg_grid g, const float *__restrict__ xs, int64_t B,
                         const FT *__restrict__ feats, const uint8_t *__restrict__ baked,
                         const float *__restrict__ params, int out_dim, int sigmoid,
                         float *__restrict__ out, int32_t *__restrict__ bad) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    DecodeSmem &sm = *reinterpret_cast<DecodeSmem *>(smem_raw);
-    const int tid = threadIdx.x;
+    DecodeSmem &S = *reinterpret_cast<DecodeSmem *>(smem_raw);
+    const int gid = threadIdx.x >> 8, tid = threadIdx.x & 255;
+    DecodeSmemW &W = S.w;
+    DecodeSmemG &sm = S.g[gid];
+    auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + gid), "r"(256) : "memory"); };
     // ---- weights to shared memory once per CTA (params = [W0|b0|W1|b1|W2|b2]) ----
     {
         const float *p = params;
-        for (int i = tid; i < kIn * kHid; i += 256) sm.w0[i] = p[i];
+        const int t0 = threadIdx.x;
+        for (int i = t0; i < kIn * kHid; i += 512) W.w0[i] = p[i];
         p += kIn * kHid;
-        for (int i = tid; i < kHid; i += 256) sm.b0[i] = p[i];
+        for (int i = t0; i < kHid; i += 512) W.b0[i] = p[i];
         p += kHid;
-        for (int i = tid; i < kHid * kHid; i += 256) sm.w1[i] = p[i];
+        for (int i = t0; i < kHid * kHid; i += 512) W.w1[i] = p[i];
         p += kHid * kHid;
-        for (int i = tid; i < kHid; i += 256) sm.b1[i] = p[i];
+        for (int i = t0; i < kHid; i += 512) W.b1[i] = p[i];
         p += kHid;
-        for (int i = tid; i < kHid * kOutMax; i += 256) {
+        for (int i = t0; i < kHid * kOutMax; i += 512) {
             const int k = i / kOutMax, j = i % kOutMax;
-            sm.w2[i] = j < out_dim ? p[k * out_dim + j] : 0.0f;
+            W.w2[i] = j < out_dim ? p[k * out_dim + j] : 0.0f;
         }
         p += kHid * out_dim;
-        for (int i = tid; i < kOutMax; i += 256) sm.b2[i] = i < out_dim ? p[i] : 0.0f;
+        for (int i = t0; i < kOutMax; i += 512) W.b2[i] = i < out_dim ? p[i] : 0.0f;
     }
+    __syncthreads();
     const int64_t ntiles = (B + kTP - 1) / kTP;
     const int pl = tid & (kTP - 1);
     const int lhalf = tid >> 7;  // 0/1: which of the two levels per iteration
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t stride = (int64_t)gridDim.x * 2, first = (int64_t)blockIdx.x * 2 + gid;
+    const int64_t base0 = (int64_t)blockIdx.x * 2;
+    const int64_t n_iter = base0 < ntiles ? (ntiles - base0 + stride - 1) / stride : 0;
+    for (int64_t iter = 0; iter < n_iter; ++iter) {
+        const int64_t tile = first + iter * stride;
+        if (tile >= ntiles) {   // pipeline 1's last iteration: keep the ping-pong count
+            if (iter > 0) asm volatile("bar.sync 4, 512;" ::: "memory");
+            asm volatile("bar.arrive 3, 512;" ::: "memory");
+            continue;
+        }
         const int64_t p0 = tile * kTP;
         const int nvalid = (int)((B - p0) < kTP ? (B - p0) : kTP);
-        __syncthreads();  // previous tile's layer 3 finished reading actA / outs
+        gsync();  // previous tile's layer 3 finished reading actA / outs
         for (int i = tid; i < kTP * D; i += 256) sm.xs[i] = i < nvalid * D ? xs[p0 * D + i] : 0.0f;
-        __syncthreads();
+        gsync();
         // ---------------- encode: thread = (query pl, levels lhalf, lhalf+2, ...) --------
         float x[D];
         bool oob = false;
@@ -262,21 +286,24 @@ __global__ void __launch_bounds__(256, 2)
             sm.actA[swz(2 * l, pl)] = y0;
             sm.actA[swz(2 * l + 1, pl)] = y1;
         }
-        __syncthreads();
-        layer_tile<kIn, EXACT>(sm.actA, sm.w0, sm.b0, sm.actB);
-        __syncthreads();
-        layer_tile<kHid, EXACT>(sm.actB, sm.w1, sm.b1, sm.actA);
-        __syncthreads();
+        gsync();
+        // MLP phase: wait for the other pipeline's previous MLP to end
+        if (gid == 0) asm volatile("bar.sync 3, 512;" ::: "memory");
+        else if (iter > 0) asm volatile("bar.sync 4, 512;" ::: "memory");
+        layer_tile<kIn, EXACT>(sm.actA, W.w0, W.b0, sm.actB);
+        gsync();
+        layer_tile<kHid, EXACT>(sm.actB, W.w1, W.b1, sm.actA);
+        gsync();
         // ---------------- output layer: thread = (query, pair of outputs) -------------
         {
             const int q = tid & (kTP - 1);
             const int j0 = (tid >> 7) * 2;
-            float acc0 = sm.b2[j0], acc1 = sm.b2[j0 + 1];
+            float acc0 = W.b2[j0], acc1 = W.b2[j0 + 1];
 #pragma unroll 16
             for (int k = 0; k < kHid; ++k) {
                 const float a = sm.actA[swz(k, q)];
-                acc0 = mac<EXACT>(acc0, a, sm.w2[k * kOutMax + j0]);
-                acc1 = mac<EXACT>(acc1, a, sm.w2[k * kOutMax + j0 + 1]);
+                acc0 = mac<EXACT>(acc0, a, W.w2[k * kOutMax + j0]);
+                acc1 = mac<EXACT>(acc1, a, W.w2[k * kOutMax + j0 + 1]);
             }
             if (sigmoid) {
                 acc0 = (float)(1.0 / (1.0 + exp(-(double)acc0)));
@@ -285,13 +312,15 @@ __global__ void __launch_bounds__(256, 2)
             sm.outs[q * kOutMax + j0] = acc0;
             sm.outs[q * kOutMax + j0 + 1] = acc1;
         }
-        __syncthreads();
+        gsync();
+        asm volatile("bar.arrive %0, 512;" ::"r"(gid == 0 ? 4 : 3) : "memory");   // MLP done
         float *dst = out + p0 * out_dim;
         for (int i = tid; i < nvalid * out_dim; i += 256) {
             const int q = i / out_dim, j = i - q * out_dim;
             dst[i] = sm.outs[q * kOutMax + j];
         }
     }
+    if (gid == 1 && n_iter > 0) asm volatile("bar.sync 4, 512;" ::: "memory");   // pipeline 0's last MLP-done
 }
 
 static bool decode_fast_ok(const pg_grid *g, const pg_mlp *m) {
@@ -322,9 +351,9 @@ static void launch_decode(const pg_grid *g, const float *xs, int64_t B, const vo
         configured = true;
     }
     const int64_t ntiles = (B + kTP - 1) / kTP;
-    const int64_t cap = (int64_t)sm_count() * 2;
-    const int grd = (int)(ntiles < cap ? ntiles : cap);
-    decode_fused_kernel<FT, D, EXACT><<<grd, 256, smem, s>>>(*g, xs, B, (const FT *)feats, baked,
+    const int64_t want = (ntiles + 1) / 2, cap = (int64_t)sm_count();
+    const int grd = (int)(want < cap ? want : cap);
+    decode_fused_kernel<FT, D, EXACT><<<grd, 512, smem, s>>>(*g, xs, B, (const FT *)feats, baked,
                                                             params, out_dim, sig, out, bad);
 }
 

@@ -52,3 +52,14 @@ if len(sys.argv) > 3 and sys.argv[3] == "stream":
     torch.cuda.synchronize()
     print(f"  stream kernel only: {e0.elapsed_time(e1) / 5:.4f} ms (incl. host sync per call)")
     del os.environ["PG_DEBUG_STREAM_NOCOPY"]
+if len(sys.argv) > 3 and sys.argv[3] == "exact":
+    for kw, name in ((dict(exact=True), "exact reference-order"), (dict(exact=False, tensor=False), "FFMA")):
+        for _ in range(2):
+            decode_device(inf, xs, out, **kw)
+        e0.record()
+        for _ in range(5):
+            decode_device(inf, xs, out, **kw)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 5
+        print(f"  {name}: {ms:.4f} ms, {(1 << 24) / ms / 1e-3:.4g} q/s")
