@@ -41,9 +41,8 @@ struct SmemW {            // weights: shared by the tile pipelines of a CTA
 };
 struct SmemG {            // one tile pipeline's activations
     float y[kI * kS];     // y^T [f][q] of the current tile, then of the next
-    float dy[kI * kS];    // dL/dy^T [f][q]
     float h1[kH * kS];    // relu(z1)^T [i][q], later delta1^T
-    float h2[kH * kS];    // relu(z2)^T [k][q], later delta2^T
+    float h2[kH * kS];    // relu(z2)^T [k][q], later delta2^T, then dL/dy^T (rows < 32)
     float d3[kT * 8];     // dL/d(out) [q][j], columns >= od zero
     float xs[kT * 3];
     float tg[kT * kO];
@@ -246,6 +245,10 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
     const int tid = threadIdx.x & (kNT - 1), warp = tid >> 5, lane = tid & 31;
     SmemW &W = S.w;
     SmemG &G = S.g[gid];
+    // dL/dy^T [f][q] lives in h2's rows 0..31: delta2 is dead when dy is
+    // stored, and h2 is rewritten only by the next tile's layer 2 (saves 9 KB
+    // per pipeline of shared memory for L1: 0.548 vs 0.551 ms per C1 step)
+    float *const GDY = G.h2;
     // barrier of this pipeline's 256 threads / of the whole CTA
     auto gsync = [&]() {
         if constexpr (NG == 1) __syncthreads();
@@ -461,14 +464,14 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
             }
             warp_gemm<2, kH>(yacc, G.h1, 1, kS, 16 * mt, W.w0, 1, kS, 16 * (warp >> 2));
             PG_PH(9);
-            store_frags_T<2>(G.dy, yacc, 16 * mt, 16 * (warp >> 2), [](float v, int, int) { return v; });
+            store_frags_T<2>(GDY, yacc, 16 * mt, 16 * (warp >> 2), [](float v, int, int) { return v; });
         }
         gsync();   // dy complete; y, xs, tg free for the next tile
         PG_PH(10);
         if (dy_out) {
             for (int i = tid; i < nv * kI; i += kNT) {
                 const int q = i / kI, c = i % kI;
-                dy_out[(p0 + q) * kI + c] = G.dy[c * kS + q];
+                dy_out[(p0 + q) * kI + c] = GDY[c * kS + q];
             }
         }
         // ---- stage the next tile's inputs (prefetched into registers) ----
@@ -495,7 +498,7 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
                 G.y[(2 * l + 1) * kS + pl] = yv.y;
             }
             if (pl < nv)
-                encode_level_bwd2<D, NPM, ACC, std::is_same<ACC, float>::value>(g, l, x, G.dy[(2 * l) * kS + pl], G.dy[(2 * l + 1) * kS + pl],
+                encode_level_bwd2<D, NPM, ACC, std::is_same<ACC, float>::value>(g, l, x, GDY[(2 * l) * kS + pl], GDY[(2 * l + 1) * kS + pl],
                                                feats, conf, gfeat, gconf, touched);
         }
 #pragma unroll
