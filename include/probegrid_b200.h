@@ -339,7 +339,8 @@ int pg_raster_coords_f32(int x0, int y0, int w, int h, int width, int height,
  * sample, every layer's input and output delta to acts, laid out as
  * [a_0 | a_1 | .. | a_{n-1} | delta_0 | .. | delta_{n-1}], each block B rows
  * of its width (a_0 = y, a_l = relu activations, delta_l = dL/d(pre-activation
- * of layer l)); pg_mlp_acts_floats(B, mlp) floats.  pg_mlp_wgrad_blas_f32
+ * of layer l)); pg_mlp_acts_floats(B, mlp) floats (which include the
+ * scratch pg_mlp_wgrad_blas_f32 uses after them).  pg_mlp_wgrad_blas_f32
  * then forms gparams += every weight and bias gradient in numpy/OpenBLAS
  * order (mlp.py:80-84): the sgemm K loop over samples is blocked by 448 (the
  * last two blocks balanced), each block one sequential FMA chain from 0,

@@ -693,36 +693,111 @@ int64_t mlp_params(const pg_mlp *m) { return mlp_param_count(m); }
 // =========================================================================
 constexpr int64_t kBlasQ = 448;
 
-__global__ void wgrad_blas_kernel(const float *__restrict__ a, int fin, const float *__restrict__ d, int fout,
-                                  int64_t B, float *__restrict__ gW, float *__restrict__ gb) {
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < fin * fout) {
-        const int i = e / fout, j = e - (e / fout) * fout;
-        float c = 0.0f;
-        for (int64_t ls = 0; ls < B;) {
-            int64_t ml = B - ls;
-            if (ml >= 2 * kBlasQ) ml = kBlasQ;
-            else if (ml > kBlasQ) ml = ml / 2;
-            float acc = 0.0f;
-#pragma unroll 8
-            for (int64_t k = ls; k < ls + ml; ++k) acc = __fmaf_rn(__ldg(a + k * fin + i), __ldg(d + k * fout + j), acc);
-            c = __fadd_rn(c, acc);
-            ls += ml;
-        }
-        gW[e] = __fadd_rn(gW[e], c);
-    } else if (e < fin * fout + fout) {
-        const int j = e - fin * fout;
-        float sacc = 0.0f;
-#pragma unroll 8
-        for (int64_t k = 0; k < B; ++k) sacc = __fadd_rn(sacc, __ldg(d + k * fout + j));
-        gb[j] = __fadd_rn(gb[j], sacc);
+// K (= sample) blocking of OpenBLAS's sgemm: Q-blocks while at least 2Q
+// samples remain, then the rest in one block (<= Q) or two balanced halves
+__host__ __device__ inline int64_t blas_nblocks(int64_t B) {
+    const int64_t nq = B >= 2 * kBlasQ ? (B - 2 * kBlasQ) / kBlasQ + 1 : 0;
+    const int64_t r = B - nq * kBlasQ;
+    return nq + (r > kBlasQ ? 2 : r > 0 ? 1 : 0);
+}
+__device__ inline void blas_block(int64_t B, int64_t blk, int64_t &start, int64_t &len) {
+    const int64_t nq = B >= 2 * kBlasQ ? (B - 2 * kBlasQ) / kBlasQ + 1 : 0;
+    if (blk < nq) {
+        start = blk * kBlasQ;
+        len = kBlasQ;
+        return;
+    }
+    const int64_t r = B - nq * kBlasQ;
+    if (r > kBlasQ) {
+        const int64_t h = r / 2;
+        start = nq * kBlasQ + (blk == nq ? 0 : h);
+        len = blk == nq ? h : r - h;
+    } else {
+        start = nq * kBlasQ;
+        len = r;
     }
 }
 
+// pass 1: every (block, element) chain in parallel -- each block's FMA chain
+// starts from 0 in OpenBLAS, so the chains are independent
+__global__ void wgrad_blas_partial_kernel(const float *__restrict__ a, int fin, const float *__restrict__ d,
+                                          int fout, int64_t B, int64_t nblk, float *__restrict__ part) {
+    const int64_t E = (int64_t)fin * fout;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nblk * E) return;
+    const int64_t blk = t / E;
+    const int e = (int)(t - blk * E);
+    const int i = e / fout, j = e - i * fout;
+    int64_t ls, ml;
+    blas_block(B, blk, ls, ml);
+    float acc = 0.0f;
+#pragma unroll 8
+    for (int64_t k = ls; k < ls + ml; ++k) acc = __fmaf_rn(__ldg(a + k * fin + i), __ldg(d + k * fout + j), acc);
+    part[t] = acc;
+}
+
+// pass 2: C = 0; C += block partial, blocks in order; then gW += C.
+// Bias: delta.sum(axis=0) adds the rows in order (sequential over samples).
+__global__ void wgrad_blas_reduce_kernel(const float *__restrict__ part, int64_t nblk, int fin, int fout,
+                                         const float *__restrict__ d, int64_t B, float *__restrict__ gW,
+                                         float *__restrict__ gb) {
+    const int64_t E = (int64_t)fin * fout;
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < E) {
+        float c = 0.0f;
+        for (int64_t b = 0; b < nblk; ++b) c = __fadd_rn(c, part[b * E + e]);
+        gW[e] = __fadd_rn(gW[e], c);
+    }
+}
+
+// Bias: delta.sum(axis=0) adds the rows in order -- one dependent add chain
+// per output over all B samples.  One CTA per layer: the rows are staged
+// through shared memory with coalesced loads, then thread j adds column j
+// in row order (the chain's adds, not the loads, set the pace).
+__global__ void bias_blas_kernel(const float *__restrict__ d0, const float *__restrict__ d1,
+                                 const float *__restrict__ d2, int f0, int f1, int f2, int64_t B,
+                                 float *__restrict__ g0, float *__restrict__ g1, float *__restrict__ g2) {
+    constexpr int R = 128;
+    __shared__ __align__(16) float tile[R * 64];
+    const float *d = blockIdx.x == 0 ? d0 : blockIdx.x == 1 ? d1 : d2;
+    const int fout = blockIdx.x == 0 ? f0 : blockIdx.x == 1 ? f1 : f2;
+    float *gb = blockIdx.x == 0 ? g0 : blockIdx.x == 1 ? g1 : g2;
+    if (!d || fout <= 0) return;
+    const int j = threadIdx.x;
+    float s = 0.0f;
+    for (int64_t r0 = 0; r0 < B; r0 += R) {
+        const int nr = (int)(B - r0 < R ? B - r0 : R);
+        __syncthreads();
+        // the chunk is contiguous (rows of fout floats): 16-byte loads, all
+        // issued before any is consumed
+        const int n = nr * fout;
+        const float *src = d + r0 * fout;
+        if ((n & 3) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+            const float4 *s4 = reinterpret_cast<const float4 *>(src);
+            float4 *t4 = reinterpret_cast<float4 *>(tile);
+#pragma unroll 4
+            for (int i = threadIdx.x; i < n / 4; i += blockDim.x) t4[i] = __ldg(s4 + i);
+        } else {
+#pragma unroll 4
+            for (int i = threadIdx.x; i < n; i += blockDim.x) tile[i] = __ldg(src + i);
+        }
+        __syncthreads();
+        if (j < fout) {
+#pragma unroll 8
+            for (int r = 0; r < nr; ++r) s = __fadd_rn(s, tile[r * fout + j]);
+        }
+    }
+    if (j < fout) gb[j] = __fadd_rn(gb[j], s);
+}
+
 int64_t mlp_acts_floats(int64_t B, const pg_mlp *m) {
-    int64_t w = 0;
-    for (int l = 0; l < m->n_layers; ++l) w += m->widths[l] + m->widths[l + 1];
-    return B * w;
+    int64_t w = 0, e = 0;
+    for (int l = 0; l < m->n_layers; ++l) {
+        w += m->widths[l] + m->widths[l + 1];
+        const int64_t el = (int64_t)m->widths[l] * m->widths[l + 1];
+        e = el > e ? el : e;
+    }
+    return B * w + blas_nblocks(B) * e;   // + the per-block partial sums of pass 1
 }
 
 int mlp_wgrad_blas(const pg_mlp *m, const float *acts, int64_t B, float *gparams, cudaStream_t s) {
@@ -731,16 +806,31 @@ int mlp_wgrad_blas(const pg_mlp *m, const float *acts, int64_t B, float *gparams
     // acts = [a_0 | .. | a_{n-1} | delta_0 | .. | delta_{n-1}]
     int64_t a_off = 0, d_off = 0;
     for (int l = 0; l < m->n_layers; ++l) d_off += B * m->widths[l];
+    int64_t w = 0;
+    for (int l = 0; l < m->n_layers; ++l) w += m->widths[l] + m->widths[l + 1];
+    float *part = const_cast<float *>(acts) + B * w;   // scratch after the activations
+    const int64_t nblk = blas_nblocks(B);
+    PG_REQUIRE(m->n_layers <= 3, "reference-order weight gradients: at most 3 layers");
+    const float *dl[3] = {nullptr, nullptr, nullptr};
+    float *gbl[3] = {nullptr, nullptr, nullptr};
+    int fo[3] = {0, 0, 0};
     float *g = gparams;
     for (int l = 0; l < m->n_layers; ++l) {
         const int fin = m->widths[l], fout = m->widths[l + 1];
-        const int n = fin * fout + fout;
-        wgrad_blas_kernel<<<(n + 127) / 128, 128, 0, s>>>(acts + a_off, fin, acts + d_off, fout, B, g,
-                                                          g + (int64_t)fin * fout);
+        PG_REQUIRE(fout <= 64, "reference-order bias sums: width <= 64");
+        const int64_t E = (int64_t)fin * fout, n1 = nblk * E;
+        wgrad_blas_partial_kernel<<<(unsigned)((n1 + 255) / 256), 256, 0, s>>>(acts + a_off, fin, acts + d_off,
+                                                                               fout, B, nblk, part);
+        wgrad_blas_reduce_kernel<<<(unsigned)((E + 127) / 128), 128, 0, s>>>(part, nblk, fin, fout, acts + d_off,
+                                                                             B, g, g + E);
+        dl[l] = acts + d_off;
+        gbl[l] = g + E;
+        fo[l] = fout;
         a_off += B * fin;
         d_off += B * fout;
-        g += (int64_t)fin * fout + fout;
+        g += E + fout;
     }
+    bias_blas_kernel<<<m->n_layers, 256, 0, s>>>(dl[0], dl[1], dl[2], fo[0], fo[1], fo[2], B, gbl[0], gbl[1], gbl[2]);
     return check_launch("mlp_wgrad_blas");
 }
 
