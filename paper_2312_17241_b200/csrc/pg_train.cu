@@ -16,6 +16,8 @@
 // activations, the loss terms and dy = dL/dy are bit-identical to the
 // reference for the same parameters and batch; only the cross-sample sums
 // (weight/bias gradients, table scatters) are reordered.
+#include <cstdlib>
+
 #include "pg_encode_dev.cuh"
 #include "pg_phase.cuh"
 
@@ -29,10 +31,12 @@ constexpr int kI = 32;    // L*F
 constexpr int kH = 64;    // hidden width
 constexpr int kO = 4;     // padded output width
 
-struct TrainSmem {
+struct TrainW {           // weights: shared by the tile pipelines of a CTA
     float w0[kI * kH], w1[kH * kH], w2[kH * kO];      // [in][out]
     float w0t[kH * kI], w1t[kH * kH];                 // [out][in]
     float b0[kH], b1[kH], b2[kO];
+};
+struct TrainG {           // one tile pipeline's activations
     float yT[kI * kT];    // encodings, later dL/dy       (swizzled rows)
     float z1T[kH * kT];   // layer-1 activations relu(z1), later delta_1
     float z2T[kH * kT];   // layer-2 activations relu(z2), later delta_2
@@ -41,14 +45,20 @@ struct TrainSmem {
     float tg[kT * kO];
     double red[kNT / 32];
 };
+// NG tile pipelines of kNT threads per CTA (pg_train_mma.cu's layout)
+template <int NG>
+struct TrainSmemT {
+    TrainW w;
+    TrainG g[NG];
+};
 
 __device__ __forceinline__ int sw(int row, int col) {
     const int chunk = (col >> 2) ^ ((row >> 2) & 7);
     return row * kT + (chunk << 2) + (col & 3);
 }
 // parity mode: copy a transposed smem tile (rows = features) to acts rows
-__device__ __forceinline__ void dump_tile(const float *srcT, int width, int nv, float *dst) {
-    for (int i = threadIdx.x; i < nv * width; i += kNT) {
+__device__ __forceinline__ void dump_tile(const float *srcT, int width, int nv, float *dst, int tid) {
+    for (int i = tid; i < nv * width; i += kNT) {
         const int q = i / width, c = i - q * width;
         dst[(int64_t)q * width + c] = srcT[sw(c, q)];
     }
@@ -62,7 +72,7 @@ __device__ __forceinline__ float mask_np(float z) { return z > 0.0f ? 1.0f : 0.0
 template <int K>
 __device__ __forceinline__ void fwd_layer(const float *__restrict__ inT, const float *__restrict__ W,
                                           const float *__restrict__ b, float *__restrict__ outT) {
-    const int og = threadIdx.x & 15, pg = threadIdx.x >> 4;  // 4 outputs x 4 samples
+    const int t = threadIdx.x & (kNT - 1), og = t & 15, pg = t >> 4;  // 4 outputs x 4 samples (pipeline-local thread)
     float acc[4][4] = {};
 #pragma unroll 8
     for (int k = 0; k < K; ++k) {
@@ -86,8 +96,13 @@ __device__ __forceinline__ void fwd_layer(const float *__restrict__ inT, const f
     }
 }
 
-template <typename FT, int D, int NPM, typename ACC, typename LACC>
-__global__ void __launch_bounds__(kNT, 2)
+// NG = 1: one 8-warp tile pipeline per CTA, two CTAs per SM.  NG = 2: one
+// CTA per SM running two 8-warp pipelines that share the weights (50 KB less
+// shared memory per SM) and ping-pong their FFMA MLP phases (named barriers
+// 3/4, as in pg_train_mma.cu), so one pipeline's MLP always runs beside the
+// other's encode.  The per-element arithmetic is the same in both.
+template <typename FT, int D, int NPM, typename ACC, typename LACC, int NG>
+__global__ void __launch_bounds__(kNT *NG, 2 / NG)
     train_fused_kernel(const pg_grid g, const float *__restrict__ xs, const float *__restrict__ targets,
                        int64_t B, const FT *__restrict__ feats_fwd, const float *__restrict__ feats,
                        const uint8_t *__restrict__ baked, const float *__restrict__ conf,
@@ -97,34 +112,45 @@ __global__ void __launch_bounds__(kNT, 2)
                        LACC *__restrict__ loss_sum, float *__restrict__ dy_out,
                        float *__restrict__ acts) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    TrainSmem &S = *reinterpret_cast<TrainSmem *>(smem_raw);
-    const int tid = threadIdx.x;
-    // ---- parameters -> shared (both layouts) ----
+    TrainSmemT<NG> &S = *reinterpret_cast<TrainSmemT<NG> *>(smem_raw);
+    const int gid = NG == 1 ? 0 : (int)(threadIdx.x >> 8);   // tile pipeline
+    const int tid = threadIdx.x & (kNT - 1);
+    TrainW &W = S.w;
+    TrainG &G = S.g[gid];
+    auto gsync = [&]() {   // barrier of this pipeline's threads
+        if constexpr (NG == 1) __syncthreads();
+        else asm volatile("bar.sync %0, %1;" ::"r"(1 + gid), "r"(kNT) : "memory");
+    };
+    auto bar_sync = [&](int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(2 * kNT) : "memory"); };
+    auto bar_arrive = [&](int id) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(2 * kNT) : "memory"); };
+    // ---- parameters -> shared (both layouts), by all NG pipelines ----
     {
+        const int tid = threadIdx.x;
+        constexpr int kNT = ::pg::kNT * NG;
         const float *p = params;
         for (int i = tid; i < kI * kH; i += kNT) {
             const float v = p[i];
-            S.w0[i] = v;
-            S.w0t[(i % kH) * kI + i / kH] = v;
+            W.w0[i] = v;
+            W.w0t[(i % kH) * kI + i / kH] = v;
         }
         p += kI * kH;
-        for (int i = tid; i < kH; i += kNT) S.b0[i] = p[i];
+        for (int i = tid; i < kH; i += kNT) W.b0[i] = p[i];
         p += kH;
         for (int i = tid; i < kH * kH; i += kNT) {
             const float v = p[i];
-            S.w1[i] = v;
-            S.w1t[(i % kH) * kH + i / kH] = v;
+            W.w1[i] = v;
+            W.w1t[(i % kH) * kH + i / kH] = v;
         }
         p += kH * kH;
-        for (int i = tid; i < kH; i += kNT) S.b1[i] = p[i];
+        for (int i = tid; i < kH; i += kNT) W.b1[i] = p[i];
         p += kH;
         for (int i = tid; i < kH * kO; i += kNT) {
             const int k = i / kO, j = i % kO;
             const float v = j < od ? p[k * od + j] : 0.0f;
-            S.w2[i] = v;
+            W.w2[i] = v;
         }
         p += kH * od;
-        for (int i = tid; i < kO; i += kNT) S.b2[i] = i < od ? p[i] : 0.0f;
+        for (int i = tid; i < kO; i += kNT) W.b2[i] = i < od ? p[i] : 0.0f;
     }
     // persistent per-thread gradient accumulators
     float gW2 = 0.0f;                 // (k = tid&63, j = tid>>6)
@@ -147,41 +173,60 @@ __global__ void __launch_bounds__(kNT, 2)
         const int q = tid / kO, j = tid % kO;
         ft = (q < n && j < od) ? __ldg(targets + (q0 + q) * od + j) : 0.0f;
     };
+    // tiles of this pipeline: first, first + stride, ...; every pipeline of a
+    // CTA runs as many iterations as its first one (the most), so the
+    // ping-pong barrier counts match up
+    const int64_t first = (int64_t)blockIdx.x * NG + gid, stride = (int64_t)gridDim.x * NG;
+    const int64_t base0 = (int64_t)blockIdx.x * NG;
+    const int64_t n_iter = base0 < ntiles ? (ntiles - base0 + stride - 1) / stride : 0;
     float pf_x, pf_t;
-    fetch(blockIdx.x, pf_x, pf_t);
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    fetch(first, pf_x, pf_t);
+    __syncthreads();   // weights staged
+    for (int64_t iter = 0; iter < n_iter; ++iter) {
+        const int64_t tile = first + iter * stride;
+        if (tile >= ntiles) {   // (only pipeline 1's last iteration) keep the barrier counts
+            if (NG > 1) {
+                if (iter > 0) bar_sync(4);
+                bar_arrive(3);
+            }
+            continue;
+        }
         const int64_t p0 = tile * kT;
         const int nv = (int)((B - p0) < kT ? (B - p0) : kT);
-        __syncthreads();
+        gsync();
         PG_PH(11);
-        if (tid < kT * D) S.xs[tid] = pf_x;
-        S.tg[tid] = pf_t;
-        fetch(tile + gridDim.x, pf_x, pf_t);
-        __syncthreads();
+        if (tid < kT * D) G.xs[tid] = pf_x;
+        G.tg[tid] = pf_t;
+        fetch(tile + stride, pf_x, pf_t);
+        gsync();
         PG_PH(0);
         // ---- encode forward: thread = (sample pl, levels lsub + 4*it) ----
         const int pl = tid & (kT - 1), lsub = tid >> 6;
         float x[D];
 #pragma unroll
-        for (int a = 0; a < D; ++a) x[a] = S.xs[pl * D + a];
+        for (int a = 0; a < D; ++a) x[a] = G.xs[pl * D + a];
 #pragma unroll 2
         for (int it = 0; it < 4; ++it) {
             const int l = lsub + 4 * it;
             const float2 yv = encode_level_fwd2<FT, D>(g, l, x, feats_fwd, baked);
-            S.yT[sw(2 * l, pl)] = yv.x;
-            S.yT[sw(2 * l + 1, pl)] = yv.y;
+            G.yT[sw(2 * l, pl)] = yv.x;
+            G.yT[sw(2 * l + 1, pl)] = yv.y;
         }
-        __syncthreads();
+        gsync();
+        if (NG > 1) {   // wait for the other pipeline's previous MLP to end
+            if (gid == 0) bar_sync(3);
+            else if (iter > 0) bar_sync(4);
+        }
         PG_PH(1);
-        if (acts) dump_tile(S.yT, kI, nv, acts + p0 * kI);
-        fwd_layer<kI>(S.yT, S.w0, S.b0, S.z1T);
-        __syncthreads();
+        if (acts) dump_tile(G.yT, kI, nv, acts + p0 * kI, tid);
+        fwd_layer<kI>(G.yT, W.w0, W.b0, G.z1T);
+        gsync();
         PG_PH(2);
-        if (acts) dump_tile(S.z1T, kH, nv, acts + B * kI + p0 * kH);
-        fwd_layer<kH>(S.z1T, S.w1, S.b1, S.z2T);
-        __syncthreads();
+        if (acts) dump_tile(G.z1T, kH, nv, acts + B * kI + p0 * kH, tid);
+        fwd_layer<kH>(G.z1T, W.w1, W.b1, G.z2T);
+        gsync();
         PG_PH(3);
-        if (acts) dump_tile(S.z2T, kH, nv, acts + B * (kI + kH) + p0 * kH);
+        if (acts) dump_tile(G.z2T, kH, nv, acts + B * (kI + kH) + p0 * kH, tid);
         // ---- output layer, loss, dpred (trainer.py:122-136) ----
         {
             const int q = tid & (kT - 1), j = tid >> 6;
@@ -189,30 +234,30 @@ __global__ void __launch_bounds__(kNT, 2)
             if (j < od && q < nv) {
                 float acc = 0.0f;
 #pragma unroll 16
-                for (int k = 0; k < kH; ++k) acc = __fmaf_rn(S.z2T[sw(k, q)], S.w2[k * kO + j], acc);
-                const float o = __fadd_rn(acc, S.b2[j]);
+                for (int k = 0; k < kH; ++k) acc = __fmaf_rn(G.z2T[sw(k, q)], W.w2[k * kO + j], acc);
+                const float o = __fadd_rn(acc, W.b2[j]);
                 const float pred = sigmoid ? 1.0f / (1.0f + expf(-o)) : o;
-                const float diff = __fsub_rn(pred, S.tg[q * kO + j]);
+                const float diff = __fsub_rn(pred, G.tg[q * kO + j]);
                 lsum += (double)diff * (double)diff;
                 d = __fmul_rn(diff, scale);
                 if (sigmoid) d = __fmul_rn(d, __fmul_rn(pred, __fsub_rn(1.0f, pred)));
             }
-            S.d3[q * kO + j] = d;
+            G.d3[q * kO + j] = d;
         }
-        __syncthreads();
+        gsync();
         PG_PH(4);
         if (acts)
             for (int i = tid; i < nv * od; i += kNT)
-                acts[B * (kI + 4 * kH) + p0 * od + i] = S.d3[(i / od) * kO + i % od];
+                acts[B * (kI + 4 * kH) + p0 * od + i] = G.d3[(i / od) * kO + i % od];
         // ---- dW2 += h2^T d3, db2 += sum d3 (4 samples per shared load) ----
         {
             const int k = tid & 63, j = tid >> 6;
             float acc = 0.0f, bs = 0.0f;
 #pragma unroll 4
             for (int q = 0; q < kT; q += 4) {
-                const float4 h = *reinterpret_cast<const float4 *>(S.z2T + sw(k, q));
-                const float d0 = S.d3[q * kO + j], d1 = S.d3[(q + 1) * kO + j];
-                const float d2 = S.d3[(q + 2) * kO + j], d3v = S.d3[(q + 3) * kO + j];
+                const float4 h = *reinterpret_cast<const float4 *>(G.z2T + sw(k, q));
+                const float d0 = G.d3[q * kO + j], d1 = G.d3[(q + 1) * kO + j];
+                const float d2 = G.d3[(q + 2) * kO + j], d3v = G.d3[(q + 3) * kO + j];
                 acc = __fmaf_rn(h.x, d0, acc);
                 acc = __fmaf_rn(h.y, d1, acc);
                 acc = __fmaf_rn(h.z, d2, acc);
@@ -222,7 +267,7 @@ __global__ void __launch_bounds__(kNT, 2)
             gW2 += acc;
             if (k == 0) gB2 += bs;
         }
-        __syncthreads();
+        gsync();
         PG_PH(5);
         // ---- delta2 = (d3 @ W2^T) * (z2 > 0), in place over z2 ----
         {
@@ -230,15 +275,15 @@ __global__ void __launch_bounds__(kNT, 2)
             float dq[4][kO];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const float4 v = *reinterpret_cast<const float4 *>(S.d3 + (pg * 4 + i) * kO);
+                const float4 v = *reinterpret_cast<const float4 *>(G.d3 + (pg * 4 + i) * kO);
                 dq[i][0] = v.x; dq[i][1] = v.y; dq[i][2] = v.z; dq[i][3] = v.w;
             }
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
                 const int k = og * 4 + jj;
-                const float4 wv = *reinterpret_cast<const float4 *>(S.w2 + k * kO);
+                const float4 wv = *reinterpret_cast<const float4 *>(W.w2 + k * kO);
                 const float w[kO] = {wv.x, wv.y, wv.z, wv.w};
-                float4 z = *reinterpret_cast<float4 *>(S.z2T + sw(k, pg * 4));
+                float4 z = *reinterpret_cast<float4 *>(G.z2T + sw(k, pg * 4));
                 float zv[4] = {z.x, z.y, z.z, z.w};
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
@@ -248,12 +293,12 @@ __global__ void __launch_bounds__(kNT, 2)
                         if (j < od) acc = __fmaf_rn(dq[i][j], w[j], acc);
                     zv[i] = __fmul_rn(acc, mask_np(zv[i]));
                 }
-                *reinterpret_cast<float4 *>(S.z2T + sw(k, pg * 4)) = make_float4(zv[0], zv[1], zv[2], zv[3]);
+                *reinterpret_cast<float4 *>(G.z2T + sw(k, pg * 4)) = make_float4(zv[0], zv[1], zv[2], zv[3]);
             }
         }
-        __syncthreads();
+        gsync();
         PG_PH(6);
-        if (acts) dump_tile(S.z2T, kH, nv, acts + B * (kI + 3 * kH) + p0 * kH);
+        if (acts) dump_tile(G.z2T, kH, nv, acts + B * (kI + 3 * kH) + p0 * kH, tid);
         // ---- dW1 += h1^T delta2, db1 += sum delta2 (summed by the ig == 0 threads) ----
         {
             const int jg = tid & 15, ig = tid >> 4;
@@ -261,9 +306,9 @@ __global__ void __launch_bounds__(kNT, 2)
             for (int q = 0; q < kT; q += 4) {
                 float4 a[4], dd[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) a[u] = *reinterpret_cast<const float4 *>(S.z1T + sw(ig * 4 + u, q));
+                for (int u = 0; u < 4; ++u) a[u] = *reinterpret_cast<const float4 *>(G.z1T + sw(ig * 4 + u, q));
 #pragma unroll
-                for (int v = 0; v < 4; ++v) dd[v] = *reinterpret_cast<const float4 *>(S.z2T + sw(jg * 4 + v, q));
+                for (int v = 0; v < 4; ++v) dd[v] = *reinterpret_cast<const float4 *>(G.z2T + sw(jg * 4 + v, q));
                 if (ig == 0) {
 #pragma unroll
                     for (int v = 0; v < 4; ++v) bs[v] += (dd[v].x + dd[v].y) + (dd[v].z + dd[v].w);
@@ -285,7 +330,7 @@ __global__ void __launch_bounds__(kNT, 2)
                 for (int v = 0; v < 4; ++v) gB1[v] += bs[v];
             }
         }
-        __syncthreads();
+        gsync();
         PG_PH(7);
         // ---- delta1 = (delta2 @ W1^T) * (z1 > 0), in place over z1 ----
         {
@@ -293,8 +338,8 @@ __global__ void __launch_bounds__(kNT, 2)
             float acc[4][4] = {};
 #pragma unroll 8
             for (int j = 0; j < kH; ++j) {
-                const float4 a = *reinterpret_cast<const float4 *>(S.z2T + sw(j, pg * 4));
-                const float4 w = *reinterpret_cast<const float4 *>(S.w1t + j * kH + og * 4);
+                const float4 a = *reinterpret_cast<const float4 *>(G.z2T + sw(j, pg * 4));
+                const float4 w = *reinterpret_cast<const float4 *>(W.w1t + j * kH + og * 4);
                 const float av[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
@@ -306,16 +351,16 @@ __global__ void __launch_bounds__(kNT, 2)
             }
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
-                float *dst = S.z1T + sw(og * 4 + jj, pg * 4);
+                float *dst = G.z1T + sw(og * 4 + jj, pg * 4);
                 const float4 z = *reinterpret_cast<float4 *>(dst);
                 *reinterpret_cast<float4 *>(dst) =
                     make_float4(__fmul_rn(acc[0][jj], mask_np(z.x)), __fmul_rn(acc[1][jj], mask_np(z.y)),
                                 __fmul_rn(acc[2][jj], mask_np(z.z)), __fmul_rn(acc[3][jj], mask_np(z.w)));
             }
         }
-        __syncthreads();
+        gsync();
         PG_PH(8);
-        if (acts) dump_tile(S.z1T, kH, nv, acts + B * (kI + 2 * kH) + p0 * kH);
+        if (acts) dump_tile(G.z1T, kH, nv, acts + B * (kI + 2 * kH) + p0 * kH, tid);
         // ---- dW0 += y^T delta1, db0 += sum delta1 (summed by the ig == 0 threads) ----
         {
             const int jg = tid & 15, ig = tid >> 4;
@@ -323,9 +368,9 @@ __global__ void __launch_bounds__(kNT, 2)
             for (int q = 0; q < kT; q += 4) {
                 float4 a[2], dd[4];
 #pragma unroll
-                for (int u = 0; u < 2; ++u) a[u] = *reinterpret_cast<const float4 *>(S.yT + sw(ig * 2 + u, q));
+                for (int u = 0; u < 2; ++u) a[u] = *reinterpret_cast<const float4 *>(G.yT + sw(ig * 2 + u, q));
 #pragma unroll
-                for (int v = 0; v < 4; ++v) dd[v] = *reinterpret_cast<const float4 *>(S.z1T + sw(jg * 4 + v, q));
+                for (int v = 0; v < 4; ++v) dd[v] = *reinterpret_cast<const float4 *>(G.z1T + sw(jg * 4 + v, q));
                 if (ig == 0) {
 #pragma unroll
                     for (int v = 0; v < 4; ++v) bs[v] += (dd[v].x + dd[v].y) + (dd[v].z + dd[v].w);
@@ -347,7 +392,7 @@ __global__ void __launch_bounds__(kNT, 2)
                 for (int v = 0; v < 4; ++v) gB0[v] += bs[v];
             }
         }
-        __syncthreads();
+        gsync();
         PG_PH(9);
         // ---- dy = delta1 @ W0^T (fma chain over j), over yT ----
         {
@@ -355,8 +400,8 @@ __global__ void __launch_bounds__(kNT, 2)
             float acc[2][4] = {};
 #pragma unroll 8
             for (int j = 0; j < kH; ++j) {
-                const float2 a = *reinterpret_cast<const float2 *>(S.z1T + sw(j, pg * 2));
-                const float4 w = *reinterpret_cast<const float4 *>(S.w0t + j * kI + og * 4);
+                const float2 a = *reinterpret_cast<const float2 *>(G.z1T + sw(j, pg * 2));
+                const float4 w = *reinterpret_cast<const float4 *>(W.w0t + j * kI + og * 4);
                 acc[0][0] = __fmaf_rn(a.x, w.x, acc[0][0]);
                 acc[0][1] = __fmaf_rn(a.x, w.y, acc[0][1]);
                 acc[0][2] = __fmaf_rn(a.x, w.z, acc[0][2]);
@@ -366,17 +411,18 @@ __global__ void __launch_bounds__(kNT, 2)
                 acc[1][2] = __fmaf_rn(a.y, w.z, acc[1][2]);
                 acc[1][3] = __fmaf_rn(a.y, w.w, acc[1][3]);
             }
-            __syncthreads();  // all reads of yT (dW0) finished before overwrite
+            gsync();  // all reads of yT (dW0) finished before overwrite
 #pragma unroll
             for (int ii = 0; ii < 4; ++ii)
-                *reinterpret_cast<float2 *>(S.yT + sw(og * 4 + ii, pg * 2)) = make_float2(acc[0][ii], acc[1][ii]);
+                *reinterpret_cast<float2 *>(G.yT + sw(og * 4 + ii, pg * 2)) = make_float2(acc[0][ii], acc[1][ii]);
         }
-        __syncthreads();
+        gsync();
+        if (NG > 1) bar_arrive(gid == 0 ? 4 : 3);   // MLP done: the other pipeline may start its own
         PG_PH(10);
         if (dy_out) {  // optional copy of dL/dy (parity tests)
             for (int i = tid; i < nv * kI; i += kNT) {
                 const int q = i / kI, c = i % kI;
-                dy_out[(p0 + q) * kI + c] = S.yT[sw(c, q)];
+                dy_out[(p0 + q) * kI + c] = G.yT[sw(c, q)];
             }
         }
         // ---- encode backward: scatter dy ----
@@ -384,11 +430,12 @@ __global__ void __launch_bounds__(kNT, 2)
 #pragma unroll 1
             for (int it = 0; it < 4; ++it) {
                 const int l = lsub + 4 * it;
-                encode_level_bwd2<D, NPM, ACC>(g, l, x, S.yT[sw(2 * l, pl)], S.yT[sw(2 * l + 1, pl)], feats,
+                encode_level_bwd2<D, NPM, ACC>(g, l, x, G.yT[sw(2 * l, pl)], G.yT[sw(2 * l + 1, pl)], feats,
                                          conf, gfeat, gconf, touched);
             }
         }
     }
+    if (NG > 1 && gid == 1 && n_iter > 0) bar_sync(4);   // consume pipeline 0's last MLP-done
     PG_PH_FLUSH
     // ---- flush gradient accumulators ----
     ACC *gW0p = gparams, *gb0p = gW0p + kI * kH, *gW1p = gb0p + kH, *gb1p = gW1p + kH * kH;
@@ -417,10 +464,10 @@ __global__ void __launch_bounds__(kNT, 2)
     // loss: block reduce in fp64
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-    if ((tid & 31) == 0) S.red[tid >> 5] = lsum;
-    __syncthreads();
+    if ((tid & 31) == 0) G.red[tid >> 5] = lsum;
+    gsync();
     if (tid < 32) {
-        double v = tid < kNT / 32 ? S.red[tid] : 0.0;
+        double v = tid < kNT / 32 ? G.red[tid] : 0.0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (tid == 0 && loss_sum) loss_add(loss_sum, v);
@@ -460,29 +507,40 @@ int train_fused(const pg_grid *g, const pg_mlp *m, const float *xs, const float 
     if (!acts && !(flags & PG_EXACT_MLP))
         return train_mma<ACC, LACC>(g, od, xs, targets, B, feats, baked, conf, params, scale, sig, gfeat, gconf,
                                     touched, gparams, loss_sum, dy_out, s);
-    const int smem = (int)sizeof(TrainSmem);
-    static bool configured[4] = {false, false, false, false};
-    int sms = 0, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static bool configured[8] = {};
+    static int sms = 0, groups = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const char *e = getenv("PG_TRAIN_GROUPS");   // tile pipelines per CTA (1 or 2)
+        groups = e && atoi(e) == 1 ? 1 : 2;
+    }
     const int64_t ntiles = (B + kT - 1) / kT;
-    const int grd = (int)(ntiles < 2 * sms ? ntiles : 2 * sms);
     const bool np4 = g->log2_np <= 2;
-#define PG_TRAIN_LAUNCH(D_, NP_, IDX)                                                                 \
+#define PG_TRAIN_LAUNCH1(D_, NP_, NG_, IDX)                                                           \
     do {                                                                                              \
-        auto kern = train_fused_kernel<float, D_, NP_, ACC, LACC>;                                    \
+        auto kern = train_fused_kernel<float, D_, NP_, ACC, LACC, NG_>;                               \
+        const int smem = (int)sizeof(TrainSmemT<NG_>);                                                \
         if (!configured[IDX]) {                                                                       \
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);            \
             configured[IDX] = true;                                                                   \
         }                                                                                             \
-        kern<<<grd, kNT, smem, s>>>(*g, xs, targets, B, feats, feats, baked, conf, params, od, scale,  \
-                                    sig, gfeat, gconf, touched, gparams, loss_sum, dy_out, acts);     \
+        const int64_t want = (ntiles + NG_ - 1) / NG_, cap = (int64_t)sms * (2 / NG_);                \
+        const int grd = (int)(want < cap ? want : cap);                                               \
+        kern<<<grd, kNT * NG_, smem, s>>>(*g, xs, targets, B, feats, feats, baked, conf, params, od,   \
+                                          scale, sig, gfeat, gconf, touched, gparams, loss_sum, dy_out, acts); \
+    } while (0)
+#define PG_TRAIN_LAUNCH(D_, NP_, IDX)                                                                 \
+    do {                                                                                              \
+        if (groups == 2) PG_TRAIN_LAUNCH1(D_, NP_, 2, (IDX) + 4); else PG_TRAIN_LAUNCH1(D_, NP_, 1, IDX); \
     } while (0)
     if (g->d == 2) {
         if (np4) PG_TRAIN_LAUNCH(2, 4, 0); else PG_TRAIN_LAUNCH(2, 16, 1);
     } else {
         if (np4) PG_TRAIN_LAUNCH(3, 4, 2); else PG_TRAIN_LAUNCH(3, 16, 3);
     }
+#undef PG_TRAIN_LAUNCH1
 #undef PG_TRAIN_LAUNCH
     return check_launch("train_fused");
 }
