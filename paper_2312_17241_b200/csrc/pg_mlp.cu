@@ -790,16 +790,17 @@ __global__ void wgrad_blas_reduce_kernel(const float *__restrict__ part, int64_t
 // per output over all B samples (~4 cycles per row: 0.53 ms for 2^18 rows,
 // the floor).  The chains are independent, so the columns are split across
 // CTAs (kBC per CTA, grid = column groups x layers) and each CTA streams only
-// its columns' 32-byte row slices through an NS-stage cp.async ring of
+// its columns' 16-byte row slices through an NS-stage cp.async ring of
 // shared memory; thread j < kBC runs column c0 + j's chain in row order while
 // the next NS-1 chunks are in flight (the previous one-CTA-per-layer kernel
-// waited for every 128-row chunk: 6.0 ms per C1 reference_order step).
-constexpr int kBC = 8, kBR = 256, kBNS = 5;   // 40 KB ring
+// waited for every 128-row chunk: 6.0 ms per C1 reference_order step; column
+// groups of 8 / 4 / 2 measured 4.2 / 3.6 / 3.3 ms per step).
+constexpr int kBC = 2, kBR = 1024, kBNS = 5, kBT = 256;   // 40 KB ring
 __device__ __forceinline__ void cp_async4(float *dst, const float *src) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
 }
-__global__ void __launch_bounds__(kBR) bias_blas_kernel(const float *__restrict__ d0, const float *__restrict__ d1,
+__global__ void __launch_bounds__(kBT) bias_blas_kernel(const float *__restrict__ d0, const float *__restrict__ d1,
                                                         const float *__restrict__ d2, int f0, int f1, int f2,
                                                         int64_t B, float *__restrict__ g0, float *__restrict__ g1,
                                                         float *__restrict__ g2) {
@@ -813,12 +814,17 @@ __global__ void __launch_bounds__(kBR) bias_blas_kernel(const float *__restrict_
     const int nc = fout - c0 < kBC ? fout - c0 : kBC;
     const int t = threadIdx.x;
     const int64_t nchunk = (B + kBR - 1) / kBR;
-    auto issue = [&](int64_t c) {   // thread t copies row c*kBR + t's nc columns
-        const int64_t row = c * kBR + t;
-        if (c < nchunk && row < B) {
-            float *dst = ring[c % kBNS] + t * kBC;
-            const float *src = d + row * fout + c0;
-            for (int q = 0; q < nc; ++q) cp_async4(dst + q, src + q);
+    auto issue = [&](int64_t c) {   // thread t copies rows c*kBR + t + i*kBT, nc columns each
+        if (c < nchunk) {
+#pragma unroll
+            for (int i = 0; i < kBR / kBT; ++i) {
+                const int64_t row = c * kBR + t + i * kBT;
+                if (row < B) {
+                    float *dst = ring[c % kBNS] + (t + i * kBT) * kBC;
+                    const float *src = d + row * fout + c0;
+                    for (int q = 0; q < nc; ++q) cp_async4(dst + q, src + q);
+                }
+            }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
@@ -893,7 +899,7 @@ int mlp_wgrad_blas(const pg_mlp *m, const float *acts, int64_t B, float *gparams
     {
         const int fmax = fo[0] > fo[1] ? (fo[0] > fo[2] ? fo[0] : fo[2]) : (fo[1] > fo[2] ? fo[1] : fo[2]);
         const dim3 grid((unsigned)((fmax + kBC - 1) / kBC), (unsigned)m->n_layers);
-        bias_blas_kernel<<<grid, kBR, 0, s>>>(dl[0], dl[1], dl[2], fo[0], fo[1], fo[2], B, gbl[0], gbl[1], gbl[2]);
+        bias_blas_kernel<<<grid, kBT, 0, s>>>(dl[0], dl[1], dl[2], fo[0], fo[1], fo[2], B, gbl[0], gbl[1], gbl[2]);
     }
     return check_launch("mlp_wgrad_blas");
 }
