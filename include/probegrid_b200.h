@@ -54,6 +54,9 @@ extern "C" {
 #define PG_SMEM_TABLES 32u    /* decode: force the shared-memory baked-index
                                * variant (default: automatic, N_p = 2 or 4) */
 #define PG_NO_SMEM_TABLES 64u /* decode: never use it                       */
+#define PG_TOUCH_ALL 256u     /* fused fp32 training: flag every probed lookup
+                                 as touched (data-parallel steps; see
+                                 pg_train_fused_f32) */
 #define PG_COMPOSITE 128u     /* fused training: volume compositing, one ray
                                * of 64 samples per tile; targets (B, 4) =
                                * (segment length, ray r, g, b) per sample */
@@ -230,7 +233,10 @@ int pg_decode_host_f32(const pg_grid *grid, const pg_mlp *mlp,
  * copy), and the D2H copy of each piece starts as soon as the kernel has
  * counted all of its tiles done (stream wait on a device counter).  chunk:
  * a power of two >= 128.  d_xs
- * holds B*d floats, d_out B*out_dim floats, d_flags 2*ceil(B/chunk) uint32.
+ * holds B*d floats, d_out B*out_dim floats, d_flags 2*ceil(B/chunk) + 1
+ * uint32 (per-chunk ready flags, per-chunk done counters, and in the last
+ * slot the number of tile pipelines that took the host fallback below).
+ * h_xs and h_out must be page-locked (checked; ValueError otherwise).
  * Needs the fused shape, the tensor-core MLP and stream memory operations:
  * pg_decode_stream_supported() says whether this call can run.  A chunk
  * whose flag has not arrived 2 ms after the kernel reached it (copies
@@ -280,7 +286,9 @@ int pg_mlp_train_f64(const pg_mlp *mlp, const double *y, const double *targets,
  * pg_encode_bwd does; touched[] is set only for lookups whose gconf
  * contribution is all zero/subnormal -- pg_lazy_adam_rebake_f32 also visits
  * every row with a non-zero gradient, which together is the reference's
- * touched set.
+ * touched set up to a row whose summed gradient cancels to exactly 0.0;
+ * flags & PG_TOUCH_ALL sets touched[] for every lookup instead (what a
+ * data-parallel step uses: the replicas' sums are added by the all-reduce).
  * flags & PG_EXACT_MLP: CUDA-core MLP in numpy/OpenBLAS's FMA-chain order, so
  * y, the loss terms and dL/dy equal the reference's bit for bit; touched[]
  * is set for every lookup.
@@ -433,10 +441,25 @@ int pg_lazy_adam_rebake_f64(double *conf, double *m, double *v,
                             double beta1, double beta2, double eps,
                             const double *d_guard, void *stream);
 
-/* touched flags as fp32 counts (for the data-parallel allreduce) and back */
+/* Full bake of `rows` confidence rows into baked indices: codebooks.py:147-152
+ * (np.argmax per row: first maximum, first NaN if any).  Replaces the
+ * reference's `bake` in init_model (model.py:150-156) and
+ * TrainState.check_bake_consistency (trainer.py:173-180). */
+int pg_bake_rows_f32(const float *conf, int64_t rows, int n_p, uint8_t *baked,
+                     void *stream);
+int pg_bake_rows_f64(const double *conf, int64_t rows, int n_p, uint8_t *baked,
+                     void *stream);
+
+/* touched flags as counts in the exchange buffer's element type (for the
+ * data-parallel allreduce: a float64 model's buffer holds doubles) and back
+ * (count > 0 -> touched: the union over replicas) */
 int pg_touched_to_f32(const uint8_t *touched, int64_t n, float *out,
                       void *stream);
 int pg_touched_from_f32(const float *in, int64_t n, uint8_t *touched,
+                        void *stream);
+int pg_touched_to_f64(const uint8_t *touched, int64_t n, double *out,
+                      void *stream);
+int pg_touched_from_f64(const double *in, int64_t n, uint8_t *touched,
                         void *stream);
 
 /* Self-test of the tcgen05 (UMMA) path: one CTA computes

@@ -19,6 +19,7 @@ PG_LEVEL_DENSE, PG_LEVEL_HASHED, PG_LEVEL_PROBED = 0, 1, 2
 PG_EXACT_MLP, PG_SIGMOID, PG_SURROGATE, PG_HALF_FEATS, PG_NO_TENSOR = 1, 2, 4, 8, 16
 PG_SMEM_TABLES, PG_NO_SMEM_TABLES = 32, 64
 PG_COMPOSITE = 128
+PG_TOUCH_ALL = 256
 
 
 class PgGrid(ctypes.Structure):
@@ -85,6 +86,10 @@ _SIGS.update({
     "pg_decode_host_stream_f32": [_G, _M, _P, _I64, _P, _P, _P, ctypes.c_uint, _I64, _P, _P, _P, _P, _P, _P, _P],
     "pg_nerf_train_f32": [_M, _P, _P, _P, _I64, _I, _P, _F, _P, _P, _P, _P, _P],
     "pg_touched_from_f32": [_P, _I64, _P, _P],
+    "pg_touched_to_f64": [_P, _I64, _P, _P],
+    "pg_bake_rows_f32": [_P, _I64, _I, _P, _P],
+    "pg_bake_rows_f64": [_P, _I64, _I, _P, _P],
+    "pg_touched_from_f64": [_P, _I64, _P, _P],
     "pg_train_fused_f32": [_G, _M, _P, _P, _I64, _P, _P, _P, _P, _F, ctypes.c_uint, _P, _P, _P,
                            _P, _P, _P, _P],
     "pg_train_fused_ref_f32": [_G, _M, _P, _P, _I64, _P, _P, _P, _P, _F, ctypes.c_uint, _P, _P,
@@ -167,6 +172,34 @@ def ptr(t) -> ctypes.c_void_p:
     if t is None:
         return ctypes.c_void_p(0)
     return ctypes.c_void_p(t.data_ptr())
+
+
+def _device_of(obj):
+    for o in (obj, getattr(obj, "model", None), getattr(obj, "inf", None), getattr(obj, "state", None)):
+        dev = getattr(o, "device", None)
+        if dev is not None:
+            return dev
+    return None
+
+
+def on_device(fn):
+    """Run a host entry point with its object's CUDA device current.
+
+    The library launches on the current device and on that device's current
+    stream (stream_ptr), so a model living on cuda:1 must make cuda:1
+    current around every call; the first positional argument (a Model,
+    InferenceModel, TrainState, HostDecoder, or a tensor) names the device."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(*args, **kw):
+        import torch
+        dev = _device_of(args[0]) if args else None
+        if dev is None or torch.device(dev).type != "cuda":
+            return fn(*args, **kw)
+        with torch.cuda.device(dev):
+            return fn(*args, **kw)
+    return wrapped
 
 
 def stream_ptr(stream=None) -> ctypes.c_void_p:

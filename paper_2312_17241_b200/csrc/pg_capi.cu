@@ -36,21 +36,26 @@ int pg_device_sm_count(int device) {
 // Roofline probes used by bench.py to MEASURE the L2 denominators the
 // gather/scatter kernels are judged against (MEASURED_PEAKS.json has HBM and
 // tensor peaks only).
-//   stream read : float4 grid-stride sum over an L2-resident buffer, reps times
+//   stream read : coalesced float4 grid-stride sum over an L2-resident buffer,
+//                 reps times: thread i of the grid reads float4 i + k*stride,
+//                 so every warp load is 512 contiguous bytes (16 full
+//                 sectors); ld.global.cg keeps it in L2 (the buffer's
+//                 per-SM slice would otherwise sit in L1 after rep 1)
 //   random gather: 8-byte loads at hashed indices of a 2^k-entry table
 // ---------------------------------------------------------------------------
 namespace pg {
 __global__ void probe_stream_kernel(const float4 *__restrict__ buf, int64_t n4, int reps,
                                     float *__restrict__ sink) {
-    // 4 independent 16-byte L2 loads in flight per thread per iteration
+    // 4 independent coalesced 16-byte loads in flight per thread per iteration
     float acc = 0.0f;
-    // (n4 must be a multiple of 4: bytes a multiple of 64)
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
     for (int r = 0; r < reps; ++r)
-        for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < n4; i += stride) {
-            const float4 a = __ldcg(buf + i), b = __ldcg(buf + i + 1);
-            const float4 c = __ldcg(buf + i + 2), d = __ldcg(buf + i + 3);
-            acc += (a.x + b.y) + (c.z + d.w);
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += 4 * nt) {
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                v[u] = i + u * nt < n4 ? __ldcg(buf + i + u * nt) : make_float4(0.f, 0.f, 0.f, 0.f);
+            acc += (v[0].x + v[1].y) + (v[2].z + v[3].w);
         }
     if (acc == 12345.678f) *sink = acc;
 }

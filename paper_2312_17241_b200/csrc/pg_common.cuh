@@ -31,6 +31,46 @@ int check_launch(const char *what);
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// ---- per-device state: the library launches on the caller's current
+// device, so every cached device property and every one-time kernel
+// attribute (cudaFuncSetAttribute is per device) is keyed by it
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d >= 0 && d < kMaxDevices ? d : 0;
+}
+inline int device_sms() {
+    static int sms[kMaxDevices] = {};
+    const int d = current_device();
+    if (!sms[d]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+        sms[d] = v > 0 ? v : 148;
+    }
+    return sms[d];
+}
+inline int device_optin_smem() {
+    static int optin[kMaxDevices] = {};
+    const int d = current_device();
+    if (!optin[d]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, d);
+        optin[d] = v > 0 ? v : 48 * 1024;
+    }
+    return optin[d];
+}
+// true the first time it is asked on the current device
+struct DeviceOnce {
+    bool done[kMaxDevices] = {};
+    bool first() {
+        const int d = current_device();
+        if (done[d]) return false;
+        done[d] = true;
+        return true;
+    }
+};
+
 inline int grid_for(int64_t n, int block, int64_t cap = (int64_t)1 << 30) {
     int64_t g = (n + block - 1) / block;
     if (g < 1) g = 1;
@@ -201,23 +241,30 @@ struct DecodeStream {
     int chunk_tiles_log2 = 0;   // chunks are 2^k tiles of 128 queries
     uint64_t timeout_ns = 0;
     const float *host_xs = nullptr;   // pinned host copy of the inputs (fallback)
+    uint32_t *fallbacks = nullptr;    // groups that took the host fallback (counted)
 };
 
 // poll a flag written by the stream front end after a copy; false if it
-// does not arrive within timeout_ns.  Relaxed polling: an acquire would
-// invalidate L1 (the tables' cache) on every check; the data behind the flag
-// is then read with L2-coherent ld.cg loads issued after the flag was
-// observed (control dependency + group barrier).
+// does not arrive within timeout_ns.  Relaxed polling (an acquire invalidates
+// L1 — the tables' cache — CCTL.IVALL in SASS, so not on every check); once
+// the flag is seen set, ONE ld.acquire of it orders the caller's later loads
+// of the data behind it (the chunk's coordinates, read by the whole group
+// after a bar.sync) after the copy that preceded the flag write.
+__device__ __forceinline__ bool acquire_flag(const uint32_t *f) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    return v != 0;
+}
 __device__ __forceinline__ bool wait_flag(const uint32_t *f, uint64_t timeout_ns) {
     uint32_t v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-    if (v) return true;
+    if (v) return acquire_flag(f);
     uint64_t t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (;;) {
         __nanosleep(128);
         asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-        if (v) return true;
+        if (v) return acquire_flag(f);
         uint64_t t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         if (t - t0 > timeout_ns) return false;

@@ -325,7 +325,10 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
                 // this kernel: profilers, CUDA_LAUNCH_BLOCKING) is not an
                 // error: the group then reads its inputs from pinned host
                 // memory directly (they are there already)
-                if (!G.host && !tc::wait_flag(st.ready + G.seen, st.timeout_ns)) G.host = 1;
+                if (!G.host && !tc::wait_flag(st.ready + G.seen, st.timeout_ns)) {
+                    G.host = 1;
+                    atomicAdd(st.fallbacks, 1u);
+                }
             }
             group_sync(grp);
         }
@@ -504,15 +507,10 @@ template <typename FT, int D, int NG, int MINB, int MODE>
 static void launch_umma(const pg_grid *g, const tc::TabPlan &plan, int smem, int grd, const float *xs,
                          int64_t B, const void *feats, const uint8_t *baked, const float *params, int od,
                          int sig, float *out, const tc::Stream &st, cudaStream_t s) {
-    static bool configured = false;
-    if (!configured) {
-        int dev = 0, optin = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    static DeviceOnce configured;
+    if (configured.first())
         cudaFuncSetAttribute(decode_umma_kernel<FT, D, NG, MINB, MODE>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-        configured = true;
-    }
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, device_optin_smem());
     decode_umma_kernel<FT, D, NG, MINB, MODE><<<grd, tc::kGT * NG, smem, s>>>(*g, plan, xs, B, (const FT *)feats,
                                                                            baked, params, od, sig, out, st);
 }
@@ -520,16 +518,10 @@ static void launch_umma(const pg_grid *g, const tc::TabPlan &plan, int smem, int
 int decode_umma(const pg_grid *g, int od, const float *xs, int64_t B, const void *feats, bool half,
                 const uint8_t *baked, const float *params, int sig, int table_flags, float *out, cudaStream_t s,
                 const tc::Stream &st) {
-    static int sms = 0, optin = 0, env_budget = -1, env_kinds = 2;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        // tuning knobs for the table variant (ablations in tools/gpu_decode_ab.sh)
-        if (const char *e = getenv("PG_DECODE_TABLE_BYTES")) env_budget = atoi(e);
-        if (const char *k = getenv("PG_DECODE_TABLE_KINDS")) env_kinds = atoi(k);  // 1 dense, 2 baked
-    }
+    // tuning knobs for the table variant (ablations in tools/gpu_decode_ab.sh)
+    static const int env_budget = getenv("PG_DECODE_TABLE_BYTES") ? atoi(getenv("PG_DECODE_TABLE_BYTES")) : -1;
+    static const int env_kinds = getenv("PG_DECODE_TABLE_KINDS") ? atoi(getenv("PG_DECODE_TABLE_KINDS")) : 2;
+    const int sms = device_sms(), optin = device_optin_smem();
     // Shared-memory tables: the three pipelines of a CTA share <= 64 KB of
     // bit-packed baked indices, so that smem + L1 stay inside the 196 KB
     // carve-out and L1 keeps ~60 KB.  On for N_p = 2 and 4 (measured with the

@@ -165,13 +165,7 @@ __global__ void __launch_bounds__(256) encode_bwd_kernel(
 
 
 static int encode_blocks(int64_t B) {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
+    const int sms = device_sms();
     const int64_t nchunks = (B + kChunk - 1) / kChunk;
     const int64_t cap = (int64_t)sms * 8;
     return (int)(nchunks < cap ? nchunks : cap);

@@ -138,7 +138,8 @@ __device__ __forceinline__ void encode_level_bwd2(const pg_grid &g, int l, const
                                                   const float *__restrict__ conf,
                                                   ACC *__restrict__ gfeat,
                                                   ACC *__restrict__ gconf,
-                                                  uint8_t *__restrict__ touched) {
+                                                  uint8_t *__restrict__ touched,
+                                                  bool touch_all = false) {
     constexpr int C = 1 << D;
     const uint32_t nf_mask = (uint32_t)g.n_f - 1u, nc_mask = (uint32_t)g.n_c - 1u;
     const int res = g.res[l], kind = g.kind[l];
@@ -258,7 +259,11 @@ __device__ __forceinline__ void encode_level_bwd2(const pg_grid &g, int l, const
 #pragma unroll
                 for (int j = 0; j < NPMAX; ++j)
                     if (j < n_p) live |= fabsf(sg[j] * (dots[j] - s)) >= 1.17549435e-38f;
-                if (!live) touched[crow[k]] = 1;
+                // touch_all (data-parallel steps): every lookup flags its
+                // row, so a row whose replicas' contributions cancel to an
+                // exact 0.0 after the all-reduce is still updated, as the
+                // reference's lazy Adam updates every touched row
+                if (!live || touch_all) touched[crow[k]] = 1;
             }
             encode_probe_reds<NPMAX, ACC>(gb, gc, n_p, sg, dots, s, g0, g1);
         }

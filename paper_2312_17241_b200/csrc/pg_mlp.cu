@@ -328,28 +328,17 @@ static bool decode_fast_ok(const pg_grid *g, const pg_mlp *m) {
            m->widths[1] == kHid && m->widths[2] == kHid && m->widths[3] >= 1 && m->widths[3] <= kOutMax;
 }
 
-static int sm_count() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
-}
+static int sm_count() { return device_sms(); }
 
 template <typename FT, int D, bool EXACT>
 static void launch_decode(const pg_grid *g, const float *xs, int64_t B, const void *feats,
                           const uint8_t *baked, const float *params, int out_dim, int sig,
                           float *out, int32_t *bad, cudaStream_t s) {
-    static bool configured = false;
+    static DeviceOnce configured;
     const int smem = (int)sizeof(DecodeSmem);
-    if (!configured) {
+    if (configured.first())
         cudaFuncSetAttribute(decode_fused_kernel<FT, D, EXACT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        configured = true;
-    }
     const int64_t ntiles = (B + kTP - 1) / kTP;
     const int64_t want = (ntiles + 1) / 2, cap = (int64_t)sm_count();
     const int grd = (int)(want < cap ? want : cap);
@@ -1022,6 +1011,15 @@ int pg_decode_stream_supported(const pg_grid *grid, const pg_mlp *mlp, unsigned 
     return grid && mlp && decode_fast_ok(grid, mlp) && !(flags & (PG_EXACT_MLP | PG_NO_TENSOR)) && stream_memops();
 }
 
+static bool is_pinned_host(const void *p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 int pg_decode_host_stream_f32(const pg_grid *grid, const pg_mlp *mlp, const float *h_xs, int64_t B,
                               const void *feats, const uint8_t *baked, const float *params, unsigned flags,
                               int64_t chunk, float *d_xs, float *d_out, uint32_t *d_flags, float *h_out,
@@ -1033,6 +1031,10 @@ int pg_decode_host_stream_f32(const pg_grid *grid, const pg_mlp *mlp, const floa
     PG_REQUIRE(chunk >= 128 && (chunk & (chunk - 1)) == 0, "chunk must be a power of two >= 128 queries");
     PG_REQUIRE(B >= 0 && (B == 0 || (h_xs && d_xs && d_out && d_flags && h_out)), "null buffer");
     if (B == 0) return PG_OK;
+    // a group whose chunk flag times out reads the inputs from h_xs through
+    // UVA: it must be page-locked host memory
+    PG_REQUIRE(is_pinned_host(h_xs) && is_pinned_host(h_out),
+               "streaming decode needs page-locked (pinned) host buffers");
     const int d = grid->d, od = mlp->widths[3];
     const int64_t nch = (B + chunk - 1) / chunk;
     cudaStream_t si = as_stream(stream_in), sk = as_stream(stream_compute), so = as_stream(stream_out);
@@ -1040,7 +1042,7 @@ int pg_decode_host_stream_f32(const pg_grid *grid, const pg_mlp *mlp, const floa
     cudaEvent_t ev0;
     cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
     const bool dbg_nocopy = getenv("PG_DEBUG_STREAM_NOCOPY") != nullptr;   // kernel-only probe
-    cudaMemsetAsync(d_flags, 0, sizeof(uint32_t) * 2 * nch, sk);
+    cudaMemsetAsync(d_flags, 0, sizeof(uint32_t) * (2 * nch + 1), sk);
     if (dbg_nocopy) cudaMemsetAsync(d_flags, 1, sizeof(uint32_t) * nch, sk);
     cudaEventRecord(ev0, sk);
     cudaStreamWaitEvent(si, ev0, 0);
@@ -1051,6 +1053,7 @@ int pg_decode_host_stream_f32(const pg_grid *grid, const pg_mlp *mlp, const floa
     while ((128ll << st.chunk_tiles_log2) < chunk) ++st.chunk_tiles_log2;
     st.timeout_ns = 2ull * 1000 * 1000;   // then read from host memory (see the kernel)
     st.host_xs = h_xs;
+    st.fallbacks = d_flags + 2 * nch;
     const bool half = (flags & PG_HALF_FEATS) != 0;
     static const bool dbg = getenv("PG_DEBUG_STREAM") != nullptr;
     cudaEvent_t dk0 = nullptr, dk1 = nullptr, dend = nullptr;
@@ -1100,14 +1103,6 @@ int pg_decode_host_stream_f32(const pg_grid *grid, const pg_mlp *mlp, const floa
 // flags or extra device memory (measured 5.50 ms per 2^24 queries vs 5.22
 // for the streaming path; a variant prefetching each tile's coordinates a
 // tile ahead spilled at the 80-register cap and ran 5.62 ms).
-static bool is_pinned_host(const void *p) {
-    cudaPointerAttributes a;
-    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    return a.type == cudaMemoryTypeHost;
-}
 
 int pg_decode_host_zc_f32(const pg_grid *grid, const pg_mlp *mlp, const float *h_xs, int64_t B,
                           const void *feats, const uint8_t *baked, const float *params, unsigned flags,

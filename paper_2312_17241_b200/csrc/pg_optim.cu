@@ -91,6 +91,34 @@ __global__ void lazy_adam_rebake_kernel(T *conf, T *m, T *v, uint8_t *baked, T *
     }
 }
 
+// full bake (codebooks.py:147-152): np.argmax over each row, i.e. the first
+// maximum, or the first NaN if the row holds one (numpy's argmax treats NaN
+// as the maximum).  The incremental re-bake in adam_row is the Cython core's
+// strict '>' scan (_core.pyx:265-272); the two agree on every finite row.
+template <typename T>
+__global__ void bake_rows_kernel(const T *conf, int64_t rows, int n_p, uint8_t *baked) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const T *cp = conf + r * n_p;
+        T best = cp[0];
+        int best_j = 0;
+        if (!isnan(best)) {
+            for (int j = 1; j < n_p; ++j) {
+                const T c = cp[j];
+                if (isnan(c)) {
+                    best_j = j;
+                    break;
+                }
+                if (c > best) {
+                    best = c;
+                    best_j = j;
+                }
+            }
+        }
+        baked[r] = (uint8_t)best_j;
+    }
+}
+
 // deterministic mode: fixed-point accumulators -> float gradients (added),
 // accumulators cleared for the next step
 __global__ void fx_accumulate_kernel(fx_t *fx, int64_t n, float *dst) {
@@ -108,13 +136,17 @@ __global__ void fx_loss_kernel(fx_t *fx, double *loss) {
     fx[0] = 0;
 }
 
-__global__ void touched_to_f32_kernel(const uint8_t *t, int64_t n, float *o) {
+// touched flags <-> slots of the exchange buffer, in the buffer's own
+// element type (a float64 model's gradient buffer holds doubles)
+template <typename T>
+__global__ void touched_to_kernel(const uint8_t *t, int64_t n, T *o) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) o[i] = (float)t[i];
+    if (i < n) o[i] = (T)t[i];
 }
-__global__ void touched_from_f32_kernel(const float *in, int64_t n, uint8_t *t) {
+template <typename T>
+__global__ void touched_from_kernel(const T *in, int64_t n, uint8_t *t) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) t[i] = in[i] > 0.0f ? 1 : 0;
+    if (i < n) t[i] = in[i] > (T)0 ? 1 : 0;
 }
 
 // ---- pixel batch (trainer.py:109-116): x = ((col+.5)/W, (row+.5)/H) in
@@ -248,6 +280,18 @@ int pg_adam_rebake_rows_f64(double *conf, double *m, double *v, int n_p, uint8_t
     return launch_rows<double>(conf, m, v, n_p, baked, rows_u, U, gconf_u, corr1, corr2, lr, b1, b2,
                                eps, stream);
 }
+int pg_bake_rows_f32(const float *conf, int64_t rows, int n_p, uint8_t *baked, void *stream) {
+    PG_REQUIRE(n_p >= 1 && n_p <= PG_MAX_PROBES, "n_p out of range");
+    if (rows == 0) return PG_OK;
+    bake_rows_kernel<float><<<grid_for(rows, 256, 148 * 16), 256, 0, as_stream(stream)>>>(conf, rows, n_p, baked);
+    return check_launch("bake_rows");
+}
+int pg_bake_rows_f64(const double *conf, int64_t rows, int n_p, uint8_t *baked, void *stream) {
+    PG_REQUIRE(n_p >= 1 && n_p <= PG_MAX_PROBES, "n_p out of range");
+    if (rows == 0) return PG_OK;
+    bake_rows_kernel<double><<<grid_for(rows, 256, 148 * 16), 256, 0, as_stream(stream)>>>(conf, rows, n_p, baked);
+    return check_launch("bake_rows");
+}
 int pg_fx_accumulate_f32(uint64_t *fx, int64_t n, float *dst, void *stream) {
     if (n == 0) return PG_OK;
     fx_accumulate_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, as_stream(stream)>>>((fx_t *)fx, n, dst);
@@ -259,13 +303,23 @@ int pg_fx_loss(uint64_t *fx, double *loss_sum, void *stream) {
 }
 int pg_touched_to_f32(const uint8_t *touched, int64_t n, float *out, void *stream) {
     if (n == 0) return PG_OK;
-    touched_to_f32_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(touched, n, out);
+    touched_to_kernel<float><<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(touched, n, out);
     return check_launch("touched_to_f32");
 }
 int pg_touched_from_f32(const float *in, int64_t n, uint8_t *touched, void *stream) {
     if (n == 0) return PG_OK;
-    touched_from_f32_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(in, n, touched);
+    touched_from_kernel<float><<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(in, n, touched);
     return check_launch("touched_from_f32");
+}
+int pg_touched_to_f64(const uint8_t *touched, int64_t n, double *out, void *stream) {
+    if (n == 0) return PG_OK;
+    touched_to_kernel<double><<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(touched, n, out);
+    return check_launch("touched_to_f64");
+}
+int pg_touched_from_f64(const double *in, int64_t n, uint8_t *touched, void *stream) {
+    if (n == 0) return PG_OK;
+    touched_from_kernel<double><<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(in, n, touched);
+    return check_launch("touched_from_f64");
 }
 int pg_pixel_batch_f32(const int64_t *pix_in, int64_t B, int width, int height, const float *image,
                        int channels, uint64_t seed, uint64_t step, int64_t *pix_out, float *xs,

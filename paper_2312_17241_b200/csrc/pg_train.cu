@@ -495,37 +495,31 @@ int train_fused(const pg_grid *g, const pg_mlp *m, const float *xs, const float 
     if (B == 0) return PG_OK;
     const int od = m->widths[3];
     const int sig = (flags & PG_SIGMOID) ? 1 : 0;
+    const int touch_all = (flags & PG_TOUCH_ALL) ? 4 : 0;
     if (flags & PG_COMPOSITE) {
         // one 64-sample tile = one ray of 64 samples (pg_train_mma.cu)
         PG_REQUIRE(od == 4 && !sig && !(flags & PG_EXACT_MLP) && !acts && B % 64 == 0,
                    "PG_COMPOSITE: out_dim 4, no sigmoid, tensor-core MLP, B a multiple of 64 samples");
-        return train_mma<ACC, LACC>(g, od, xs, targets, B, feats, baked, conf, params, scale, 2, gfeat, gconf,
+        return train_mma<ACC, LACC>(g, od, xs, targets, B, feats, baked, conf, params, scale, 2 | touch_all, gfeat, gconf,
                                     touched, gparams, loss_sum, dy_out, s);
     }
     // fast path: tensor-core MLP (pg_train_mma.cu); this file's FFMA kernel is
     // the OpenBLAS-order path (PG_EXACT_MLP, reference-order mode)
     if (!acts && !(flags & PG_EXACT_MLP))
-        return train_mma<ACC, LACC>(g, od, xs, targets, B, feats, baked, conf, params, scale, sig, gfeat, gconf,
+        return train_mma<ACC, LACC>(g, od, xs, targets, B, feats, baked, conf, params, scale, sig | touch_all, gfeat, gconf,
                                     touched, gparams, loss_sum, dy_out, s);
-    static bool configured[8] = {};
-    static int sms = 0, groups = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const char *e = getenv("PG_TRAIN_GROUPS");   // tile pipelines per CTA (1 or 2)
-        groups = e && atoi(e) == 1 ? 1 : 2;
-    }
+    static DeviceOnce configured[8];
+    const int sms = device_sms();
+    // tile pipelines per CTA (1 or 2)
+    static const int groups = getenv("PG_TRAIN_GROUPS") && atoi(getenv("PG_TRAIN_GROUPS")) == 1 ? 1 : 2;
     const int64_t ntiles = (B + kT - 1) / kT;
     const bool np4 = g->log2_np <= 2;
 #define PG_TRAIN_LAUNCH1(D_, NP_, NG_, IDX)                                                           \
     do {                                                                                              \
         auto kern = train_fused_kernel<float, D_, NP_, ACC, LACC, NG_>;                               \
         const int smem = (int)sizeof(TrainSmemT<NG_>);                                                \
-        if (!configured[IDX]) {                                                                       \
+        if (configured[IDX].first())                                                                  \
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);            \
-            configured[IDX] = true;                                                                   \
-        }                                                                                             \
         const int64_t want = (ntiles + NG_ - 1) / NG_, cap = (int64_t)sms * (2 / NG_);                \
         const int grd = (int)(want < cap ? want : cap);                                               \
         kern<<<grd, kNT * NG_, smem, s>>>(*g, xs, targets, B, feats, feats, baked, conf, params, od,   \

@@ -235,10 +235,13 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
                      int64_t B, const FT *__restrict__ feats_fwd, const float *__restrict__ feats,
                      const uint8_t *__restrict__ baked, const float *__restrict__ conf,
                      const float *__restrict__ params, int od, float scale,
-                     int sigmoid,   // 1: logistic output; 2: volume compositing (one ray per tile)
+                     int mode_flags,   // bits 0-1: 1 logistic output, 2 volume compositing (one ray
+                                       // per tile); bit 2: flag every probed lookup as touched
                      ACC *__restrict__ gfeat, ACC *__restrict__ gconf, uint8_t *__restrict__ touched,
                      ACC *__restrict__ gparams, LACC *__restrict__ loss_sum, float *__restrict__ dy_out) {
     using namespace tm;
+    const int sigmoid = mode_flags & 3;
+    const bool touch_all = (mode_flags & 4) != 0;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SmemT<NG> &S = *reinterpret_cast<SmemT<NG> *>(smem_raw);
     const int gid = NG == 1 ? 0 : (int)(threadIdx.x >> 8);   // tile pipeline
@@ -499,7 +502,7 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
             }
             if (pl < nv)
                 encode_level_bwd2<D, NPM, ACC, std::is_same<ACC, float>::value>(g, l, x, GDY[(2 * l) * kS + pl], GDY[(2 * l + 1) * kS + pl],
-                                               feats, conf, gfeat, gconf, touched);
+                                               feats, conf, gfeat, gconf, touched, touch_all);
         }
 #pragma unroll
         for (int a = 0; a < D; ++a) x[a] = xn[a];
@@ -564,25 +567,18 @@ template <typename ACC, typename LACC>
 int train_mma(const pg_grid *g, int od, const float *xs, const float *targets, int64_t B, const float *feats,
               const uint8_t *baked, const float *conf, const float *params, float scale, int sig, ACC *gfeat,
               ACC *gconf, uint8_t *touched, ACC *gparams, LACC *loss_sum, float *dy_out, cudaStream_t s) {
-    static bool configured[12] = {};
-    static int sms = 0, groups = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const char *e = getenv("PG_TRAIN_GROUPS");   // tile pipelines per CTA (1 or 2)
-        groups = e && atoi(e) == 1 ? 1 : 2;
-    }
+    static DeviceOnce configured[12];
+    const int sms = device_sms();
+    // tile pipelines per CTA (1 or 2)
+    static const int groups = getenv("PG_TRAIN_GROUPS") && atoi(getenv("PG_TRAIN_GROUPS")) == 1 ? 1 : 2;
     const int64_t ntiles = (B + tm::kT - 1) / tm::kT;
     const int npm = g->log2_np <= 2 ? 4 : g->log2_np == 3 ? 8 : 16;   // probing range held in registers
 #define PG_TRAIN_MMA(D_, NP_, NG_, IDX)                                                               \
     do {                                                                                              \
         auto kern = train_mma_kernel<float, D_, NP_, ACC, LACC, NG_>;                                 \
         const int smem = (int)sizeof(tm::SmemT<NG_>);                                                 \
-        if (!configured[IDX]) {                                                                       \
+        if (configured[IDX].first())                                                                  \
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);            \
-            configured[IDX] = true;                                                                   \
-        }                                                                                             \
         const int64_t want = (ntiles + NG_ - 1) / NG_, cap = (int64_t)sms * (2 / NG_);                \
         const int grd = (int)(want < cap ? want : cap);                                               \
         kern<<<grd, tm::kNT * NG_, smem, s>>>(*g, xs, targets, B, feats, feats, baked, conf, params, od, \

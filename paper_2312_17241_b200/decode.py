@@ -20,6 +20,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from ._lib import on_device
 from .errors import DomainViolation, UnbakedModel
 from .grid_model import Model
 from .hyper import HyperParams, build_level_specs, grid_struct, mlp_struct
@@ -73,6 +74,7 @@ class InferenceModel:
         return cls(hyper, width, height, f, bk, probed, torch.from_numpy(flat), device)
 
 
+@on_device
 def to_inference(model: Model, width: int = 0, height: int = 0) -> InferenceModel:
     """Downcast a trained device model to its storable half-precision form."""
     if model.probed and model.baked.numel() == 0:
@@ -96,6 +98,7 @@ def _flags(inf: InferenceModel, exact: bool, tensor: bool = True, smem_tables=No
     return f
 
 
+@on_device
 def decode_device(inf: InferenceModel, xs: torch.Tensor, out: torch.Tensor = None,
                   exact: bool = True, stream=None, tensor: bool = True,
                   smem_tables=None) -> torch.Tensor:
@@ -120,6 +123,7 @@ def decode_device(inf: InferenceModel, xs: torch.Tensor, out: torch.Tensor = Non
     return out
 
 
+@on_device
 def decode_pixels(inf: InferenceModel, xs, counter: TouchCounter | None = None,
                   exact: bool = True):
     """Decode arbitrary coordinates (numpy in -> numpy out, or CUDA tensor in
@@ -159,6 +163,7 @@ def grid_coords(width: int, height: int, x0: int, y0: int, x1: int, y1: int) -> 
                     axis=1).astype(np.float32)
 
 
+@on_device
 def decode_rect(inf: InferenceModel, rect, width: int | None = None,
                 height: int | None = None, exact: bool = True) -> np.ndarray:
     """Decode the half-open pixel rectangle (x0, y0, x1, y1) (model_io.py:327-339)."""
@@ -200,6 +205,7 @@ class HostDecoder:
     pg_decode_host_f32 — successive chunks on three streams, two buffer
     slots, event-ordered."""
 
+    @on_device
     def __init__(self, inf: InferenceModel, chunk: int = 1 << 21, exact: bool = False,
                  stream: bool | None = None, stream_chunk: int = 1 << 18):
         if not inf.fast:
@@ -216,6 +222,7 @@ class HostDecoder:
         self.s_k = torch.cuda.Stream(device=inf.device)
         self.s_out = torch.cuda.Stream(device=inf.device)
         self._cap = 0
+        self.fallbacks = 0
         if not self.streaming:
             self.d_xs = torch.empty(2 * chunk * d, dtype=torch.float32, device=inf.device)
             self.d_out = torch.empty(2 * chunk * od, dtype=torch.float32, device=inf.device)
@@ -227,9 +234,11 @@ class HostDecoder:
         self.d_xs = torch.empty(B * inf.hyper.d, dtype=torch.float32, device=inf.device)
         self.d_out = torch.empty(B * inf.out_dim, dtype=torch.float32, device=inf.device)
         n = -(-B // self.stream_chunk)
-        self.d_flags = torch.empty(2 * n, dtype=torch.int32, device=inf.device)
+        # [ready per chunk | done per chunk | host-fallback count]
+        self.d_flags = torch.empty(2 * n + 1, dtype=torch.int32, device=inf.device)
         self._cap = B
 
+    @on_device
     def __call__(self, h_xs: torch.Tensor, h_out: torch.Tensor) -> torch.Tensor:
         inf = self.inf
         assert h_xs.is_pinned() and h_out.is_pinned(), "host buffers must be pinned"
@@ -242,6 +251,8 @@ class HostDecoder:
                       _lib.ptr(inf.feats16), _lib.ptr(inf.baked), _lib.ptr(inf.params),
                       _flags(inf, self.exact), self.stream_chunk, _lib.ptr(self.d_xs), _lib.ptr(self.d_out),
                       _lib.ptr(self.d_flags), _lib.ptr(h_out), *streams)
+            n = -(-B // self.stream_chunk)
+            self.fallbacks = int(self.d_flags[2 * n])   # pipelines that read inputs from host memory
             return h_out
         _lib.call("pg_decode_host_f32", inf.grid, inf.mlp_desc, _lib.ptr(h_xs), h_xs.shape[0],
                   _lib.ptr(inf.feats16), _lib.ptr(inf.baked), _lib.ptr(inf.params),

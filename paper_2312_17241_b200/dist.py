@@ -45,8 +45,10 @@ class DataParallel:
         st.apply_updates()
 
     def step(self) -> float:
+        """One data-parallel step; raises TrainingDiverged (and keeps the
+        step count) on a non-finite global loss, like TrainState.step."""
         self.launch_step()
-        return self.state.loss_value()
+        return self.state.finish_step()
 
 
 def shard_range(n: int, rank: int, world: int):

@@ -16,6 +16,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from ._lib import on_device
 from .errors import DomainViolation, StaleTrace
 from .grid_model import Model
 
@@ -55,6 +56,7 @@ def _prepare_xs(model: Model, xs, check_domain: bool):
     return torch.from_numpy(a).to(model.device), True
 
 
+@on_device
 def encode_forward_device(model: Model, xs: torch.Tensor, y: torch.Tensor = None,
                           surrogate: bool = False, bad: torch.Tensor = None, stream=None):
     """Launch the fused forward on device tensors; returns y (B, L*F)."""
@@ -69,6 +71,7 @@ def encode_forward_device(model: Model, xs: torch.Tensor, y: torch.Tensor = None
     return y
 
 
+@on_device
 def encode_backward_device(model: Model, xs: torch.Tensor, dy: torch.Tensor, stream=None,
                            deterministic: bool = False, flush: bool = True):
     """Launch the fused backward: accumulate into model.grads / touched.
@@ -89,6 +92,7 @@ def encode_backward_device(model: Model, xs: torch.Tensor, dy: torch.Tensor, str
               _lib.ptr(model.gconf), _lib.ptr(model.touched), _lib.stream_ptr(stream))
 
 
+@on_device
 def encode_forward(model: Model, xs, surrogate: bool = False):
     """Encode a batch; returns (features (B, L*F), trace).
 
@@ -106,6 +110,7 @@ def encode_forward(model: Model, xs, surrogate: bool = False):
     return (y.cpu().numpy() if was_numpy else y), trace
 
 
+@on_device
 def encode_backward(model: Model, trace: EncodeTrace, upstream, deterministic: bool = False) -> None:
     """Accumulate codebook gradients from an encoded batch (encoding.py:119-133).
     deterministic=True: order-independent fixed-point accumulation (float32)."""

@@ -26,6 +26,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from ._lib import on_device
 from .hyper import (SEED_CONFIDENCE, SEED_FEATURES, SEED_MLP, HyperParams, LevelMode, LevelSpec,
                     build_level_specs, grid_struct, mlp_struct, seeded_rng)
 
@@ -192,6 +193,7 @@ class Model:
         return (_lib.ctypes.c_void_p(base), _lib.ctypes.c_void_p(base + 8 * self.n_feat),
                 _lib.ctypes.c_void_p(base + 8 * self.off_gconf))
 
+    @on_device
     def fx_flush(self, loss_sum=None, stream=None) -> None:
         """Add the fixed-point accumulators into the float gradients (and the
         loss into loss_sum), clearing them."""
@@ -213,9 +215,19 @@ class Model:
         """Full argmax bake of every probed level (codebooks.py:147-152; ties
         to the smallest probe like the strict '>' scan)."""
         if self.probed:
-            self.baked.copy_(torch.argmax(self.conf, dim=-1).to(torch.uint8))
+            self.bake_into(self.baked)
+
+    @on_device
+    def bake_into(self, out: torch.Tensor) -> torch.Tensor:
+        """np.argmax of every confidence row (codebooks.py:151-152) into `out`
+        (P, n_c) uint8, on the device."""
+        sfx = "f64" if self.tdtype == torch.float64 else "f32"
+        _lib.call(f"pg_bake_rows_{sfx}", _lib.ptr(self.conf), self.n_rows, self.hyper.n_p,
+                  _lib.ptr(out), _lib.stream_ptr())
+        return out
 
     # -- host interchange (parity tests, checkpoints) ------------------------
+    @on_device
     def load_host(self, feats, conf=None, weights=None, biases=None, baked=None) -> "Model":
         """Upload per-level numpy tables (lists indexed by level / slot)."""
         with torch.no_grad():
@@ -236,6 +248,7 @@ class Model:
                 self.rebake_all()
         return self
 
+    @on_device
     def to_host(self) -> dict:
         """numpy copies keyed like the reference's attribute paths."""
         feats = self.feats.cpu().numpy()

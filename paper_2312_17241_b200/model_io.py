@@ -178,8 +178,9 @@ def deserialize(data: bytes, device=None):
     baked = torch.empty((len(pf.probed), hyper.n_c), dtype=torch.uint8, device=dev)
     if pf.probed:
         packed = torch.from_numpy(np.ascontiguousarray(pf.packed)).to(dev)
-        _lib.call("pg_unpack_indices", _lib.ptr(packed), len(pf.probed), hyper.n_c,
-                  _log2(hyper.n_p), _lib.ptr(baked), _lib.stream_ptr())
+        with torch.cuda.device(dev):
+            _lib.call("pg_unpack_indices", _lib.ptr(packed), len(pf.probed), hyper.n_c,
+                      _log2(hyper.n_p), _lib.ptr(baked), _lib.stream_ptr())
     params = torch.from_numpy(pf.mlp16.astype(np.float32)).to(dev)
     return InferenceModel(hyper, pf.width, pf.height, feats16, baked, pf.probed, params, dev)
 
@@ -203,8 +204,9 @@ def serialize(model) -> bytes:
     packed = np.zeros((len(inf.probed), ibytes), np.uint8)
     if inf.probed and w > 0:
         dpk = torch.empty((len(inf.probed), ibytes), dtype=torch.uint8, device=inf.device)
-        _lib.call("pg_pack_indices", _lib.ptr(inf.baked), len(inf.probed), hyper.n_c, w,
-                  _lib.ptr(dpk), _lib.stream_ptr())
+        with torch.cuda.device(inf.device):
+            _lib.call("pg_pack_indices", _lib.ptr(inf.baked), len(inf.probed), hyper.n_c, w,
+                      _lib.ptr(dpk), _lib.stream_ptr())
         packed = dpk.cpu().numpy()
     feats = inf.feats16.cpu().numpy().astype("<f2", copy=False)
     mlp16 = inf.params.cpu().numpy().astype("<f2")   # fp16-rounded values: exact

@@ -23,12 +23,14 @@ import numpy as np
 import torch
 
 from . import _lib
+from ._lib import on_device
 from .encoding import encode_backward_device, encode_forward_device
 from .errors import InvalidHyperparameter
 from .grid_model import Model
 from .train import TrainConfig, TrainState
 
 
+@on_device
 def sample_points(origins: torch.Tensor, dirs: torch.Tensor, n_samples: int):
     """Midpoint samples along each ray inside the unit cube (slab entry and
     exit; rays that miss get zero-length segments): points (R*S, 3) clamped
@@ -63,6 +65,7 @@ def _check_model(model: Model):
                                     "(sigma, r, g, b) and out_sigmoid=False")
 
 
+@on_device
 def mlp_raw(model: Model, y: torch.Tensor) -> torch.Tensor:
     """Per-sample MLP outputs (B, 4) on the device (row-wise kernel)."""
     B = y.shape[0]
@@ -73,6 +76,7 @@ def mlp_raw(model: Model, y: torch.Tensor) -> torch.Tensor:
     return out
 
 
+@on_device
 def composite(raw: torch.Tensor, deltas: torch.Tensor, n_samples: int, weights: bool = False):
     """rgb (R, 3) [and per-sample weights (R, S)] from raw (R*S, 4)."""
     R = raw.shape[0] // n_samples
@@ -83,6 +87,7 @@ def composite(raw: torch.Tensor, deltas: torch.Tensor, n_samples: int, weights: 
     return (rgb, w) if weights else rgb
 
 
+@on_device
 def render(model: Model, origins, dirs, n_samples: int = 64, chunk: int = 1 << 14) -> torch.Tensor:
     """Render rays (R, 3) -> rgb (R, 3) through the current model."""
     _check_model(model)
@@ -144,6 +149,7 @@ class NerfTrainState(TrainState):
     def loss_denominator(self) -> int:
         return self.world * self.cfg.batch_size * 3
 
+    @on_device
     def sample_batch(self):
         """Next contiguous ray slice -> (points (R*S, 3), (deltas, target rgb))."""
         n, R = self.origins.shape[0], self.cfg.batch_size
@@ -153,6 +159,7 @@ class NerfTrainState(TrainState):
         pts, deltas = sample_points(self.origins[lo:lo + R], self.dirs[lo:lo + R], self.n_samples)
         return pts, (deltas, self.rgb[lo:lo + R])
 
+    @on_device
     def compute_grads(self, xs, targets, dy_out=None) -> None:
         m, s = self.model, _lib.stream_ptr()
         deltas, rgb = targets
@@ -164,7 +171,8 @@ class NerfTrainState(TrainState):
             t4[:, :, 1:] = rgb[:, None, :]
             _lib.call("pg_train_fused_f32", m.grid, m.mlp_desc, _lib.ptr(xs), _lib.ptr(t4), R * S,
                       _lib.ptr(m.feats), _lib.ptr(m.baked), _lib.ptr(m.conf), _lib.ptr(m.mlp_params),
-                      float(np.float32(self.scale)), _lib.PG_COMPOSITE, _lib.ptr(m.gfeats), _lib.ptr(m.gconf),
+                      float(np.float32(self.scale)),
+                      _lib.PG_COMPOSITE | (_lib.PG_TOUCH_ALL if self.touch_all else 0), _lib.ptr(m.gfeats), _lib.ptr(m.gconf),
                       _lib.ptr(m.touched), _lib.ptr(m.gmlp), _lib.ptr(self.loss_sum), _lib.ptr(dy_out), s)
             return
         encode_forward_device(m, xs, self.y)

@@ -26,6 +26,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from ._lib import on_device
 from .encoding import encode_backward_device, encode_forward_device
 from .errors import InvalidHyperparameter, TrainingDiverged
 from .grid_model import Model, init_model
@@ -148,6 +149,7 @@ class TrainState:
         self.loss_sum = torch.zeros(1, dtype=torch.float64, device=dev)
         self.loss_host = torch.zeros(1, dtype=torch.float64, pin_memory=True)
         self.rank, self.world = 0, 1
+        self.touch_all = False
         self.scale = 2.0 / (B * h.out_dim)   # trainer.py:134, cast to the model dtype
 
     def shard(self, rank: int, world: int) -> "TrainState":
@@ -157,9 +159,14 @@ class TrainState:
         equal the global-batch gradient."""
         self.rank, self.world = rank, world
         self.scale = 2.0 / (world * self.cfg.batch_size * self.model.hyper.out_dim)
+        # replicas' gconf sums meet only in the all-reduce, where a row's
+        # contributions can cancel to an exact 0.0: flag every lookup so the
+        # touched union is the reference's touched set exactly
+        self.touch_all = world > 1
         return self
 
     # ---------------------------------------------------------------- batch
+    @on_device
     def sample_batch(self):
         """Draw the next batch; returns device (xs, targets)."""
         m, B, s = self.model, self.cfg.batch_size, _lib.stream_ptr()
@@ -194,24 +201,29 @@ class TrainState:
         [gfeats | gmlp | pad | gconf | pad | touched-as-float | loss]."""
         return self.model.grads
 
+    @on_device
     def pack_exchange(self) -> None:
         m, s = self.model, _lib.stream_ptr()
         if m.n_rows:
-            _lib.call("pg_touched_to_f32", _lib.ptr(m.touched), m.n_rows, _lib.ptr(m.touched_f), s)
+            sfx = "f64" if m.touched_f.dtype == torch.float64 else "f32"
+            _lib.call(f"pg_touched_to_{sfx}", _lib.ptr(m.touched), m.n_rows, _lib.ptr(m.touched_f), s)
         m.loss_slot.copy_(self.loss_sum)
 
+    @on_device
     def unpack_exchange(self) -> None:
         """After the all-reduce: touched = union over replicas (every replica
         then updates the same rows, keeping replicas identical), loss = sum."""
         m, s = self.model, _lib.stream_ptr()
         if m.n_rows:
-            _lib.call("pg_touched_from_f32", _lib.ptr(m.touched_f), m.n_rows, _lib.ptr(m.touched), s)
+            sfx = "f64" if m.touched_f.dtype == torch.float64 else "f32"
+            _lib.call(f"pg_touched_from_{sfx}", _lib.ptr(m.touched_f), m.n_rows, _lib.ptr(m.touched), s)
         self.loss_sum.copy_(m.loss_slot)
 
     def loss_denominator(self) -> int:
         return self.world * self.cfg.batch_size * self.model.hyper.out_dim
 
     # ----------------------------------------------------------------- step
+    @on_device
     def launch_step(self) -> None:
         """Enqueue one full step on the current stream (no host sync)."""
         m, cfg = self.model, self.cfg
@@ -223,6 +235,7 @@ class TrainState:
         self.t += 1
         self.apply_updates()
 
+    @on_device
     def compute_grads(self, xs, targets, dy_out=None) -> None:
         """Forward + backward of one batch into model.grads / touched /
         loss_sum: the fused single-kernel path when the shape allows it, else
@@ -231,6 +244,8 @@ class TrainState:
         flags = _lib.PG_SIGMOID if m.hyper.out_sigmoid else 0
         if self.exact_mlp and self.fused:
             flags |= _lib.PG_EXACT_MLP
+        if self.touch_all:
+            flags |= _lib.PG_TOUCH_ALL
         scale = float(np.dtype(m.dtype).type(self.scale))
         if self.reference_order and self.deterministic:
             if dy_out is not None:
@@ -287,6 +302,7 @@ class TrainState:
             dy_out.copy_(self.dy)
         encode_backward_device(m, xs, self.dy)
 
+    @on_device
     def apply_updates(self) -> None:
         """Dense Adam over [features | MLP] and lazy Adam + re-bake over the
         touched confidence rows; both skip the update if the loss diverged."""
@@ -301,25 +317,34 @@ class TrainState:
                       m.n_rows, m.hyper.n_p, self.t, cfg.lr, cfg.beta1, cfg.beta2, cfg.eps,
                       _lib.ptr(self.loss_sum), s)
 
+    @on_device
     def loss_value(self) -> float:
         self.loss_host.copy_(self.loss_sum, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return float(self.loss_host[0]) / self.loss_denominator()
 
+    @on_device
     def step(self) -> float:
         self.launch_step()
+        return self.finish_step()
+
+    def finish_step(self) -> float:
+        """Read the launched step's loss; on a non-finite loss (the optimizer
+        kernels skipped the update) undo the step count and raise, as the
+        reference raises before counting the step (trainer.py:131-133)."""
         loss = self.loss_value()
         if not math.isfinite(loss):
-            self.t -= 1   # the reference raises before counting the step
+            self.t -= 1
             raise TrainingDiverged(f"non-finite loss at step {self.t}")
         if self.cfg.debug_check_every and self.t % self.cfg.debug_check_every == 0:
             self.check_bake_consistency()
         return loss
 
+    @on_device
     def check_bake_consistency(self) -> None:
         m = self.model
         if m.probed:
-            full = torch.argmax(m.conf, dim=-1).to(torch.uint8)
+            full = m.bake_into(torch.empty_like(m.baked))     # codebooks.bake
             bad = (full != m.baked).any(dim=-1).nonzero()
             if bad.numel():
                 raise TrainingDiverged(

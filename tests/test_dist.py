@@ -116,6 +116,13 @@ class OracleReplica:
     def loss_value(self):
         return float(self.loss_sum[0]) / (self.world * self.B * 3)
 
+    def finish_step(self):
+        loss = self.loss_value()
+        if not np.isfinite(loss):
+            self.t -= 1
+            raise FloatingPointError(f"non-finite loss at step {self.t}")
+        return loss
+
     def state(self):
         m = self.m
         return [L.feats.copy() for L in m.levels] + [L.conf.copy() for L in self.probed] + \

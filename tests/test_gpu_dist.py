@@ -85,3 +85,43 @@ def test_one_dp_step_equals_global_batch_step(dp_run):
     conf = st.model.conf.cpu().numpy()
     assert (np.abs(a["conf"] - conf) > 1e-7 + 1e-5 * np.abs(conf)).mean() <= 0.002
     assert (a["baked"] != st.model.baked.cpu().numpy()).mean() <= 0.0005
+
+
+class _SoloDist:
+    """world-1 stand-in for torch.distributed (the all-reduce is the identity)."""
+    class ReduceOp:
+        SUM = None
+
+    @staticmethod
+    def get_rank(group=None):
+        return 0
+
+    @staticmethod
+    def get_world_size(group=None):
+        return 1
+
+    @staticmethod
+    def all_reduce(t, op=None, group=None):
+        return t
+
+
+def test_dataparallel_divergence_raises_and_keeps_step_count():
+    """DataParallel.step applies TrainState's divergence rule: a non-finite
+    global loss raises TrainingDiverged, the optimizer kernels skipped the
+    update and the step count is not advanced (trainer.py:131-133)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2312_17241_b200 as pg
+    from paper_2312_17241_b200.dist import DataParallel
+    kw = dict(n_f=32, n_c=64, n_p=4, n_levels=3, n_min=4, n_max=16, n_neurons=8)
+    img = np.random.default_rng(2).random((12, 12, 3)).astype(np.float32)
+    st = pg.TrainState(pg.init_model(pg.HyperParams(**kw), seed=0), img,
+                       pg.TrainConfig(batch_size=64, lr=1e25, seed=0))
+    dp = DataParallel(st, _SoloDist)
+    with pytest.raises(pg.TrainingDiverged):
+        for _ in range(50):
+            t0 = st.t
+            before = st.model.dense.clone()
+            dp.step()
+    assert st.t == t0
+    assert torch.equal(st.model.dense, before)

@@ -410,6 +410,52 @@ def test_touched_rows_with_zero_weight_corners(exact):
     _assert_due_rows(m, traces)
 
 
+def test_touch_all_flags_every_lookup():
+    """PG_TOUCH_ALL (data-parallel steps): the touched flags alone — without
+    the non-zero-gradient rule — are exactly the rows the reference looked
+    up, so a row whose replicas' gradients cancel after the all-reduce is
+    still updated."""
+    import paper_2312_17241_b200 as pg
+    m, om = _models(C1, perturb=False)
+    st = pg.TrainState(m, _smooth(), pg.TrainConfig(batch_size=4096, seed=0))
+    st.shard(0, 2)
+    assert st.touch_all
+    xs = _edge_points(4096, 2, np.float32, seed=5)
+    tg = np.random.default_rng(3).random((4096, 3)).astype(np.float32)
+    st.loss_sum.zero_()
+    st.compute_grads(torch.from_numpy(xs).cuda(), torch.from_numpy(tg).cuda())
+    _, traces = O.encode_forward(om, xs)
+    t = m.touched.cpu().numpy().reshape(len(m.probed), -1).astype(bool)
+    for i, lv in enumerate(m.probed):
+        eq(np.nonzero(t[i])[0], np.unique(traces[lv].row))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_exchange_touched_union_any_dtype(dtype):
+    """pack_exchange / unpack_exchange in the gradient buffer's own dtype: the
+    summed buffer of two replicas unpacks to the union of their touched rows
+    (float64 models included — the flags must not be written as float32)."""
+    import paper_2312_17241_b200 as pg
+    kw = dict(n_f=2**10, n_c=2**12, n_p=4)
+    reps = []
+    rng = np.random.default_rng(0)
+    for r in range(2):
+        st = pg.TrainState(pg.init_model(pg.HyperParams(**kw), seed=0, dtype=dtype), _smooth(),
+                           pg.TrainConfig(batch_size=256, seed=0,
+                                           precision="f64" if dtype == np.float64 else "f32")).shard(r, 2)
+        flags = (rng.random(st.model.n_rows) < 0.01).astype(np.uint8)
+        st.model.touched.copy_(torch.from_numpy(flags))
+        st.loss_sum.fill_(1.5 + r)
+        st.pack_exchange()
+        reps.append((st, flags))
+    total = reps[0][0].exchange_buffer() + reps[1][0].exchange_buffer()   # the all-reduce
+    for st, _ in reps:
+        st.exchange_buffer().copy_(total)
+        st.unpack_exchange()
+        eq(st.model.touched.cpu().numpy(), reps[0][1] | reps[1][1])
+        assert float(st.loss_sum[0]) == 4.0
+
+
 @pytest.mark.parametrize("od", [3, 2, 4])
 def test_reference_order_mlp_grads_bit_exact(od):
     """reference_order=True: every MLP weight and bias gradient of a batch is
@@ -645,6 +691,28 @@ def test_zero_copy_host_decode():
                   _lib.ptr(ho), _lib.stream_ptr())
 
 
+def test_streaming_decode_refuses_pageable_host_buffers():
+    """The streaming entry point's host fallback reads h_xs over UVA, so the
+    C ABI refuses pageable buffers (ValueError) instead of faulting."""
+    import paper_2312_17241_b200 as pg
+    from paper_2312_17241_b200 import _lib
+    from paper_2312_17241_b200.decode import _flags
+    inf = pg.to_inference(pg.init_model(pg.HyperParams(n_f=2**12, n_c=2**14, n_p=4), seed=0))
+    n, chunk = 1000, 1 << 16
+    hx = torch.rand((n, 2))                       # pageable
+    ho = torch.empty((n, 3)).pin_memory()
+    d_xs = torch.empty(n * 2, device="cuda")
+    d_out = torch.empty(n * 3, device="cuda")
+    d_flags = torch.empty(3, dtype=torch.int32, device="cuda")
+    s = _lib.stream_ptr()
+    if not _lib.lib().pg_decode_stream_supported(inf.grid, inf.mlp_desc, _flags(inf, False)):
+        pytest.skip("no stream memory operations")
+    with pytest.raises(ValueError, match="pinned"):
+        _lib.call("pg_decode_host_stream_f32", inf.grid, inf.mlp_desc, _lib.ptr(hx), n, _lib.ptr(inf.feats16),
+                  _lib.ptr(inf.baked), _lib.ptr(inf.params), _flags(inf, False), chunk, _lib.ptr(d_xs),
+                  _lib.ptr(d_out), _lib.ptr(d_flags), _lib.ptr(ho), s, s, s)
+
+
 def test_streaming_decode_survives_serialised_launches():
     """With CUDA_LAUNCH_BLOCKING=1 the copies that feed the streaming kernel
     can only run after it: its groups time out on the flags and read the
@@ -663,6 +731,7 @@ def test_streaming_decode_survives_serialised_launches():
         "hd(hx, ho)\n"
         "ref = decode_device(inf, hx.cuda(), exact=False).cpu()\n"
         "assert torch.equal(ref, ho), 'mismatch'\n"
+        "assert hd.fallbacks > 0, 'the serialised copies must be counted as host fallbacks'\n"
         "print('ok')\n")
     env = dict(os.environ, CUDA_LAUNCH_BLOCKING="1")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
