@@ -117,6 +117,17 @@ def ncu_traffic(kernel, units):
         return None
 
 
+# ------------------------------------------------------------------ config
+def c2_config(world):
+    """The workload both arms report (identical dicts: same_config)."""
+    return {"workload": "C2 inference: 2-D probed hash grid decode, fused encode+MLP",
+            "queries_per_gpu_per_step": B_INFER, "log2_n_f": 16, "n_c": 2**16, "n_p": 4,
+            "n_levels": 16, "feature_dim": 2, "n_min": 16, "n_max": 8192, "mlp": [32, 64, 64, 3],
+            "parallelism": f"query-sharded x{world}",
+            "l2_policy": "inputs (128 MiB coords + 192 MiB outputs per GPU) larger than L2; "
+                         "tables L2-resident"}
+
+
 # ------------------------------------------------------------------ models
 def inference_model(pg, hyper, seed=0):
     """conf ~ N(0,1) then full bake (uniform probes), features
@@ -186,47 +197,56 @@ def measure_l2(lib_call, torch, table_mib=8):
 
 
 # ------------------------------------------------------------------ CPU arm
-def cpu_decode_baseline(hyper, budget_s=15.0, sample=1 << 24, threads=None):
+class CpuDecode:
     """The reference's decode_pixels on the host: the reference's own compiled
     Cython core (oracle/_ref) when it was built, else the C port, driven by the
     oracle's restatement of model_io.decode_pixels; chunks of 16384 queries
     (model_io.py:45) spread over all host threads (the kernels release the
-    GIL).  Bounded: stops after `budget_s` seconds or `sample` queries."""
-    from concurrent.futures import ThreadPoolExecutor
+    GIL).  The model is built as bench.inference_model builds the GPU one."""
 
-    from oracle import oracle as O
-    ref = O.reference_core_backend()
-    kern, kind = (ref, "reference") if ref is not None else (O.CBackend, "port")
-    oh = O.Hyper(**hyper)
-    om = O.init_model(oh, seed=0)
-    rng = np.random.default_rng(0)
-    for L in om.levels:
-        L.feats[:] = (rng.standard_normal(L.feats.shape) * 0.1).astype(np.float32)
-    for L in om.levels:
-        if L.conf is not None:
-            L.conf[:] = rng.standard_normal(L.conf.shape).astype(np.float32)
-            L.baked[:] = np.argmax(L.conf, axis=1)
-    inf = O.to_inference(om)
+    def __init__(self, hyper, threads=None):
+        from oracle import oracle as O
+        self.O = O
+        ref = O.reference_core_backend()
+        self.kern, self.kind = (ref, "reference") if ref is not None else (O.CBackend, "port")
+        om = O.init_model(O.Hyper(**hyper), seed=0)
+        rng = np.random.default_rng(0)
+        for L in om.levels:
+            L.feats[:] = (rng.standard_normal(L.feats.shape) * 0.1).astype(np.float32)
+        for L in om.levels:
+            if L.conf is not None:
+                L.conf[:] = rng.standard_normal(L.conf.shape).astype(np.float32)
+                L.baked[:] = np.argmax(L.conf, axis=1)
+        self.inf = O.to_inference(om)
+        self.threads = threads or os.cpu_count() or 1
+
+    def run(self, xs, budget_s=None):
+        """Decode xs (all of it, or until budget_s); returns (queries, seconds)."""
+        from concurrent.futures import ThreadPoolExecutor
+        chunk = self.O.DECODE_CHUNK
+        done = 0
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(self.threads) as ex:
+            futs = [ex.submit(self.O.decode_pixels, self.inf, xs[lo:lo + chunk], self.kern)
+                    for lo in range(0, xs.shape[0], chunk)]
+            for lo, f in zip(range(0, xs.shape[0], chunk), futs):
+                f.result()
+                done += min(chunk, xs.shape[0] - lo)
+                if budget_s is not None and time.perf_counter() - t0 > budget_s:
+                    for g in futs:
+                        g.cancel()
+                    break
+        return done, time.perf_counter() - t0
+
+
+def cpu_decode_baseline(hyper, budget_s=15.0, sample=1 << 24, threads=None):
+    """Bounded CPU sample of the headline workload (about budget_s seconds)."""
+    cd = CpuDecode(hyper, threads)
     xs = np.random.default_rng(1234).random((sample, 2), dtype=np.float32)
-    threads = threads or os.cpu_count() or 1
-    chunk = O.DECODE_CHUNK
-    done = 0
-    t0 = time.perf_counter()
-    with ThreadPoolExecutor(threads) as ex:
-        futs = []
-        for lo in range(0, sample, chunk):
-            futs.append(ex.submit(O.decode_pixels, inf, xs[lo:lo + chunk], kern))
-        for f in futs:
-            f.result()
-            done += chunk
-            if time.perf_counter() - t0 > budget_s:
-                for g in futs:
-                    g.cancel()
-                break
-    el = time.perf_counter() - t0
-    return {"value": done / el, "unit": "queries/s", "cores": threads, "kind": kind,
-            "sample": f"{done} of the same C2 queries (decode_pixels, {chunk}-query chunks, "
-                      f"{threads} threads, {el:.1f} s)"}
+    done, el = cd.run(xs, budget_s)
+    return {"value": done / el, "unit": "queries/s", "cores": cd.threads, "kind": cd.kind,
+            "sample": f"{done} of the same C2 queries (decode_pixels, {cd.O.DECODE_CHUNK}-query chunks, "
+                      f"{cd.threads} threads, {el:.1f} s)"}
 
 
 def cpu_train_baseline(budget_s=8.0):
@@ -353,11 +373,28 @@ def run_gpu(args, rank, world, local_rank):
         hd(hx, ho)
     barrier()
     t0 = time.perf_counter()
+    fallbacks = 0
     for _ in range(args.steps):
         hd(hx, ho)
+        fallbacks += hd.fallbacks
     el = max_over_ranks(time.perf_counter() - t0)
     e2e_qps = world * B_INFER * args.steps / el
     e2e_launches = args.steps * (1 if hd.streaming else math.ceil(B_INFER / hd.chunk))
+
+    # ---------------- e2e through the reference-facing numpy call ----------------
+    # pg.decode_pixels(inf, numpy) is what a caller of the reference's
+    # model_io.decode_pixels(inf, xs) switches to: numpy in, numpy out,
+    # reference-order MLP by default (bit-identical), tcgen05 with exact=False
+    q_np = hx.numpy()
+    dropin = {}
+    for name, ex in (("exact_reference_order", True), ("tcgen05", False)):
+        pg.decode_pixels(inf, q_np, exact=ex)
+        barrier()
+        t0 = time.perf_counter()
+        n_rep = max(3, args.steps // 4)
+        for _ in range(n_rep):
+            pg.decode_pixels(inf, q_np, exact=ex)
+        dropin[name] = world * B_INFER * n_rep / max_over_ranks(time.perf_counter() - t0)
 
     # ---------------- training (C1, data parallel) ----------------
     train = run_train(args, pg, torch, dist, rank, world, dev, barrier, max_over_ranks, l2_stream)
@@ -369,6 +406,8 @@ def run_gpu(args, rank, world, local_rank):
                                             l2_stream)
         extra["train_c4_nerf"] = run_train_nerf(args, pg, torch, dist, rank, world, barrier, max_over_ranks,
                                                 l2_stream)
+        extra["train_c5"] = run_train_c5(args, pg, torch, dist, rank, world, barrier, max_over_ranks,
+                                         l2_stream)
         if world == 1:
             extra["sweep_inference_c2_c5"] = run_sweep(args, pg, torch, decode_device)
 
@@ -377,15 +416,14 @@ def run_gpu(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32 (fp16-stored tables, fp32 math)", "data": "synthetic",
-        "config": {"workload": "C2 inference: 2-D probed hash grid decode, fused encode+MLP",
-                   "queries_per_gpu_per_step": B_INFER, "log2_n_f": 16, "n_c": 2**16, "n_p": 4,
-                   "n_levels": 16, "feature_dim": 2, "n_min": 16, "n_max": 8192,
-                   "mlp": inf.widths, "probed_levels": n_probed,
-                   "mlp_mode": "exact (reference order, bit-identical)" if exact else "tcgen05 kind::tf32 UMMA, 2-term split (fp32-level)",
-                   "parallelism": f"query-sharded x{world}",
-                   "l2_policy": "inputs (128 MiB coords + 192 MiB outputs per GPU) larger than L2; tables L2-resident"},
+        "config": c2_config(world),
+        "engine": {"kernel": "decode_umma_kernel", "probed_levels": n_probed,
+                   "mlp_mode": ("exact (reference order, bit-identical)" if exact
+                                else "tcgen05 kind::tf32 UMMA, 2-term split (fp32-level)")},
         "e2e": {"value": e2e_qps, "unit": "queries/s", "h2d_bytes_per_step": B_INFER * 2 * 4,
                 "d2h_bytes_per_step": B_INFER * hyper.out_dim * 4,
+                "host_fallback_pipelines": fallbacks,
+                "dropin_decode_pixels_numpy_qps": dropin,
                 "path": ("pg_decode_host_stream_f32 (pinned host in/out; ONE decode launch fed 2^18-query "
                          "pieces by the copy engine through device flags, D2H of each piece on a stream wait "
                          "for its tile counter; 3 streams)" if hd.streaming else
@@ -394,6 +432,11 @@ def run_gpu(args, rank, world, local_rank):
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak,
+                     "binding_unit": "L1TEX/LSU random-gather issue (ncu: L1TEX ~80% busy, L2 ~46%, "
+                                     "DRAM ~1%; profiles/r02_*)",
+                     "frac_by_unit": {"hbm": achieved / hbm_peak,
+                                      "l2_stream": achieved / l2_stream,
+                                      "random_gather_rate": qps / world * gpq / (l2_gather * 1e9 / 8)},
                      "traffic": ncu_traffic("decode_umma_kernel", B_INFER),
                      "kernel": "decode_umma_kernel", "bytes_per_query": bpq,
                      "peak_source": peak_src,
@@ -457,6 +500,48 @@ def run_train(args, pg, torch, dist, rank, world, dev, barrier, max_over_ranks, 
             "kernel": "train_mma_kernel (3xTF32 mma.sync MLP; exact_mlp=True selects the OpenBLAS-order FFMA kernel)",
             "traffic": ncu_traffic("train_mma_kernel", B_TRAIN),
             "last_loss": loss, "scaling": "weak"}
+
+
+def run_train_c5(args, pg, torch, dist, rank, world, barrier, max_over_ranks, l2_stream=None):
+    """configs[4] training side (C5): train samples/s of the unprobed hash grid
+    (N_p = 1) against probed N_p = 2..16 at EQUAL feature-table size, on the
+    shape of the reference's own overhead criterion (test_acceptance.py:227-256:
+    n_f = 2^8, n_c = 2^12, B = 8192, step(N_p=16) <= 3.0 x step(N_p=1)), at the
+    reference batch and at 2^18 samples per GPU; plus the default
+    HyperParams() step (n_f = 2^6, N_p = 16)."""
+    from paper_2312_17241_b200.dist import DataParallel
+    from tests.golden_util import smooth_image
+    img = smooth_image(256, 256)
+
+    def one(hk, B):
+        hyper = pg.HyperParams(**hk)
+        st = pg.TrainState(pg.init_model(hyper, seed=0), img, pg.TrainConfig(batch_size=B, seed=rank),
+                           sampler="device")
+        step = DataParallel(st, dist).launch_step if world > 1 else st.launch_step
+        ms = _time_steps(torch, step, max(5, args.steps), args.warmup, barrier, max_over_ranks)
+        n_probed = len(st.model.probed)
+        bps = train_bytes_per_sample(hyper, n_probed)
+        r = {"n_f": hyper.n_f, "n_c": hyper.n_c, "n_p": hyper.n_p, "batch_per_gpu": B,
+             "probed_levels": n_probed, "ms_per_step": ms, "samples_per_s": world * B / (ms * 1e-3),
+             "encode_bytes_per_sample": bps, "encode_algorithmic_gbs": B * bps / (ms * 1e-3) / 1e9}
+        if l2_stream:
+            r["encode_frac_of_l2_stream"] = r["encode_algorithmic_gbs"] / l2_stream
+        del st
+        return r
+
+    rows = []
+    for B in (8192, B_TRAIN):
+        for n_p in (1, 2, 4, 8, 16):
+            rows.append(one(dict(n_f=2**8, n_c=2**12, n_p=n_p), B))
+    env = {}
+    for B in (8192, B_TRAIN):
+        t = {r["n_p"]: r["ms_per_step"] for r in rows if r["batch_per_gpu"] == B}
+        env[f"B{B}"] = {"step_np16_over_np1": t[16] / t[1], "bound": 3.0, "holds": t[16] / t[1] <= 3.0}
+    default = one({}, B_TRAIN)
+    return {"metric": "train samples/s", "unit": "samples/s",
+            "config": {"workload": "C5 training: unprobed (N_p=1) vs probed at equal n_f",
+                       "image": "256x256 synthetic smooth", "sampler": "device", "parallelism": f"dp{world}"},
+            "points": rows, "overhead_envelope": env, "default_hyperparams_step": default}
 
 
 def _time_steps(torch, step, steps, warmup, barrier, max_over_ranks):
@@ -592,24 +677,39 @@ def run_sweep(args, pg, torch, decode_device):
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's own CPU path on this host."""
+    """--impl reference: the reference's own CPU path on this host, rank 0
+    only.  Every step decodes one full 2^24-query batch when the whole run
+    fits in ~4 minutes at the rate the warm-up measured; otherwise each step
+    is a bounded sample of the batch (stated in cpu_baseline.sample) and
+    ms_per_step is the time of that sample."""
     if rank != 0:
         return None
-    hyper = C2
-    res = [cpu_decode_baseline(hyper, budget_s=max(2.0, 20.0 / max(1, args.steps + args.warmup)))
-           for _ in range(args.warmup + args.steps)]
-    timed = res[args.warmup:]
-    v = float(np.median([r["value"] for r in timed]))
-    cb = dict(timed[-1])
-    cb["value"] = v
+    cd = CpuDecode(C2)
+    xs = np.random.default_rng(1234).random((B_INFER, 2), dtype=np.float32)
+    n_w, el_w = cd.run(xs[:1 << 20])                      # warm-up + rate estimate
+    for _ in range(max(0, args.warmup - 1)):
+        cd.run(xs[:1 << 20])
+    rate = n_w / el_w
+    per_step = B_INFER
+    if args.steps * B_INFER / rate > 240.0:
+        per_step = max(1 << 16, int(240.0 * rate / args.steps) // (1 << 14) * (1 << 14))
+    times, n = [], 0
+    for k in range(args.steps):
+        lo = (k * per_step) % B_INFER
+        done, el = cd.run(xs[lo:lo + per_step])
+        times.append(el)
+        n += done
+    v = n / sum(times)
+    sample = (f"every step the full {B_INFER}-query C2 batch" if per_step == B_INFER else
+              f"every step a {per_step}-query slice of the {B_INFER}-query C2 batch")
+    cb = {"value": v, "unit": "queries/s", "cores": cd.threads, "kind": cd.kind,
+          "sample": f"{sample} (decode_pixels, {cd.O.DECODE_CHUNK}-query chunks on {cd.threads} threads)"}
     return {"metric": METRIC, "impl": "reference", "value": v, "unit": "queries/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": B_INFER / v * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": float(np.mean(times)) * 1e3, "queries_per_timed_step": per_step,
+            "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "C2 inference: 2-D probed hash grid decode, fused encode+MLP",
-                       "queries_per_gpu_per_step": B_INFER, "log2_n_f": 16, "n_c": 2**16,
-                       "n_p": 4, "n_levels": 16, "feature_dim": 2, "n_min": 16, "n_max": 8192,
-                       "parallelism": "host threads"},
+            "config": c2_config(world),
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 

@@ -302,6 +302,29 @@ int pg_train_fused_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
                        float *gparams, double *loss_sum, float *dy_out,
                        void *stream);
 
+/* Standalone batched MLP, mlp.py:55-85 (mlp_forward / mlp_backward with an
+ * arbitrary upstream gradient; ReLU hidden layers, linear output; numpy /
+ * OpenBLAS operation order: each output an FMA chain over k from zero, the
+ * bias a separate rounded add).  pg_mlp_forward: out (B, widths[-1]); ws
+ * holds the hidden pre-activations, pg_mlp_train_workspace_floats(B, mlp)
+ * floats.  pg_mlp_backward: re-runs the forward from x, then
+ * gparams += parameter grads (params layout) for dL/d(out) = upstream
+ * (B, widths[-1]) and writes dx (B, widths[0]). */
+int pg_mlp_forward_f32(const pg_mlp *mlp, const float *x, int64_t B,
+                       const float *params, float *ws, float *out, void *stream);
+int pg_mlp_forward_f64(const pg_mlp *mlp, const double *x, int64_t B,
+                       const double *params, double *ws, double *out, void *stream);
+int pg_mlp_backward_f32(const pg_mlp *mlp, const float *x, int64_t B,
+                        const float *params, const float *upstream,
+                        float *gparams, float *dx, float *ws, void *stream);
+int pg_mlp_backward_f64(const pg_mlp *mlp, const double *x, int64_t B,
+                        const double *params, const double *upstream,
+                        double *gparams, double *dx, double *ws, void *stream);
+
+/* Output quantisation for PNG (pngio.py:34-41): out[i] = uint8(rint(clip(x[i],
+ * 0, 1) * 255)) in float32 arithmetic, half-to-even (numpy on a float32 array). */
+int pg_quantize_u8_f32(const float *x, int64_t n, uint8_t *out, void *stream);
+
 /* Volume-compositing head (the reference has no
  * renderer, so these are checked against the numpy restatement in
  * oracle/oracle.py and finite differences).  raw (R*S, 4) = per-sample MLP
@@ -316,6 +339,12 @@ int pg_composite_fwd_f32(const float *raw, const float *deltas, int64_t R,
  * deltas (R*S) = segment length.  origins/dirs (R, 3). */
 int pg_ray_samples_f32(const float *origins, const float *dirs, int64_t R,
                        int S, float *pts, float *deltas, void *stream);
+/* pg_ray_samples_f32 plus the fused NeRF step's targets in one pass:
+ * t4 (R*S, 4) = (segment length, target r, g, b) per sample (16-byte
+ * aligned), rgb (R, 3) the rays' target colours. */
+int pg_ray_samples_targets_f32(const float *origins, const float *dirs,
+                               const float *rgb, int64_t R, int S, float *pts,
+                               float *deltas, float *t4, void *stream);
 /* NeRF-style training pass over R rays x S samples: y (R*S, widths[0]) are
  * the samples' encodings (pg_encode_fwd_f32); MLP forward (widths[-1] = 4),
  * compositing, loss = sum (rgb - target_rgb)^2 into *loss_sum (fp64),

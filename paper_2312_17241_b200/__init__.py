@@ -11,7 +11,8 @@ __version__ = "0.1.0"
 
 from .errors import (BadMagic, DimensionMismatch, DomainViolation, InvalidHyperparameter,
                      InvariantViolation, ModelFileError, ProbeGridError, ShapeMismatch, StaleTrace,
-                     TargetTooSmall, TrainingDiverged, TruncatedFile, UnbakedModel, VersionMismatch)
+                     TargetTooSmall, TrainingDiverged, TruncatedFile, UnbakedModel, UnsupportedFormat,
+                     VersionMismatch)
 from .hyper import (AUX_PRIMES, PRIMARY_PRIMES, HyperParams, LevelMode, LevelSpec,
                     build_level_specs, level_resolution)
 
@@ -27,6 +28,7 @@ __all__ = [
     "unpack_indices", "HEADER_BYTES", "load", "save", "select_hyperparams",
     "expand_grid", "run_sweep", "write_csv", "SweepPoint", "psnr", "pareto_front",
     "NerfTrainState", "render", "composite", "orbit_rays", "sample_points",
+    "UnsupportedFormat", "save_image", "load_image", "mlp_forward", "mlp_backward", "MlpCache",
 ]
 
 
@@ -55,4 +57,10 @@ def __getattr__(name):
                 "unpack_indices", "HEADER_BYTES", "parse", "load", "save"):
         from . import model_io
         return getattr(model_io, name)
+    if name in ("save_image", "load_image"):
+        from . import pngio
+        return getattr(pngio, name)
+    if name in ("mlp_forward", "mlp_backward", "MlpCache"):
+        from . import mlp
+        return getattr(mlp, name)
     raise AttributeError(name)

@@ -70,6 +70,8 @@ for _t, _s in (("f32", _F), ("f64", _D)):
         f"pg_encode_fwd_{_t}": [_G, _P, _I64, _P, _P, _P, ctypes.c_uint, _P, _P, _P],
         f"pg_encode_bwd_{_t}": [_G, _P, _I64, _P, _P, _P, _P, _P, _P, _P],
         f"pg_mlp_train_{_t}": [_M, _P, _P, _I64, _P, _s, ctypes.c_uint, _P, _P, _P, _P, _P],
+        f"pg_mlp_forward_{_t}": [_M, _P, _I64, _P, _P, _P, _P],
+        f"pg_mlp_backward_{_t}": [_M, _P, _I64, _P, _P, _P, _P, _P, _P],
         f"pg_pixel_batch_{_t}": [_P, _I64, _I, _I, _P, _I, _U64, _U64, _P, _P, _P, _P],
         f"pg_adam_{_t}": [_P, _P, _P, _P, _I64, _I64, _D, _D, _D, _D, _P, _P],
         f"pg_lazy_adam_rebake_{_t}": [_P, _P, _P, _P, _P, _P, _I64, _I, _I64, _D, _D, _D, _D, _P, _P],
@@ -81,6 +83,7 @@ _SIGS.update({
     "pg_touched_to_f32": [_P, _I64, _P, _P],
     "pg_composite_fwd_f32": [_P, _P, _I64, _I, _P, _P, _P],
     "pg_ray_samples_f32": [_P, _P, _I64, _I, _P, _P, _P],
+    "pg_ray_samples_targets_f32": [_P, _P, _P, _I64, _I, _P, _P, _P, _P],
     "pg_decode_stream_supported": [_G, _M, ctypes.c_uint],
     "pg_decode_host_zc_f32": [_G, _M, _P, _I64, _P, _P, _P, ctypes.c_uint, _P, _P],
     "pg_decode_host_stream_f32": [_G, _M, _P, _I64, _P, _P, _P, ctypes.c_uint, _I64, _P, _P, _P, _P, _P, _P, _P],
@@ -88,6 +91,7 @@ _SIGS.update({
     "pg_touched_from_f32": [_P, _I64, _P, _P],
     "pg_touched_to_f64": [_P, _I64, _P, _P],
     "pg_bake_rows_f32": [_P, _I64, _I, _P, _P],
+    "pg_quantize_u8_f32": [_P, _I64, _P, _P],
     "pg_bake_rows_f64": [_P, _I64, _I, _P, _P],
     "pg_touched_from_f64": [_P, _I64, _P, _P],
     "pg_train_fused_f32": [_G, _M, _P, _P, _I64, _P, _P, _P, _P, _F, ctypes.c_uint, _P, _P, _P,

@@ -127,11 +127,59 @@ __device__ __forceinline__ float2 encode_level_fwd2_rng(const pg_grid &g, int l,
 // feature-gradient table (all N_p probes, softmax-weighted, for probed
 // levels), the softmax-Jacobian term into gconf, and flag the row touched.
 // ACC = float (vector reductions into L2) or fx_t (deterministic fixed point).
-template <int NPMAX, typename ACC>
+template <int NPMAX, typename ACC, bool FEATS = true>
 __device__ __forceinline__ void encode_probe_reds(ACC *gb, ACC *gc, int n_p, const float (&sg)[NPMAX],
                                                   const float (&dots)[NPMAX], float s, float g0, float g1);
 
-template <int D, int NPMAX, typename ACC = float, bool LAZY = false>
+// Warp-aggregated feature-gradient reduction of one corner's probing range
+// (AGG): lanes whose ranges start at the same row `base` (key; -1 = lane
+// contributes nothing) are summed by a shuffle reduce-scatter of the
+// range's 2*n_p floats (element i = sg[i/2] * (i odd ? g1 : g0)), then ONE
+// coalesced reduction per distinct range and warp.  Called by all 32 lanes.
+template <int NPMAX>
+__device__ __forceinline__ void warp_agg_range_reds(float *gtab, int key, int n_p, const float (&sg)[NPMAX],
+                                                    float g0, float g1) {
+    static_assert(NPMAX <= 16, "a probing range of 2*N_p floats must fit one warp");
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned grp = __match_any_sync(full, key);
+    unsigned todo = full;
+    while (todo) {
+        const int lead = __ffs(todo) - 1;
+        const unsigned gmask = __shfl_sync(full, grp, lead);
+        const int kb = __shfl_sync(full, key, lead);
+        todo &= ~gmask;
+        if (kb < 0) continue;
+        const bool in = (gmask >> lane) & 1u;
+        // step 1 (xor 16) from the contributions directly, then 8, 4, 2, 1:
+        // lane l ends with the group's sum of element l
+        float x[16];
+        const bool u16 = (lane & 16) != 0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            float lo = 0.0f, hi = 0.0f;
+            if ((i >> 1) < NPMAX && in) lo = sg[(i >> 1) % NPMAX] * ((i & 1) ? g1 : g0);
+            if (((i + 16) >> 1) < NPMAX && in) hi = sg[((i + 16) >> 1) % NPMAX] * ((i & 1) ? g1 : g0);
+            const float send = u16 ? lo : hi, keep = u16 ? hi : lo;
+            x[i] = keep + __shfl_xor_sync(full, send, 16);
+        }
+#pragma unroll
+        for (int s = 8; s >= 1; s >>= 1) {
+            const bool up = (lane & s) != 0;
+#pragma unroll
+            for (int i = 0; i < s; ++i) {
+                const float send = up ? x[i] : x[i + s], keep = up ? x[i + s] : x[i];
+                x[i] = keep + __shfl_xor_sync(full, send, s);
+            }
+        }
+        if (lane < 2 * n_p) red_add(gtab + (int64_t)kb * 2 + lane, x[0]);
+    }
+}
+
+// AGG: feature reductions of probed levels through warp_agg_range_reds (all
+// 32 lanes must call; `valid` = this lane has a sample).  Dense / hashed
+// levels and the confidence rows keep per-lane reductions.
+template <int D, int NPMAX, typename ACC = float, bool LAZY = false, bool AGG = false>
 __device__ __forceinline__ void encode_level_bwd2(const pg_grid &g, int l, const float (&x)[D],
                                                   float up0, float up1,
                                                   const float *__restrict__ feats,
@@ -139,7 +187,7 @@ __device__ __forceinline__ void encode_level_bwd2(const pg_grid &g, int l, const
                                                   ACC *__restrict__ gfeat,
                                                   ACC *__restrict__ gconf,
                                                   uint8_t *__restrict__ touched,
-                                                  bool touch_all = false) {
+                                                  bool touch_all = false, bool valid = true) {
     constexpr int C = 1 << D;
     const uint32_t nf_mask = (uint32_t)g.n_f - 1u, nc_mask = (uint32_t)g.n_c - 1u;
     const int res = g.res[l], kind = g.kind[l];
@@ -157,6 +205,7 @@ __device__ __forceinline__ void encode_level_bwd2(const pg_grid &g, int l, const
 #pragma unroll
     for (int k = 0; k < C; ++k) wk[k] = corner_weight<float, D>(k, t, omt);
     if (kind != PG_LEVEL_PROBED) {
+        if (!valid) return;
 #pragma unroll
         for (int k = 0; k < C; ++k) {
             const int lin = kind == PG_LEVEL_DENSE ? corner_dense<D>(k, c, res + 1)
@@ -222,7 +271,7 @@ __device__ __forceinline__ void encode_level_bwd2(const pg_grid &g, int l, const
 #pragma unroll
         for (int u = 0; u < PF; ++u) {
             const int k = k0 + u;
-            if (!LAZY) touched[crow[k]] = 1;
+            if (!LAZY && valid) touched[crow[k]] = 1;
             const float g0 = __fmul_rn(wk[k], up0), g1 = __fmul_rn(wk[k], up1);
             ACC *gc = gconf + crow[k] * n_p;
             ACC *gb = gtab + (int64_t)bs[k] * 2;
@@ -263,19 +312,26 @@ __device__ __forceinline__ void encode_level_bwd2(const pg_grid &g, int l, const
                 // row, so a row whose replicas' contributions cancel to an
                 // exact 0.0 after the all-reduce is still updated, as the
                 // reference's lazy Adam updates every touched row
-                if (!live || touch_all) touched[crow[k]] = 1;
+                if ((!live || touch_all) && valid) touched[crow[k]] = 1;
             }
-            encode_probe_reds<NPMAX, ACC>(gb, gc, n_p, sg, dots, s, g0, g1);
+            if constexpr (AGG) {
+                static_assert(std::is_same<ACC, float>::value, "AGG: fp32 reductions only");
+                // confidence rows first: dots are dead during the shuffles
+                if (valid) encode_probe_reds<NPMAX, ACC, false>(gb, gc, n_p, sg, dots, s, g0, g1);
+                warp_agg_range_reds<NPMAX>(gtab, valid ? bs[k] : -1, n_p, sg, g0, g1);
+            } else {
+                encode_probe_reds<NPMAX, ACC>(gb, gc, n_p, sg, dots, s, g0, g1);
+            }
         }
     }
 }
 
 // scatter of one probed corner: softmax-weighted feature grads over the
 // probing range (16-byte vector reductions) + confidence-row gradient
-template <int NPMAX, typename ACC>
+template <int NPMAX, typename ACC, bool FEATS>
 __device__ __forceinline__ void encode_probe_reds(ACC *gb, ACC *gc, int n_p, const float (&sg)[NPMAX],
                                                   const float (&dots)[NPMAX], float s, float g0, float g1) {
-    {
+    if constexpr (FEATS) {
         if (n_p >= 2) {
 #pragma unroll
             for (int j = 0; j < NPMAX; j += 2)
@@ -284,6 +340,8 @@ __device__ __forceinline__ void encode_probe_reds(ACC *gb, ACC *gc, int n_p, con
         } else {
             red_add_v2(gb, sg[0] * g0, sg[0] * g1);
         }
+    }
+    {
         if (n_p >= 4) {
 #pragma unroll
             for (int j = 0; j < NPMAX; j += 4)

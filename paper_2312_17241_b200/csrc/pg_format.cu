@@ -54,6 +54,17 @@ __global__ void raster_coords_kernel(int x0, int y0, int w, int64_t n, int W, in
 
 }  // namespace pg
 
+namespace pg {
+// pngio.py:39: np.rint(np.clip(p, 0, 1) * 255).astype(uint8) on a float32
+// array: float32 clip, rounded float32 multiply, round half to even
+__global__ void quantize_u8_kernel(const float *__restrict__ x, int64_t n, uint8_t *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float v = fminf(fmaxf(x[i], 0.0f), 1.0f);
+        out[i] = (uint8_t)rintf(__fmul_rn(v, 255.0f));
+    }
+}
+}  // namespace pg
+
 extern "C" {
 
 int pg_raster_coords_f32(int x0, int y0, int w, int h, int width, int height, float *xs, void *stream) {
@@ -90,6 +101,13 @@ int pg_pack_indices(const uint8_t *entries, int64_t n_rows, int64_t n_c, int log
     pg::pack_indices_kernel<<<(unsigned)((n + 255) / 256), 256, 0, pg::as_stream(stream)>>>(
         entries, n_rows, n_c, log2_np, block_bytes, packed);
     return pg::check_launch("pack_indices");
+}
+
+int pg_quantize_u8_f32(const float *x, int64_t n, uint8_t *out, void *stream) {
+    PG_REQUIRE(n >= 0, "quantize: negative size");
+    if (n == 0) return PG_OK;
+    pg::quantize_u8_kernel<<<pg::grid_for(n, 256, 148 * 16), 256, 0, pg::as_stream(stream)>>>(x, n, out);
+    return pg::check_launch("quantize_u8");
 }
 
 }  // extern "C"

@@ -555,8 +555,11 @@ int mlp_train_generic(const pg_mlp *m, const T *y, const T *targets, int64_t B, 
 // =========================================================================
 // midpoint samples along each ray inside the unit cube (slab test); rays
 // that miss get zero-length segments at their clamped origin
+// t4 (optional): the fused NeRF step's per-sample targets (segment length,
+// ray colour) written alongside, rgb (R, 3) the rays' target colours
 __global__ void ray_samples_kernel(const float *__restrict__ o, const float *__restrict__ dir, int64_t R,
-                                   int S, float *__restrict__ pts, float *__restrict__ deltas) {
+                                   int S, float *__restrict__ pts, float *__restrict__ deltas,
+                                   const float *__restrict__ rgb = nullptr, float *__restrict__ t4 = nullptr) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= R * S) return;
     const int64_t r = i / S;
@@ -575,6 +578,7 @@ __global__ void ray_samples_kernel(const float *__restrict__ o, const float *__r
     const float t = nr + ((float)k + 0.5f) * step;
     for (int a = 0; a < 3; ++a) pts[i * 3 + a] = fminf(fmaxf(ov[a] + t * dv[a], 0.0f), 1.0f);
     deltas[i] = step;
+    if (t4) *reinterpret_cast<float4 *>(t4 + i * 4) = make_float4(step, rgb[r * 3], rgb[r * 3 + 1], rgb[r * 3 + 2]);
 }
 
 __device__ __forceinline__ float softplus_f(float x) { return x > 20.0f ? x : log1pf(expf(x)); }
@@ -661,6 +665,40 @@ __global__ void composite_loss_kernel(const float *__restrict__ raw, const float
     }
 }
 
+
+// standalone batched MLP (mlp.py:55-85): forward into the pre-activation
+// workspace (the "cache"), and a backward that re-runs the forward from x and
+// seeds the backward with a caller-supplied dL/d(output)
+template <typename T>
+int mlp_forward_generic(const pg_mlp *m, const T *x, int64_t B, const T *params, T *ws, T *out,
+                        cudaStream_t s) {
+    if (int e = validate_mlp(m)) return e;
+    if (B == 0) return PG_OK;
+    PG_REQUIRE(ws != nullptr && out != nullptr, "mlp_forward: null buffer");
+    const int nl = m->n_layers;
+    int64_t off = 0, zoff = 0;
+    const T *a = x;
+    for (int l = 0; l < nl; ++l) {
+        const int fi = m->widths[l], fo = m->widths[l + 1];
+        T *z = l == nl - 1 ? out : ws + zoff;
+        train_linear_fwd_kernel<T><<<grid_for(B * fo, 256), 256, 0, s>>>(a, l > 0, B, fi, params + off,
+                                                                        params + off + (int64_t)fi * fo, fo, z);
+        off += (int64_t)fi * fo + fo;
+        zoff += B * fo;
+        a = z;
+    }
+    return check_launch("mlp_forward");
+}
+
+template <typename T>
+int mlp_backward_generic(const pg_mlp *m, const T *x, int64_t B, const T *params, const T *upstream,
+                         T *gparams, T *dx, T *ws, cudaStream_t s) {
+    PG_REQUIRE(B == 0 || upstream != nullptr, "mlp_backward: null upstream");
+    const int od = m->widths[m->n_layers];
+    return mlp_train_core<T, T>(m, x, B, params, gparams, dx, ws, s, [&](const T *, T *delta) {
+        cudaMemcpyAsync(delta, upstream, sizeof(T) * B * od, cudaMemcpyDeviceToDevice, s);
+    });
+}
 
 int64_t mlp_train_ws(int64_t B, const pg_mlp *m) {
     int64_t zsum = 0;
@@ -1145,6 +1183,15 @@ int pg_ray_samples_f32(const float *origins, const float *dirs, int64_t R, int S
     ray_samples_kernel<<<grid_for(R * S, 256), 256, 0, as_stream(stream)>>>(origins, dirs, R, S, pts, deltas);
     return check_launch("ray_samples");
 }
+int pg_ray_samples_targets_f32(const float *origins, const float *dirs, const float *rgb, int64_t R, int S,
+                               float *pts, float *deltas, float *t4, void *stream) {
+    PG_REQUIRE(R >= 0 && S >= 1, "ray_samples: R >= 0 and S >= 1");
+    PG_REQUIRE(R == 0 || (rgb && t4 && ((uintptr_t)t4 & 15) == 0), "ray_samples: rgb / 16-byte aligned t4");
+    if (R == 0) return PG_OK;
+    ray_samples_kernel<<<grid_for(R * S, 256), 256, 0, as_stream(stream)>>>(origins, dirs, R, S, pts, deltas,
+                                                                          rgb, t4);
+    return check_launch("ray_samples_targets");
+}
 int pg_composite_fwd_f32(const float *raw, const float *deltas, int64_t R, int S, float *rgb,
                          float *weights, void *stream) {
     PG_REQUIRE(R >= 0 && S >= 1, "composite: R >= 0 and S >= 1");
@@ -1175,6 +1222,22 @@ int pg_mlp_train_f64(const pg_mlp *mlp, const double *y, const double *targets, 
                      double *dy, double *loss_sum, double *ws, void *stream) {
     return mlp_train_generic<double>(mlp, y, targets, B, params, scale, flags, gparams, dy,
                                      loss_sum, ws, as_stream(stream));
+}
+int pg_mlp_forward_f32(const pg_mlp *mlp, const float *x, int64_t B, const float *params, float *ws,
+                       float *out, void *stream) {
+    return mlp_forward_generic<float>(mlp, x, B, params, ws, out, as_stream(stream));
+}
+int pg_mlp_forward_f64(const pg_mlp *mlp, const double *x, int64_t B, const double *params, double *ws,
+                       double *out, void *stream) {
+    return mlp_forward_generic<double>(mlp, x, B, params, ws, out, as_stream(stream));
+}
+int pg_mlp_backward_f32(const pg_mlp *mlp, const float *x, int64_t B, const float *params,
+                        const float *upstream, float *gparams, float *dx, float *ws, void *stream) {
+    return mlp_backward_generic<float>(mlp, x, B, params, upstream, gparams, dx, ws, as_stream(stream));
+}
+int pg_mlp_backward_f64(const pg_mlp *mlp, const double *x, int64_t B, const double *params,
+                        const double *upstream, double *gparams, double *dx, double *ws, void *stream) {
+    return mlp_backward_generic<double>(mlp, x, B, params, upstream, gparams, dx, ws, as_stream(stream));
 }
 
 }  // extern "C"

@@ -29,6 +29,7 @@ constexpr int kNT = 256;  // threads (8 warps), 2 CTAs per SM
 constexpr int kI = 32;    // L*F
 constexpr int kH = 64;    // hidden width
 constexpr int kO = 4;     // max output width
+constexpr int kAggRanges = 8;   // warp-aggregate feature reductions up to this many ranges per level
 constexpr int kS = 72;    // row stride (floats) of [feature][sample] tiles and weights:
                           // 72 = 8 mod 32 makes the A/B fragment loads of the
                           // feature-indexed GEMMs bank-conflict free
@@ -229,7 +230,14 @@ __device__ __forceinline__ double composite_tile(float *d3, const float *tg, flo
 // held in anti-phase by a CTA-wide barrier at every phase switch, so one
 // pipeline's MLP (shared memory + tensor pipe) always runs beside the
 // other's table gathers/scatters (L1/L2).
-template <typename FT, int D, int NPM, typename ACC, typename LACC, int NG>
+// AGG: warp-aggregated feature-gradient reductions for probed levels with
+// few probing ranges (n_f / N_p <= kAggRanges).  Every lookup of such a
+// level lands in one of a handful of ranges, so per-lane reductions from all
+// SMs serialise on the same L2 addresses (C5 / default-HyperParams shapes:
+// 2-9x slower steps); instead the lanes of a warp that share a range sum
+// their contributions with a shuffle reduce-scatter and one coalesced
+// reduction per range and warp is issued (encode_level_bwd2<..., AGG>).
+template <typename FT, int D, int NPM, typename ACC, typename LACC, int NG, bool AGG = false>
 __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
     train_mma_kernel(const pg_grid g, const float *__restrict__ xs, const float *__restrict__ targets,
                      int64_t B, const FT *__restrict__ feats_fwd, const float *__restrict__ feats,
@@ -292,6 +300,7 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
     umma::fence_after_sync();
     const uint32_t tm = S.tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 32) +
                         (uint32_t)(64 * gid);
+
     {
         const float z16[16] = {}, z8[8] = {}, z4[4] = {};
         umma::tmem_st16(tm, z16);
@@ -500,9 +509,17 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
                 G.y[(2 * l) * kS + pl] = yv.x;
                 G.y[(2 * l + 1) * kS + pl] = yv.y;
             }
-            if (pl < nv)
-                encode_level_bwd2<D, NPM, ACC, std::is_same<ACC, float>::value>(g, l, x, GDY[(2 * l) * kS + pl], GDY[(2 * l + 1) * kS + pl],
-                                               feats, conf, gfeat, gconf, touched, touch_all);
+            constexpr bool lazy = std::is_same<ACC, float>::value;
+            if constexpr (AGG) {
+                // every lane of the warp takes part (the shuffles); lanes past
+                // the batch end contribute nothing
+                encode_level_bwd2<D, NPM, ACC, lazy, true>(g, l, x, GDY[(2 * l) * kS + pl],
+                                                           GDY[(2 * l + 1) * kS + pl], feats, conf, gfeat, gconf,
+                                                           touched, touch_all, pl < nv);
+            } else if (pl < nv) {
+                encode_level_bwd2<D, NPM, ACC, lazy>(g, l, x, GDY[(2 * l) * kS + pl], GDY[(2 * l + 1) * kS + pl],
+                                                     feats, conf, gfeat, gconf, touched, touch_all);
+            }
         }
 #pragma unroll
         for (int a = 0; a < D; ++a) x[a] = xn[a];
@@ -567,12 +584,17 @@ template <typename ACC, typename LACC>
 int train_mma(const pg_grid *g, int od, const float *xs, const float *targets, int64_t B, const float *feats,
               const uint8_t *baked, const float *conf, const float *params, float scale, int sig, ACC *gfeat,
               ACC *gconf, uint8_t *touched, ACC *gparams, LACC *loss_sum, float *dy_out, cudaStream_t s) {
-    static DeviceOnce configured[12];
+    static DeviceOnce configured[18];
     const int sms = device_sms();
     // tile pipelines per CTA (1 or 2)
     static const int groups = getenv("PG_TRAIN_GROUPS") && atoi(getenv("PG_TRAIN_GROUPS")) == 1 ? 1 : 2;
     const int64_t ntiles = (B + tm::kT - 1) / tm::kT;
     const int npm = g->log2_np <= 2 ? 4 : g->log2_np == 3 ? 8 : 16;   // probing range held in registers
+    // warp-aggregated feature reductions (fast fp32 path, two pipelines per
+    // CTA) when the probed levels have at most kAggRanges probing ranges
+    static const int agg_ranges = getenv("PG_TRAIN_AGG_RANGES") ? atoi(getenv("PG_TRAIN_AGG_RANGES"))
+                                                                 : tm::kAggRanges;   // 0 disables
+    const bool agg = std::is_same<ACC, float>::value && groups == 2 && (g->n_f >> g->log2_np) <= agg_ranges;
 #define PG_TRAIN_MMA(D_, NP_, NG_, IDX)                                                               \
     do {                                                                                              \
         auto kern = train_mma_kernel<float, D_, NP_, ACC, LACC, NG_>;                                 \
@@ -584,9 +606,24 @@ int train_mma(const pg_grid *g, int od, const float *xs, const float *targets, i
         kern<<<grd, tm::kNT * NG_, smem, s>>>(*g, xs, targets, B, feats, feats, baked, conf, params, od, \
                                               scale, sig, gfeat, gconf, touched, gparams, loss_sum, dy_out); \
     } while (0)
+#define PG_TRAIN_MMA_AGG(D_, NP_, IDX)                                                                \
+    do {                                                                                              \
+        auto kern = train_mma_kernel<float, D_, NP_, ACC, LACC, 2, true>;                             \
+        const int smem = (int)sizeof(tm::SmemT<2>);                                                   \
+        if (configured[IDX].first())                                                                  \
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);            \
+        const int64_t want = (ntiles + 1) / 2, cap = (int64_t)sms;                                    \
+        const int grd = (int)(want < cap ? want : cap);                                               \
+        kern<<<grd, tm::kNT * 2, smem, s>>>(*g, xs, targets, B, feats, feats, baked, conf, params, od,   \
+                                            scale, sig, gfeat, gconf, touched, gparams, loss_sum, dy_out); \
+    } while (0)
 #define PG_TRAIN_MMA_NG(D_, NP_, IDX)                                                                 \
     do {                                                                                              \
-        if (groups == 2) PG_TRAIN_MMA(D_, NP_, 2, (IDX) + 6); else PG_TRAIN_MMA(D_, NP_, 1, IDX);     \
+        if (agg) {                                                                                    \
+            if constexpr (std::is_same<ACC, float>::value) PG_TRAIN_MMA_AGG(D_, NP_, (IDX) + 12);     \
+        }                                                                                             \
+        else if (groups == 2) PG_TRAIN_MMA(D_, NP_, 2, (IDX) + 6);                                    \
+        else PG_TRAIN_MMA(D_, NP_, 1, IDX);                                                           \
     } while (0)
     if (g->d == 2) {
         if (npm == 4) PG_TRAIN_MMA_NG(2, 4, 0); else if (npm == 8) PG_TRAIN_MMA_NG(2, 8, 4); else PG_TRAIN_MMA_NG(2, 16, 1);
@@ -594,6 +631,7 @@ int train_mma(const pg_grid *g, int od, const float *xs, const float *targets, i
         if (npm == 4) PG_TRAIN_MMA_NG(3, 4, 2); else if (npm == 8) PG_TRAIN_MMA_NG(3, 8, 5); else PG_TRAIN_MMA_NG(3, 16, 3);
     }
 #undef PG_TRAIN_MMA_NG
+#undef PG_TRAIN_MMA_AGG
 #undef PG_TRAIN_MMA
     return check_launch("train_mma");
 }

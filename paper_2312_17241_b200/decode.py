@@ -144,11 +144,41 @@ def decode_pixels(inf: InferenceModel, xs, counter: TouchCounter | None = None,
         if t.numel() and bool(((t < 0.0) | (t > 1.0)).any()):   # encoding.py:37-38 (NaN passes, as there)
             raise DomainViolation("coordinates outside the unit hypercube")
     if counter is not None:
-        per = t.shape[0] * (1 << d)
+        per = (a if as_numpy else t).shape[0] * (1 << d)
         counter.feature_rows += per * inf.hyper.n_levels
         counter.index_rows += per * len(inf.probed)
+    if as_numpy:
+        if a.shape[0] >= HOST_PATH_MIN and inf.fast:
+            return _decode_host_numpy(inf, a, exact)
+        t = torch.from_numpy(a).to(inf.device)
     out = decode_device(inf, t, exact=exact)
     return out.cpu().numpy() if as_numpy else out
+
+
+# numpy batches at least this large go through pinned staging buffers and the
+# host-buffer decode (one streaming tcgen05 launch fed by the copy engine, or
+# chunked launches for the exact engine) instead of pageable copies, which
+# measured ~10x slower at 2^24 queries (tools/e2e_dropin.py)
+HOST_PATH_MIN = 1 << 16
+
+
+def _decode_host_numpy(inf: InferenceModel, a: np.ndarray, exact: bool) -> np.ndarray:
+    B, d, od = a.shape[0], inf.hyper.d, inf.out_dim
+    cache = inf.__dict__.setdefault("_host_path", {})
+    hd = cache.get(exact)
+    if hd is None:
+        hd = cache[exact] = HostDecoder(inf, exact=exact)
+    cap = cache.get("cap", 0)
+    if cap < B:
+        cap = max(B, 2 * cap)
+        cache["cap"] = cap
+        cache["xs"] = torch.empty(cap * d, dtype=torch.float32).pin_memory()
+        cache["out"] = torch.empty(cap * od, dtype=torch.float32).pin_memory()
+    hx = cache["xs"][:B * d].view(B, d)
+    ho = cache["out"][:B * od].view(B, od)
+    hx.copy_(torch.from_numpy(a))
+    hd(hx, ho)
+    return ho.numpy().copy()
 
 
 def decode_at(inf: InferenceModel, x, counter: TouchCounter | None = None) -> np.ndarray:
@@ -242,6 +272,11 @@ class HostDecoder:
     def __call__(self, h_xs: torch.Tensor, h_out: torch.Tensor) -> torch.Tensor:
         inf = self.inf
         assert h_xs.is_pinned() and h_out.is_pinned(), "host buffers must be pinned"
+        # the model's tables were written on the caller's stream (to_inference,
+        # deserialize): order this decode's streams after it
+        cur = torch.cuda.current_stream(inf.device)
+        for s in (self.s_in, self.s_k, self.s_out):
+            s.wait_stream(cur)
         streams = (_lib.ctypes.c_void_p(self.s_in.cuda_stream), _lib.ctypes.c_void_p(self.s_k.cuda_stream),
                    _lib.ctypes.c_void_p(self.s_out.cuda_stream))
         if self.streaming:

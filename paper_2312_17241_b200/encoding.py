@@ -10,7 +10,7 @@ weight arrays (12-48 B per point-level the reference keeps in LevelTrace).
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -19,11 +19,30 @@ from . import _lib
 from ._lib import on_device
 from .errors import DomainViolation, StaleTrace
 from .grid_model import Model
+from .hyper import AUX_PRIMES, PRIMARY_PRIMES, LevelMode
+
+
+@dataclass
+class LevelTrace:
+    """The reference's per-level trace (encoding.py:22-30)."""
+    kind: str                 # "dense" | "hashed" | "probed"
+    weights: np.ndarray       # (B, 2^d)
+    idx: np.ndarray = None    # dense/hashed: final feature rows (B, 2^d)
+    base: np.ndarray = None   # probed: (n_p * hash) mod n_f
+    row: np.ndarray = None    # probed: hash2 mod n_c
+    feat_shape: tuple = None
+    conf_shape: tuple = None
 
 
 @dataclass
 class EncodeTrace:
-    """Everything the fused backward needs (replaces list[LevelTrace])."""
+    """Everything the fused backward needs: the batch's coordinates (the
+    backward recomputes corners, hashes and weights on the fly instead of
+    storing 2^d x L index/weight arrays).  It still reads like the
+    reference's list[LevelTrace]: len() is the level count and indexing or
+    iterating materialises a level's LevelTrace (weights, idx / base, row)
+    through the per-level protocol kernels, for callers that inspect traces
+    (e.g. model_io.py:302-307 counting lookups)."""
 
     xs: torch.Tensor
     model_id: int
@@ -32,9 +51,36 @@ class EncodeTrace:
     feat_shape: tuple
     conf_shape: tuple
     surrogate: bool
+    model: object = field(default=None, repr=False, compare=False)
 
     def __len__(self):  # reference callers check len(traces) == len(levels)
         return self.n_levels
+
+    def __getitem__(self, i) -> LevelTrace:
+        from . import backend
+        m = self.model
+        if m is None:
+            raise StaleTrace("trace holds no model to materialise level traces from")
+        i = range(self.n_levels)[i]
+        spec, lv = m.specs[i], m.levels[i]
+        h = m.hyper
+        xs = self.xs.cpu().numpy()
+        feats = lv.features.values.cpu().numpy()
+        fshape = (h.n_f, h.feature_dim) if spec.mode is not LevelMode.DENSE else \
+            ((spec.resolution + 1) ** h.d, h.feature_dim)
+        if spec.mode is LevelMode.DENSE:
+            _, idx, w = backend.dense_fwd(xs, spec.resolution, feats[:fshape[0]])
+            return LevelTrace("dense", w, idx=idx, feat_shape=fshape)
+        if lv.conf is None:
+            _, idx, w = backend.hashed_fwd(xs, spec.resolution, h.n_f, feats, PRIMARY_PRIMES)
+            return LevelTrace("hashed", w, idx=idx, feat_shape=fshape)
+        _, base, row, w = backend.probed_fwd(xs, spec.resolution, h.n_f, h.n_c, h.n_p.bit_length() - 1, feats,
+                                             lv.baked.entries.cpu().numpy(), PRIMARY_PRIMES, AUX_PRIMES)
+        return LevelTrace("probed", w, base=base, row=row, feat_shape=fshape,
+                          conf_shape=(h.n_c, h.n_p))
+
+    def __iter__(self):
+        return (self[i] for i in range(self.n_levels))
 
 
 def _sfx(model):
@@ -106,7 +152,7 @@ def encode_forward(model: Model, xs, surrogate: bool = False):
     if bad is not None and int(bad.item()):
         raise DomainViolation("coordinates outside the unit hypercube")
     trace = EncodeTrace(t, id(model), model.layout_version, model.hyper.n_levels,
-                        tuple(model.feats.shape), tuple(model.conf.shape), surrogate)
+                        tuple(model.feats.shape), tuple(model.conf.shape), surrogate, model)
     return (y.cpu().numpy() if was_numpy else y), trace
 
 

@@ -31,10 +31,41 @@ from .hyper import (SEED_CONFIDENCE, SEED_FEATURES, SEED_MLP, HyperParams, Level
                     build_level_specs, grid_struct, mlp_struct, seeded_rng)
 
 
-@dataclass
 class Codebook:
-    values: torch.Tensor
-    grads: torch.Tensor | None = None
+    """A level's table (codebooks.py:24-84 attribute paths) as views into the
+    model's device buffers.  Assigning ``values`` / ``grads`` uploads into the
+    device table when the shape matches (the reference swaps the array, same
+    contents); a different shape cannot live in the fixed device layout, so
+    the tables are kept and the model's layout version moves on: traces
+    recorded before then raise StaleTrace in encode_backward, as the
+    reference's shape check does (encoding.py:122-127)."""
+
+    def __init__(self, values: torch.Tensor, grads: torch.Tensor | None = None, owner=None):
+        self._values, self._grads, self._owner = values, grads, owner
+
+    def _assign(self, dst, src):
+        src_t = src if isinstance(src, torch.Tensor) else torch.as_tensor(np.asarray(src))
+        if tuple(src_t.shape) == tuple(dst.shape):
+            with torch.no_grad():
+                dst.copy_(src_t.to(device=dst.device, dtype=dst.dtype))
+        elif self._owner is not None:
+            self._owner.layout_version += 1
+
+    @property
+    def values(self) -> torch.Tensor:
+        return self._values
+
+    @values.setter
+    def values(self, v) -> None:
+        self._assign(self._values, v)
+
+    @property
+    def grads(self) -> torch.Tensor | None:
+        return self._grads
+
+    @grads.setter
+    def grads(self, v) -> None:
+        self._assign(self._grads, v)
 
 
 @dataclass
@@ -162,10 +193,10 @@ class Model:
         slot = {lv: i for i, lv in enumerate(self.probed)}
         self.levels = []
         for s in self.specs:
-            lv = LevelState(spec=s, features=Codebook(feats[s.level], gfeats[s.level]))
+            lv = LevelState(spec=s, features=Codebook(feats[s.level], gfeats[s.level], self))
             if s.level in slot:
                 i = slot[s.level]
-                lv.conf = Codebook(self.conf[i], self.gconf[i])
+                lv.conf = Codebook(self.conf[i], self.gconf[i], self)
                 lv.baked = BakedView(self.baked[i])
             self.levels.append(lv)
         w, b = self._mlp_views(self.mlp_params)

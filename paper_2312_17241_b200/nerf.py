@@ -156,19 +156,32 @@ class NerfTrainState(TrainState):
         lo = (self.t * self.world + self.rank) * R % n
         if lo + R > n:
             lo = 0
-        pts, deltas = sample_points(self.origins[lo:lo + R], self.dirs[lo:lo + R], self.n_samples)
-        return pts, (deltas, self.rgb[lo:lo + R])
+        if not self.nerf_fused:
+            pts, deltas = sample_points(self.origins[lo:lo + R], self.dirs[lo:lo + R], self.n_samples)
+            return pts, (deltas, self.rgb[lo:lo + R])
+        # fused step: the per-sample targets (delta, rgb) written by the same kernel
+        S = self.n_samples
+        pts = torch.empty((R * S, 3), dtype=torch.float32, device=self.origins.device)
+        deltas = torch.empty(R * S, dtype=torch.float32, device=self.origins.device)
+        t4 = self.tgt4[:R * S]
+        _lib.call("pg_ray_samples_targets_f32", _lib.ptr(self.origins[lo:lo + R]), _lib.ptr(self.dirs[lo:lo + R]),
+                  _lib.ptr(self.rgb[lo:lo + R]), R, S, _lib.ptr(pts), _lib.ptr(deltas), _lib.ptr(t4),
+                  _lib.stream_ptr())
+        return pts, (deltas, self.rgb[lo:lo + R], t4)
 
     @on_device
     def compute_grads(self, xs, targets, dy_out=None) -> None:
         m, s = self.model, _lib.stream_ptr()
-        deltas, rgb = targets
+        deltas, rgb = targets[0], targets[1]
         R = rgb.shape[0]
         if self.nerf_fused:
             S = self.n_samples
-            t4 = self.tgt4[:R * S].view(R, S, 4)
-            t4[:, :, 0] = deltas.view(R, S)
-            t4[:, :, 1:] = rgb[:, None, :]
+            if len(targets) > 2:
+                t4 = targets[2]          # written by pg_ray_samples_targets_f32
+            else:                        # caller-supplied (deltas, rgb)
+                t4 = self.tgt4[:R * S].view(R, S, 4)
+                t4[:, :, 0] = deltas.view(R, S)
+                t4[:, :, 1:] = rgb[:, None, :]
             _lib.call("pg_train_fused_f32", m.grid, m.mlp_desc, _lib.ptr(xs), _lib.ptr(t4), R * S,
                       _lib.ptr(m.feats), _lib.ptr(m.baked), _lib.ptr(m.conf), _lib.ptr(m.mlp_params),
                       float(np.float32(self.scale)),

@@ -84,10 +84,15 @@ def test_nerf_step_gradients_vs_oracle(fused, R, S):
     tgt = torch.from_numpy(np.random.default_rng(6).random((R, 3)).astype(np.float32)).cuda()
     st = nerf.NerfTrainState(m, o, d, tgt, pg.TrainConfig(batch_size=R, seed=0), n_samples=S, fused=fused)
     assert st.nerf_fused == fused
-    pts, (deltas, rgb) = st.sample_batch()
+    pts, tg = st.sample_batch()
+    deltas, rgb = tg[0], tg[1]
+    if fused:   # per-sample targets written by the sampling kernel (pg_ray_samples_targets_f32)
+        t4 = tg[2].view(R, S, 4)
+        assert torch.equal(t4[:, :, 0], deltas.view(R, S))
+        assert torch.equal(t4[:, :, 1:], rgb[:, None, :].expand(R, S, 3))
     dy = torch.empty((R * S, 32), device="cuda")
     st.loss_sum.zero_()
-    st.compute_grads(pts, (deltas, rgb), dy_out=dy)
+    st.compute_grads(pts, tg, dy_out=dy)
     loss = float(st.loss_sum.item())
     oloss, ody = O.nerf_step_grads(om, pts.cpu().numpy(), deltas.cpu().numpy(), rgb.cpu().numpy(), S,
                                    st.scale)
