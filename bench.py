@@ -160,6 +160,20 @@ def smem_baked_levels(hyper, n_probed, budget=65536):
     return min(n_probed, budget // (hyper.n_c * lg // 8))
 
 
+def gathers_per_query(hyper, inf):
+    """Random global gathers one C2 query issues in decode_umma_kernel: one
+    16-byte record per level in the decode cell cache; else 2^d feature
+    rows / probing ranges, plus 2^d baked bytes for probed levels whose
+    baked indices are not in shared memory (the uncached probed levels,
+    smallest first, within the 64 KB table budget)."""
+    C = 1 << hyper.d
+    cells = inf.cells()
+    cached = [cells is not None and cells.off[lv] >= 0 for lv in range(hyper.n_levels)]
+    probed_unc = [lv for lv in inf.probed if not cached[lv]]
+    smem = smem_baked_levels(hyper, len(probed_unc))
+    return sum(1 if c else C for c in cached) + C * (len(probed_unc) - smem)
+
+
 def train_bytes_per_sample(hyper, n_probed):
     """encode fwd + recompute-bwd bytes per training sample."""
     C, L, F, d, n_p = 1 << hyper.d, hyper.n_levels, hyper.feature_dim, hyper.d, hyper.n_p
@@ -323,7 +337,7 @@ def run_gpu(args, rank, world, local_rank):
     qps = world * B_INFER / (ms_step * 1e-3)
     n_probed = len(inf.probed)
     bpq = infer_bytes_per_query(hyper, n_probed, table_bytes_per_row=2 * hyper.feature_dim)
-    gpq = (1 << hyper.d) * (hyper.n_levels + n_probed - smem_baked_levels(hyper, n_probed))
+    gpq = gathers_per_query(hyper, inf)
     achieved = B_INFER * bpq / (ms_step * 1e-3) / 1e9    # per GPU, per launch
     l2_stream, l2_gather = measure_l2(None, torch, table_mib=32)
     mlp_flops = 2 * sum(a * b for a, b in zip(inf.widths[:-1], inf.widths[1:]))
@@ -418,6 +432,8 @@ def run_gpu(args, rank, world, local_rank):
         "dtype": "f32 (fp16-stored tables, fp32 math)", "data": "synthetic",
         "config": c2_config(world),
         "engine": {"kernel": "decode_umma_kernel", "probed_levels": n_probed,
+                   "cell_cache_bytes": inf.cell_cache_bytes,
+                   "cell_cached_levels": int(sum(1 for o in (inf.cells().off if inf.cells() else []) if o >= 0)),
                    "mlp_mode": ("exact (reference order, bit-identical)" if exact
                                 else "tcgen05 kind::tf32 UMMA, 2-term split (fp32-level)")},
         "e2e": {"value": e2e_qps, "unit": "queries/s", "h2d_bytes_per_step": B_INFER * 2 * 4,

@@ -86,6 +86,19 @@ typedef struct pg_mlp {
     int32_t widths[PG_MAX_LAYERS + 1];
 } pg_mlp;
 
+/* Decode cell cache (inference-time acceleration structure, not part of the
+ * model file): for the coarsest levels, one record per grid cell holding
+ * the 2^d corners' RESOLVED fp16 feature rows (dense index, or probed base +
+ * baked offset) in corner order — one 16-byte (2-D) / 32-byte (3-D) load per
+ * query and level instead of 2^d dependent index + row gathers.  The values
+ * are copies of the table rows, so a cached decode is bit-identical to an
+ * uncached one.  off[l]: record offset of level l in 16-byte units, -1 when
+ * the level is not cached. */
+typedef struct pg_cells {
+    const void *data;
+    int64_t off[PG_MAX_LEVELS];
+} pg_cells;
+
 const char *pg_last_error(void);
 const char *pg_version(void);
 int pg_device_sm_count(int device);
@@ -226,6 +239,36 @@ int pg_decode_host_f32(const pg_grid *grid, const pg_mlp *mlp,
                        unsigned flags, int64_t chunk, float *d_xs,
                        float *d_out, float *h_out, void *stream_in,
                        void *stream_compute, void *stream_out);
+
+/* Cell cache: pg_cells_plan fills plan->off for the coarsest levels whose
+ * records fit `budget_bytes` (levels in order, stopping at the first that
+ * does not fit) and returns the bytes needed (0: nothing cached);
+ * pg_cells_build writes the records of fp16 tables feats16/baked (the
+ * InferenceModel's) into cells->data.  Rebuild after the tables change. */
+int64_t pg_cells_plan(const pg_grid *grid, int64_t budget_bytes, pg_cells *plan);
+int pg_cells_build(const pg_grid *grid, const void *feats16, const uint8_t *baked,
+                   const pg_cells *cells, void *stream);
+/* pg_decode_f32 / pg_decode_host_f32 / pg_decode_host_stream_f32 reading the
+ * cached levels from `cells` (NULL = none); every fused engine (tcgen05,
+ * FFMA, exact reference order) uses it on fp16 tables. */
+int pg_decode_cells_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
+                        int64_t B, const void *feats, const uint8_t *baked,
+                        const float *params, unsigned flags, const pg_cells *cells,
+                        float *ws, float *out, void *stream);
+int pg_decode_host_cells_f32(const pg_grid *grid, const pg_mlp *mlp,
+                             const float *h_xs, int64_t B, const void *feats,
+                             const uint8_t *baked, const float *params,
+                             unsigned flags, const pg_cells *cells, int64_t chunk,
+                             float *d_xs, float *d_out, float *h_out,
+                             void *stream_in, void *stream_compute,
+                             void *stream_out);
+int pg_decode_host_stream_cells_f32(const pg_grid *grid, const pg_mlp *mlp,
+                                    const float *h_xs, int64_t B, const void *feats,
+                                    const uint8_t *baked, const float *params,
+                                    unsigned flags, const pg_cells *cells, int64_t chunk,
+                                    float *d_xs, float *d_out, uint32_t *d_flags,
+                                    float *h_out, void *stream_in,
+                                    void *stream_compute, void *stream_out);
 
 /* Streaming end-to-end decode from HOST memory: one tcgen05 decode launch
  * over the whole batch consumes `chunk`-query pieces as

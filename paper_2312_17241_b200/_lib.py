@@ -42,6 +42,10 @@ class PgMlp(ctypes.Structure):
     _fields_ = [("n_layers", ctypes.c_int32), ("widths", ctypes.c_int32 * (PG_MAX_LAYERS + 1))]
 
 
+class PgCells(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("off", ctypes.c_int64 * PG_MAX_LEVELS)]
+
+
 class PgError(RuntimeError):
     """A non-zero status from the CUDA library (message from pg_last_error)."""
 
@@ -55,6 +59,7 @@ _D = ctypes.c_double
 _F = ctypes.c_float
 _G = ctypes.POINTER(PgGrid)
 _M = ctypes.POINTER(PgMlp)
+_C = ctypes.POINTER(PgCells)
 
 _SIGS = {}
 for _t, _s in (("f32", _F), ("f64", _D)):
@@ -79,6 +84,11 @@ for _t, _s in (("f32", _F), ("f64", _D)):
 _SIGS.update({
     "pg_dedup_rows": [_P, _I64, _I64, _P, _P, _P, _P, _P],
     "pg_decode_f32": [_G, _M, _P, _I64, _P, _P, _P, ctypes.c_uint, _P, _P, _P],
+    "pg_decode_cells_f32": [_G, _M, _P, _I64, _P, _P, _P, ctypes.c_uint, _C, _P, _P, _P],
+    "pg_decode_host_stream_cells_f32": [_G, _M, _P, _I64, _P, _P, _P, ctypes.c_uint, _C, _I64, _P, _P, _P, _P,
+                                        _P, _P, _P],
+    "pg_cells_build": [_G, _P, _P, _C, _P],
+    "pg_decode_host_cells_f32": [_G, _M, _P, _I64, _P, _P, _P, ctypes.c_uint, _C, _I64, _P, _P, _P, _P, _P, _P],
     "pg_decode_host_f32": [_G, _M, _P, _I64, _P, _P, _P, ctypes.c_uint, _I64, _P, _P, _P, _P, _P, _P],
     "pg_touched_to_f32": [_P, _I64, _P, _P],
     "pg_composite_fwd_f32": [_P, _P, _I64, _I, _P, _P, _P],
@@ -115,6 +125,7 @@ _SIGS.update({
     "pg_probe_gather": [_P, _I64, _I64, _U32, _P, _P],
 })
 _RESTYPE_I64 = {"pg_dedup_workspace_bytes": [_I64, _I64],
+                "pg_cells_plan": [_G, _I64, _C],
                 "pg_mlp_train_workspace_floats": [_I64, _M],
                 "pg_mlp_acts_floats": [_I64, _M]}
 

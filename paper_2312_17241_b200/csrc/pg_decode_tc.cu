@@ -68,6 +68,8 @@ struct TabPlan {
     int32_t off[PG_MAX_LEVELS];  // -1: global memory
     int32_t pbits;               // packed bits per baked index; 0 when N_p == 1
     int32_t bytes;
+    const uint4 *cells;          // decode cell cache (pg_cells), or null
+    int32_t cell[PG_MAX_LEVELS]; // level's record offset in uint4 units, -1: not cached
 };
 using Stream = DecodeStream;
 using pg::wait_flag;
@@ -97,13 +99,15 @@ template <> struct RangeLoad<__half> {
     }
 };
 
-// encode_level_fwd2 (pg_encode_dev.cuh) with optional on-chip tables:
-// identical indices, weights and blend order, so the result is bit-identical.
+// encode_level_fwd2 (pg_encode_dev.cuh) with optional on-chip tables and
+// the decode cell cache: identical indices, weights and blend order, so the
+// result is bit-identical.
 template <typename FT, int D>
 __device__ __forceinline__ float2 encode_level_fwd2_tab(const pg_grid &g, int l, const float (&x)[D],
                                                         const FT *__restrict__ feats,
                                                         const uint8_t *__restrict__ baked,
-                                                        const unsigned char *tabs, int off, int pbits) {
+                                                        const unsigned char *tabs, int off, int pbits,
+                                                        const uint4 *__restrict__ cellrec = nullptr) {
     constexpr int C = 1 << D;
     const uint32_t nf_mask = (uint32_t)g.n_f - 1u, nc_mask = (uint32_t)g.n_c - 1u;
     const int res = g.res[l], kind = g.kind[l];
@@ -114,6 +118,7 @@ __device__ __forceinline__ float2 encode_level_fwd2_tab(const pg_grid &g, int l,
         c[a] = cell_coord(x[a], res, t[a]);
         omt[a] = __fsub_rn(1.0f, t[a]);
     }
+    if (RangeLoad<FT>::ok && cellrec != nullptr) return encode_level_fwd2_cell<D>(g, l, x, cellrec);
     int idx[C];
     float w[C];
 #pragma unroll
@@ -351,10 +356,13 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
 #pragma unroll 2
             for (int it = 0; it < 4; ++it) {
                 const int P = lsub + 2 * it;  // warp-uniform level pair (2P, 2P+1)
+                const int ca = plan.cell[2 * P], cb = plan.cell[2 * P + 1];
                 const float2 ya = encode_level_fwd2_tab<FT, D>(g, 2 * P, x, feats, baked, tabs,
-                                                               plan.off[2 * P], plan.pbits);
+                                                               plan.off[2 * P], plan.pbits,
+                                                               ca >= 0 ? plan.cells + ca : nullptr);
                 const float2 yb = encode_level_fwd2_tab<FT, D>(g, 2 * P + 1, x, feats, baked, tabs,
-                                                               plan.off[2 * P + 1], plan.pbits);
+                                                               plan.off[2 * P + 1], plan.pbits,
+                                                               cb >= 0 ? plan.cells + cb : nullptr);
                 float h[4], lo[4];
                 umma::split_tf32(ya.x, h[0], lo[0]);
                 umma::split_tf32(ya.y, h[1], lo[1]);
@@ -475,14 +483,23 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
 
 // Host: choose the on-chip tables (smallest first, they save the same 2^d
 // gathers per query each) within the shared-memory budget.
-static tc::TabPlan plan_tables(const pg_grid *g, size_t feat_bytes, int budget, int kinds) {
+static tc::TabPlan plan_tables(const pg_grid *g, size_t feat_bytes, int budget, int kinds, const pg_cells *cells) {
     tc::TabPlan p;
-    for (int l = 0; l < PG_MAX_LEVELS; ++l) p.off[l] = -1;
+    p.cells = nullptr;
+    for (int l = 0; l < PG_MAX_LEVELS; ++l) {
+        p.off[l] = -1;
+        p.cell[l] = -1;
+    }
+    if (cells && cells->data && feat_bytes == 2) {
+        p.cells = reinterpret_cast<const uint4 *>(cells->data);
+        for (int l = 0; l < g->n_levels; ++l) p.cell[l] = cells->off[l] >= 0 ? (int32_t)cells->off[l] : -1;
+    }
     p.pbits = g->log2_np == 0 ? 0 : g->log2_np == 1 ? 1 : g->log2_np == 2 ? 2 : g->log2_np <= 4 ? 4 : -1;
     p.bytes = 0;
     std::vector<std::pair<int64_t, int>> cand;
     for (int l = 0; l < g->n_levels; ++l) {
         int64_t bytes = -1;
+        if (p.cell[l] >= 0) continue;   // served by the cell cache
         if (g->kind[l] == PG_LEVEL_DENSE && (kinds & 1)) {
             int64_t e = 1;
             for (int a = 0; a < g->d; ++a) e *= (int64_t)(g->res[l] + 1);
@@ -517,7 +534,7 @@ static void launch_umma(const pg_grid *g, const tc::TabPlan &plan, int smem, int
 
 int decode_umma(const pg_grid *g, int od, const float *xs, int64_t B, const void *feats, bool half,
                 const uint8_t *baked, const float *params, int sig, int table_flags, float *out, cudaStream_t s,
-                const tc::Stream &st) {
+                const tc::Stream &st, const pg_cells *cells) {
     // tuning knobs for the table variant (ablations in tools/gpu_decode_ab.sh)
     static const int env_budget = getenv("PG_DECODE_TABLE_BYTES") ? atoi(getenv("PG_DECODE_TABLE_BYTES")) : -1;
     static const int env_kinds = getenv("PG_DECODE_TABLE_KINDS") ? atoi(getenv("PG_DECODE_TABLE_KINDS")) : 2;
@@ -542,7 +559,7 @@ int decode_umma(const pg_grid *g, int od, const float *xs, int64_t B, const void
         budget = env_budget >= 0 ? env_budget : 65536;
         if (budget > room) budget = room;
     }
-    const tc::TabPlan plan = plan_tables(g, half ? 2 : 4, budget, env_kinds);
+    const tc::TabPlan plan = plan_tables(g, half ? 2 : 4, budget, env_kinds, cells);
     const int smem = fixed + plan.bytes;
     const int per_sm = ng == 3 ? 1 : 3;
     const int64_t ntiles = (B + tc::kTP - 1) / tc::kTP;
@@ -570,4 +587,90 @@ int decode_umma(const pg_grid *g, int od, const float *xs, int64_t B, const void
     return check_launch("decode_umma");
 }
 
+// ---- decode cell cache (pg_cells): records of the 2^d resolved corner rows
+// per cell of the coarsest levels (pg_cells_plan / pg_cells_build)
+template <int D>
+__global__ void build_cells_kernel(const pg_grid g, int l, const __half *__restrict__ feats,
+                                   const uint8_t *__restrict__ baked, uint32_t *__restrict__ rec, int64_t ncells) {
+    constexpr int C = 1 << D;
+    const uint32_t nf_mask = (uint32_t)g.n_f - 1u, nc_mask = (uint32_t)g.n_c - 1u;
+    const int res = g.res[l], kind = g.kind[l];
+    const uint32_t *tab = reinterpret_cast<const uint32_t *>(feats + (int64_t)l * g.n_f * 2);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ncells;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int c[D];
+        int64_t rem = i;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            c[a] = (int)(rem % res);
+            rem /= res;
+        }
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            int idx;
+            if (kind == PG_LEVEL_DENSE) {
+                idx = corner_dense<D>(k, c, res + 1);
+            } else {
+                const uint32_t h = corner_hash<D>(k, c, g.primary);
+                if (kind == PG_LEVEL_HASHED) {
+                    idx = (int)(h & nf_mask);
+                } else {
+                    const uint32_t r = corner_hash<D>(k, c, g.aux) & nc_mask;
+                    idx = (int)((h << g.log2_np) & nf_mask) + (int)baked[(int64_t)g.slot[l] * g.n_c + r];
+                }
+            }
+            rec[i * C + k] = tab[idx];
+        }
+    }
+}
+
 }  // namespace pg
+
+using namespace pg;
+
+extern "C" {
+
+int64_t pg_cells_plan(const pg_grid *grid, int64_t budget_bytes, pg_cells *plan) {
+    if (!grid || !plan) return -1;
+    const int C = 1 << grid->d;
+    int64_t total = 0;
+    bool open = true;
+    plan->data = nullptr;
+    for (int l = 0; l < PG_MAX_LEVELS; ++l) {
+        plan->off[l] = -1;
+        if (!open || l >= grid->n_levels) continue;
+        int64_t cells = 1;
+        for (int a = 0; a < grid->d; ++a) cells *= grid->res[l];
+        const int64_t bytes = cells * C * 4;
+        if (total + bytes > budget_bytes) {
+            open = false;
+            continue;
+        }
+        plan->off[l] = total / 16;
+        total += bytes;
+    }
+    return total;
+}
+
+int pg_cells_build(const pg_grid *grid, const void *feats16, const uint8_t *baked, const pg_cells *cells,
+                   void *stream) {
+    if (int e = validate_grid(grid)) return e;
+    PG_REQUIRE(cells != nullptr, "cells: null");
+    PG_REQUIRE(grid->feature_dim == 2, "cell cache: F = 2 fp16 tables only");
+    cudaStream_t s = as_stream(stream);
+    for (int l = 0; l < grid->n_levels; ++l) {
+        if (cells->off[l] < 0) continue;
+        PG_REQUIRE(cells->data != nullptr, "cells: null data with cached levels");
+        int64_t ncells = 1;
+        for (int a = 0; a < grid->d; ++a) ncells *= grid->res[l];
+        uint32_t *rec = reinterpret_cast<uint32_t *>(const_cast<void *>(cells->data)) + cells->off[l] * 4;
+        const int grd = grid_for(ncells, 256, 148 * 32);
+        if (grid->d == 2)
+            build_cells_kernel<2><<<grd, 256, 0, s>>>(*grid, l, (const __half *)feats16, baked, rec, ncells);
+        else
+            build_cells_kernel<3><<<grd, 256, 0, s>>>(*grid, l, (const __half *)feats16, baked, rec, ncells);
+    }
+    return check_launch("cells_build");
+}
+
+}  // extern "C"

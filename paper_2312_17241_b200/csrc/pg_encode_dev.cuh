@@ -15,6 +15,53 @@ __device__ __forceinline__ void ld_nc_v8(const float *p, float (&v)[8]) {
         : "l"(p));
 }
 
+// Decode cell cache (pg_cells): per-level record offsets (uint4 units, -1 =
+// not cached) into one buffer of per-cell records holding the 2^d resolved
+// corner rows (binary16 F = 2, 4 B each) in corner order.
+struct CellMap {
+    const uint4 *cells;
+    int32_t off[PG_MAX_LEVELS];
+};
+
+// Forward of a cached level: ONE 16 B (2-D) / 32 B (3-D) record load instead
+// of 2^d index + row gathers; same weights, values and blend order as
+// encode_level_fwd2, so bit-identical.
+template <int D>
+__device__ __forceinline__ float2 encode_level_fwd2_cell(const pg_grid &g, int l, const float (&x)[D],
+                                                         const uint4 *__restrict__ rec) {
+    constexpr int C = 1 << D;
+    const int res = g.res[l];
+    int c[D];
+    float t[D], omt[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        c[a] = cell_coord(x[a], res, t[a]);
+        omt[a] = __fsub_rn(1.0f, t[a]);
+    }
+    int64_t cell = c[D - 1];
+#pragma unroll
+    for (int a = D - 2; a >= 0; --a) cell = cell * res + c[a];
+    uint32_t r[C];
+    if constexpr (D == 2) {
+        const uint4 v = __ldg(rec + cell);
+        r[0] = v.x; r[1 % C] = v.y; r[2 % C] = v.z; r[3 % C] = v.w;
+    } else {
+        float v8[8];
+        ld_nc_v8(reinterpret_cast<const float *>(rec + 2 * cell), v8);
+#pragma unroll
+        for (int k = 0; k < C; ++k) r[k] = __float_as_uint(v8[k % 8]);
+    }
+    float y0 = 0.0f, y1 = 0.0f;
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+        const float w = corner_weight<float, D>(k, t, omt);
+        const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&r[k]));
+        y0 = __fadd_rn(y0, __fmul_rn(w, f.x));
+        y1 = __fadd_rn(y1, __fmul_rn(w, f.y));
+    }
+    return make_float2(y0, y1);
+}
+
 // Forward: blended F=2 feature of point x at level l (bit-exact vs _core).
 template <typename FT, int D>
 __device__ __forceinline__ float2 encode_level_fwd2(const pg_grid &g, int l, const float (&x)[D],

@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(512, 1)
     decode_fused_kernel(const pg_grid g, const float *__restrict__ xs, int64_t B,
                         const FT *__restrict__ feats, const uint8_t *__restrict__ baked,
                         const float *__restrict__ params, int out_dim, int sigmoid,
-                        float *__restrict__ out, int32_t *__restrict__ bad) {
+                        float *__restrict__ out, int32_t *__restrict__ bad, const CellMap cmap) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     DecodeSmem &S = *reinterpret_cast<DecodeSmem *>(smem_raw);
     const int gid = threadIdx.x >> 8, tid = threadIdx.x & 255;
@@ -281,7 +281,11 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll 2
         for (int it = 0; it < 8; ++it) {
             const int l = 2 * it + lhalf;  // warp-uniform
-            const float2 yv = encode_level_fwd2_rng<FT, D>(g, l, x, feats, baked);
+            float2 yv;
+            if (std::is_same<FT, __half>::value && cmap.off[l] >= 0)
+                yv = encode_level_fwd2_cell<D>(g, l, x, cmap.cells + cmap.off[l]);
+            else
+                yv = encode_level_fwd2_rng<FT, D>(g, l, x, feats, baked);
             const float y0 = yv.x, y1 = yv.y;
             sm.actA[swz(2 * l, pl)] = y0;
             sm.actA[swz(2 * l + 1, pl)] = y1;
@@ -333,7 +337,7 @@ static int sm_count() { return device_sms(); }
 template <typename FT, int D, bool EXACT>
 static void launch_decode(const pg_grid *g, const float *xs, int64_t B, const void *feats,
                           const uint8_t *baked, const float *params, int out_dim, int sig,
-                          float *out, int32_t *bad, cudaStream_t s) {
+                          float *out, int32_t *bad, cudaStream_t s, const CellMap &cmap) {
     static DeviceOnce configured;
     const int smem = (int)sizeof(DecodeSmem);
     if (configured.first())
@@ -343,16 +347,16 @@ static void launch_decode(const pg_grid *g, const float *xs, int64_t B, const vo
     const int64_t want = (ntiles + 1) / 2, cap = (int64_t)sm_count();
     const int grd = (int)(want < cap ? want : cap);
     decode_fused_kernel<FT, D, EXACT><<<grd, 512, smem, s>>>(*g, xs, B, (const FT *)feats, baked,
-                                                            params, out_dim, sig, out, bad);
+                                                            params, out_dim, sig, out, bad, cmap);
 }
 
 int decode_umma(const pg_grid *g, int od, const float *xs, int64_t B, const void *feats, bool half,
                 const uint8_t *baked, const float *params, int sig, int table_flags, float *out, cudaStream_t s,
-                const DecodeStream &st = DecodeStream());
+                const DecodeStream &st = DecodeStream(), const pg_cells *cells = nullptr);
 
 int decode_device(const pg_grid *g, const pg_mlp *m, const float *xs, int64_t B,
                   const void *feats, const uint8_t *baked, const float *params, unsigned flags,
-                  float *ws, float *out, int32_t *bad, cudaStream_t s) {
+                  float *ws, float *out, int32_t *bad, cudaStream_t s, const pg_cells *cells = nullptr) {
     if (int e = validate_grid(g)) return e;
     if (int e = validate_mlp(m)) return e;
     PG_REQUIRE(m->widths[0] == g->n_levels * g->feature_dim, "MLP input width != L*F");
@@ -364,10 +368,17 @@ int decode_device(const pg_grid *g, const pg_mlp *m, const float *xs, int64_t B,
         const int od = m->widths[3];
         if (!exact && !(flags & PG_NO_TENSOR))  // tcgen05 path (pg_decode_tc.cu)
             return decode_umma(g, od, xs, B, feats, half, baked, params, sig, (int)(flags & (PG_SMEM_TABLES | PG_NO_SMEM_TABLES)),
-                               out, s);
+                               out, s, DecodeStream(), cells);
+        CellMap cmap;
+        cmap.cells = nullptr;
+        for (int l = 0; l < PG_MAX_LEVELS; ++l) cmap.off[l] = -1;
+        if (half && cells && cells->data) {
+            cmap.cells = reinterpret_cast<const uint4 *>(cells->data);
+            for (int l = 0; l < g->n_levels; ++l) cmap.off[l] = cells->off[l] >= 0 ? (int32_t)cells->off[l] : -1;
+        }
 #define PG_DEC(FT_, D_)                                                                    \
-    (exact ? launch_decode<FT_, D_, true>(g, xs, B, feats, baked, params, od, sig, out, bad, s) \
-           : launch_decode<FT_, D_, false>(g, xs, B, feats, baked, params, od, sig, out, bad, s))
+    (exact ? launch_decode<FT_, D_, true>(g, xs, B, feats, baked, params, od, sig, out, bad, s, cmap) \
+           : launch_decode<FT_, D_, false>(g, xs, B, feats, baked, params, od, sig, out, bad, s, cmap))
         if (half) {
             if (g->d == 2) PG_DEC(__half, 2); else PG_DEC(__half, 3);
         } else {
@@ -952,11 +963,17 @@ int pg_decode_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs, int64
     return decode_device(grid, mlp, xs, B, feats, baked, params, flags, ws, out, nullptr,
                          as_stream(stream));
 }
+int pg_decode_cells_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs, int64_t B,
+                        const void *feats, const uint8_t *baked, const float *params, unsigned flags,
+                        const pg_cells *cells, float *ws, float *out, void *stream) {
+    return decode_device(grid, mlp, xs, B, feats, baked, params, flags, ws, out, nullptr,
+                         as_stream(stream), cells);
+}
 
-int pg_decode_host_f32(const pg_grid *grid, const pg_mlp *mlp, const float *h_xs, int64_t B,
+static int decode_host_chunked(const pg_grid *grid, const pg_mlp *mlp, const float *h_xs, int64_t B,
                        const void *feats, const uint8_t *baked, const float *params,
                        unsigned flags, int64_t chunk, float *d_xs, float *d_out, float *h_out,
-                       void *stream_in, void *stream_compute, void *stream_out) {
+                       void *stream_in, void *stream_compute, void *stream_out, const pg_cells *cells) {
     if (int e = validate_grid(grid)) return e;
     if (int e = validate_mlp(mlp)) return e;
     PG_REQUIRE(decode_fast_ok(grid, mlp), "host decode needs the fused [32,64,64,<=4] shape");
@@ -996,7 +1013,7 @@ int pg_decode_host_f32(const pg_grid *grid, const pg_mlp *mlp, const float *h_xs
         cudaEventRecord(ev_in[slot], si);
         cudaStreamWaitEvent(sk, ev_in[slot], 0);
         if (c >= 2) cudaStreamWaitEvent(sk, ev_out[slot], 0);   // copy-out c-2 has drained this output slot
-        if ((err = decode_device(grid, mlp, dx, n, feats, baked, params, flags, nullptr, dout, nullptr, sk)))
+        if ((err = decode_device(grid, mlp, dx, n, feats, baked, params, flags, nullptr, dout, nullptr, sk, cells)))
             break;
         cudaEventRecord(ev_k[slot], sk);
         cudaStreamWaitEvent(so, ev_k[slot], 0);
@@ -1013,6 +1030,20 @@ int pg_decode_host_f32(const pg_grid *grid, const pg_mlp *mlp, const float *h_xs
     }
     if (err) return err;
     return check_launch("decode_host");
+}
+int pg_decode_host_f32(const pg_grid *grid, const pg_mlp *mlp, const float *h_xs, int64_t B,
+                       const void *feats, const uint8_t *baked, const float *params,
+                       unsigned flags, int64_t chunk, float *d_xs, float *d_out, float *h_out,
+                       void *stream_in, void *stream_compute, void *stream_out) {
+    return decode_host_chunked(grid, mlp, h_xs, B, feats, baked, params, flags, chunk, d_xs, d_out, h_out,
+                               stream_in, stream_compute, stream_out, nullptr);
+}
+int pg_decode_host_cells_f32(const pg_grid *grid, const pg_mlp *mlp, const float *h_xs, int64_t B,
+                             const void *feats, const uint8_t *baked, const float *params, unsigned flags,
+                             const pg_cells *cells, int64_t chunk, float *d_xs, float *d_out, float *h_out,
+                             void *stream_in, void *stream_compute, void *stream_out) {
+    return decode_host_chunked(grid, mlp, h_xs, B, feats, baked, params, flags, chunk, d_xs, d_out, h_out,
+                               stream_in, stream_compute, stream_out, cells);
 }
 
 // Streaming end-to-end decode: ONE tcgen05 decode launch over the whole
@@ -1058,10 +1089,10 @@ static bool is_pinned_host(const void *p) {
     return a.type == cudaMemoryTypeHost;
 }
 
-int pg_decode_host_stream_f32(const pg_grid *grid, const pg_mlp *mlp, const float *h_xs, int64_t B,
+static int decode_host_stream(const pg_grid *grid, const pg_mlp *mlp, const float *h_xs, int64_t B,
                               const void *feats, const uint8_t *baked, const float *params, unsigned flags,
                               int64_t chunk, float *d_xs, float *d_out, uint32_t *d_flags, float *h_out,
-                              void *stream_in, void *stream_compute, void *stream_out) {
+                              void *stream_in, void *stream_compute, void *stream_out, const pg_cells *cells) {
     if (int e = validate_grid(grid)) return e;
     if (int e = validate_mlp(mlp)) return e;
     PG_REQUIRE(pg_decode_stream_supported(grid, mlp, flags),
@@ -1102,7 +1133,7 @@ int pg_decode_host_stream_f32(const pg_grid *grid, const pg_mlp *mlp, const floa
         cudaEventRecord(dk0, sk);
     }
     int err = decode_umma(grid, od, d_xs, B, feats, half, baked, params, (flags & PG_SIGMOID) ? 1 : 0,
-                          (int)(flags & (PG_SMEM_TABLES | PG_NO_SMEM_TABLES)), d_out, sk, st);
+                          (int)(flags & (PG_SMEM_TABLES | PG_NO_SMEM_TABLES)), d_out, sk, st, cells);
     if (dbg) cudaEventRecord(dk1, sk);
     for (int64_t c = 0; c < nch && !err && !dbg_nocopy; ++c) {
         const int64_t off = c * chunk, n = B - off < chunk ? B - off : chunk;
@@ -1134,6 +1165,21 @@ int pg_decode_host_stream_f32(const pg_grid *grid, const pg_mlp *mlp, const floa
     }
     if (err) return err;
     return check_launch("decode_host_stream");
+}
+int pg_decode_host_stream_f32(const pg_grid *grid, const pg_mlp *mlp, const float *h_xs, int64_t B,
+                              const void *feats, const uint8_t *baked, const float *params, unsigned flags,
+                              int64_t chunk, float *d_xs, float *d_out, uint32_t *d_flags, float *h_out,
+                              void *stream_in, void *stream_compute, void *stream_out) {
+    return decode_host_stream(grid, mlp, h_xs, B, feats, baked, params, flags, chunk, d_xs, d_out, d_flags, h_out,
+                              stream_in, stream_compute, stream_out, nullptr);
+}
+int pg_decode_host_stream_cells_f32(const pg_grid *grid, const pg_mlp *mlp, const float *h_xs, int64_t B,
+                                    const void *feats, const uint8_t *baked, const float *params, unsigned flags,
+                                    const pg_cells *cells, int64_t chunk, float *d_xs, float *d_out,
+                                    uint32_t *d_flags, float *h_out, void *stream_in, void *stream_compute,
+                                    void *stream_out) {
+    return decode_host_stream(grid, mlp, h_xs, B, feats, baked, params, flags, chunk, d_xs, d_out, d_flags, h_out,
+                              stream_in, stream_compute, stream_out, cells);
 }
 
 // Zero-copy end-to-end decode: the decode kernel reads the coordinates from

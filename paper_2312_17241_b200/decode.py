@@ -14,6 +14,7 @@ input row either way (model_io.py:294-295), so any batching is bit-identical.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -55,6 +56,35 @@ class InferenceModel:
         self.params = params.to(self.device).contiguous()        # fp32 of fp16-rounded MLP
         self.fast = (hyper.feature_dim == 2 and hyper.n_levels == 16 and len(self.widths) == 4
                      and self.widths[1] == 64 and self.widths[2] == 64 and hyper.out_dim <= 4)
+        self.cell_budget = CELL_BUDGET
+        self._cells = None
+
+    def cells(self):
+        """The decode cell cache of this model's tables (built on first use;
+        None when no level fits the budget or the tables are not fp16)."""
+        if self._cells is None:
+            plan = _lib.PgCells()
+            nbytes = 0
+            if self.feats16.dtype == torch.float16 and self.cell_budget > 0:
+                nbytes = int(_lib.lib().pg_cells_plan(self.grid, int(self.cell_budget), plan))
+            if nbytes <= 0:
+                self._cells = (None, None)
+            else:
+                buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+                plan.data = buf.data_ptr()
+                with torch.cuda.device(self.device):
+                    _lib.call("pg_cells_build", self.grid, _lib.ptr(self.feats16), _lib.ptr(self.baked), plan,
+                              _lib.stream_ptr())
+                self._cells = (plan, buf)
+        return self._cells[0]
+
+    def invalidate_cells(self) -> None:
+        """Drop the cell cache (call after editing feats16 / baked in place)."""
+        self._cells = None
+
+    @property
+    def cell_cache_bytes(self) -> int:
+        return 0 if self._cells is None or self._cells[1] is None else self._cells[1].numel()
 
     @property
     def out_dim(self) -> int:
@@ -85,6 +115,14 @@ def to_inference(model: Model, width: int = 0, height: int = 0) -> InferenceMode
                           params, model.device)
 
 
+# Bytes of device memory the decode cell cache may use per inference model
+# (coarsest levels first; pg_cells_plan).  0 disables it.  Measured at C2
+# (log2 n_f 16, N_p 4, 2^24 queries): no cache 3.37e9 q/s, 8 MiB 4.01e9,
+# 32 MiB (28 used) 4.63e9, 96 MiB (65 used: the 11 coarsest levels) 5.22e9;
+# the next level would need 88 MB more and no longer stays L2-resident.
+CELL_BUDGET = int(float(os.environ.get("PG_DECODE_CELL_MB", "96")) * (1 << 20))
+
+
 def _flags(inf: InferenceModel, exact: bool, tensor: bool = True, smem_tables=None) -> int:
     f = _lib.PG_HALF_FEATS
     if exact:
@@ -101,7 +139,7 @@ def _flags(inf: InferenceModel, exact: bool, tensor: bool = True, smem_tables=No
 @on_device
 def decode_device(inf: InferenceModel, xs: torch.Tensor, out: torch.Tensor = None,
                   exact: bool = True, stream=None, tensor: bool = True,
-                  smem_tables=None) -> torch.Tensor:
+                  smem_tables=None, cells: bool = True) -> torch.Tensor:
     """Fused encode + MLP on device-resident queries; returns (B, out_dim).
 
     exact=True: reference operation order on CUDA cores (bit-identical).
@@ -109,7 +147,9 @@ def decode_device(inf: InferenceModel, xs: torch.Tensor, out: torch.Tensor = Non
     tf32, fp32-level accuracy); tensor=False keeps FFMA instead (ablation);
     smem_tables forces (True) or forbids (False) serving the probed levels'
     baked indices from bit-packed shared-memory copies; None = automatic
-    (on for N_p = 2 and 4, where it measured faster)."""
+    (on for N_p = 2 and 4, where it measured faster).  cells: read the
+    coarsest levels from the model's decode cell cache (tcgen05 engine;
+    bit-identical — the records are copies of the resolved table rows)."""
     B = xs.shape[0]
     if out is None:
         out = torch.empty((B, inf.out_dim), dtype=torch.float32, device=inf.device)
@@ -117,9 +157,15 @@ def decode_device(inf: InferenceModel, xs: torch.Tensor, out: torch.Tensor = Non
     if not inf.fast:
         n = B * inf.hyper.encoded_width + 2 * B * max(inf.widths)
         ws = torch.empty(max(n, 1), dtype=torch.float32, device=inf.device)
-    _lib.call("pg_decode_f32", inf.grid, inf.mlp_desc, _lib.ptr(xs), B, _lib.ptr(inf.feats16),
-              _lib.ptr(inf.baked), _lib.ptr(inf.params), _flags(inf, exact, tensor, smem_tables), _lib.ptr(ws),
-              _lib.ptr(out), _lib.stream_ptr(stream))
+    cells = inf.cells() if (cells and inf.fast) else None
+    if cells is not None:
+        _lib.call("pg_decode_cells_f32", inf.grid, inf.mlp_desc, _lib.ptr(xs), B, _lib.ptr(inf.feats16),
+                  _lib.ptr(inf.baked), _lib.ptr(inf.params), _flags(inf, exact, tensor, smem_tables), cells,
+                  _lib.ptr(ws), _lib.ptr(out), _lib.stream_ptr(stream))
+    else:
+        _lib.call("pg_decode_f32", inf.grid, inf.mlp_desc, _lib.ptr(xs), B, _lib.ptr(inf.feats16),
+                  _lib.ptr(inf.baked), _lib.ptr(inf.params), _flags(inf, exact, tensor, smem_tables), _lib.ptr(ws),
+                  _lib.ptr(out), _lib.stream_ptr(stream))
     return out
 
 
@@ -134,7 +180,7 @@ def decode_pixels(inf: InferenceModel, xs, counter: TouchCounter | None = None,
         a = np.ascontiguousarray(np.asarray(xs, dtype=np.float32))
         if a.ndim != 2 or a.shape[1] != d:
             raise DomainViolation(f"expected (batch, {d}) coordinates, got {a.shape}")
-        if np.any(a < 0.0) or np.any(a > 1.0):
+        if not (a.shape[0] >= HOST_PATH_MIN and inf.fast) and (np.any(a < 0.0) or np.any(a > 1.0)):
             raise DomainViolation("coordinates outside the unit hypercube")
         t = torch.from_numpy(a).to(inf.device)
     else:
@@ -176,9 +222,14 @@ def _decode_host_numpy(inf: InferenceModel, a: np.ndarray, exact: bool) -> np.nd
         cache["out"] = torch.empty(cap * od, dtype=torch.float32).pin_memory()
     hx = cache["xs"][:B * d].view(B, d)
     ho = cache["out"][:B * od].view(B, od)
-    hx.copy_(torch.from_numpy(a))
+    hx.copy_(torch.from_numpy(a))                 # multi-threaded host copy into pinned memory
+    lo, hi = torch.aminmax(hx)                    # encoding.py:37-38 (NaN passes, as there)
+    if float(lo) < 0.0 or float(hi) > 1.0:
+        raise DomainViolation("coordinates outside the unit hypercube")
     hd(hx, ho)
-    return ho.numpy().copy()
+    res = torch.empty((B, od), dtype=torch.float32)
+    res.copy_(ho)
+    return res.numpy()
 
 
 def decode_at(inf: InferenceModel, x, counter: TouchCounter | None = None) -> np.ndarray:
@@ -237,12 +288,13 @@ class HostDecoder:
 
     @on_device
     def __init__(self, inf: InferenceModel, chunk: int = 1 << 21, exact: bool = False,
-                 stream: bool | None = None, stream_chunk: int = 1 << 18):
+                 stream: bool | None = None, stream_chunk: int = 1 << 18, cells: bool = True):
         if not inf.fast:
             raise ValueError("host decode needs the fused [32,64,64,<=4] shape")
         if stream_chunk < 128 or stream_chunk & (stream_chunk - 1):
             raise ValueError("stream_chunk must be a power of two >= 128")
         self.inf, self.chunk, self.exact, self.stream_chunk = inf, chunk, exact, stream_chunk
+        self.cells = cells
         d, od = inf.hyper.d, inf.out_dim
         ok = bool(_lib.lib().pg_decode_stream_supported(inf.grid, inf.mlp_desc, _flags(inf, exact)))
         if stream and not ok:
@@ -272,8 +324,10 @@ class HostDecoder:
     def __call__(self, h_xs: torch.Tensor, h_out: torch.Tensor) -> torch.Tensor:
         inf = self.inf
         assert h_xs.is_pinned() and h_out.is_pinned(), "host buffers must be pinned"
-        # the model's tables were written on the caller's stream (to_inference,
-        # deserialize): order this decode's streams after it
+        # the model's tables (to_inference, deserialize) and its cell cache
+        # (built on first use) are written on the caller's stream: order this
+        # decode's streams after it
+        cells = inf.cells() if self.cells else None
         cur = torch.cuda.current_stream(inf.device)
         for s in (self.s_in, self.s_k, self.s_out):
             s.wait_stream(cur)
@@ -282,15 +336,27 @@ class HostDecoder:
         if self.streaming:
             B = h_xs.shape[0]
             self._reserve(B)
-            _lib.call("pg_decode_host_stream_f32", inf.grid, inf.mlp_desc, _lib.ptr(h_xs), B,
-                      _lib.ptr(inf.feats16), _lib.ptr(inf.baked), _lib.ptr(inf.params),
-                      _flags(inf, self.exact), self.stream_chunk, _lib.ptr(self.d_xs), _lib.ptr(self.d_out),
-                      _lib.ptr(self.d_flags), _lib.ptr(h_out), *streams)
+            if cells is not None:
+                _lib.call("pg_decode_host_stream_cells_f32", inf.grid, inf.mlp_desc, _lib.ptr(h_xs), B,
+                          _lib.ptr(inf.feats16), _lib.ptr(inf.baked), _lib.ptr(inf.params),
+                          _flags(inf, self.exact), cells, self.stream_chunk, _lib.ptr(self.d_xs),
+                          _lib.ptr(self.d_out), _lib.ptr(self.d_flags), _lib.ptr(h_out), *streams)
+            else:
+                _lib.call("pg_decode_host_stream_f32", inf.grid, inf.mlp_desc, _lib.ptr(h_xs), B,
+                          _lib.ptr(inf.feats16), _lib.ptr(inf.baked), _lib.ptr(inf.params),
+                          _flags(inf, self.exact), self.stream_chunk, _lib.ptr(self.d_xs), _lib.ptr(self.d_out),
+                          _lib.ptr(self.d_flags), _lib.ptr(h_out), *streams)
             n = -(-B // self.stream_chunk)
             self.fallbacks = int(self.d_flags[2 * n])   # pipelines that read inputs from host memory
             return h_out
-        _lib.call("pg_decode_host_f32", inf.grid, inf.mlp_desc, _lib.ptr(h_xs), h_xs.shape[0],
-                  _lib.ptr(inf.feats16), _lib.ptr(inf.baked), _lib.ptr(inf.params),
-                  _flags(inf, self.exact), self.chunk, _lib.ptr(self.d_xs), _lib.ptr(self.d_out),
-                  _lib.ptr(h_out), *streams)
+        if cells is not None:
+            _lib.call("pg_decode_host_cells_f32", inf.grid, inf.mlp_desc, _lib.ptr(h_xs), h_xs.shape[0],
+                      _lib.ptr(inf.feats16), _lib.ptr(inf.baked), _lib.ptr(inf.params),
+                      _flags(inf, self.exact), cells, self.chunk, _lib.ptr(self.d_xs), _lib.ptr(self.d_out),
+                      _lib.ptr(h_out), *streams)
+        else:
+            _lib.call("pg_decode_host_f32", inf.grid, inf.mlp_desc, _lib.ptr(h_xs), h_xs.shape[0],
+                      _lib.ptr(inf.feats16), _lib.ptr(inf.baked), _lib.ptr(inf.params),
+                      _flags(inf, self.exact), self.chunk, _lib.ptr(self.d_xs), _lib.ptr(self.d_out),
+                      _lib.ptr(h_out), *streams)
         return h_out

@@ -66,3 +66,46 @@ def test_c2_decode_default_plan_vs_oracle(log2_nf, n_p):
     # the drop-in numpy entry point (pinned streaming path for large batches)
     import paper_2312_17241_b200 as pg
     np.testing.assert_array_equal(pg.decode_pixels(inf, q), want)
+
+
+@pytest.mark.parametrize("kw", [dict(n_f=2 ** 16, n_c=2 ** 16, n_p=4, n_max=8192),
+                                dict(n_f=2 ** 14, n_c=2 ** 16, n_p=16, n_max=8192),
+                                dict(n_f=2 ** 18, n_c=2 ** 16, n_p=1, n_max=8192),
+                                dict(n_f=2 ** 12, n_c=2 ** 14, n_p=8),
+                                dict(d=3, n_f=2 ** 12, n_c=2 ** 12, n_p=4, out_dim=1),
+                                dict(d=3, n_f=2 ** 10, n_c=2 ** 10, n_p=2, out_dim=4, out_sigmoid=True)])
+@pytest.mark.parametrize("mib", [1, 32])
+def test_decode_cell_cache_bit_identical(kw, mib):
+    """The decode cell cache (pg_cells: per-cell records of the resolved
+    corner rows of the coarsest levels) changes where rows are read from,
+    not their values or the blend order: cached == uncached bit for bit,
+    device and streaming host paths, at a small and the default budget."""
+    import paper_2312_17241_b200 as pg
+    from paper_2312_17241_b200.decode import HostDecoder, decode_device
+    m = pg.init_model(pg.HyperParams(**kw), seed=2)
+    rng = np.random.default_rng(4)
+    with torch.no_grad():
+        m.feats.copy_(torch.from_numpy((rng.standard_normal(tuple(m.feats.shape)) * 0.1).astype(np.float32)))
+        if m.probed:
+            m.conf.copy_(torch.from_numpy(rng.standard_normal(tuple(m.conf.shape)).astype(np.float32)))
+            m.rebake_all()
+    inf = pg.to_inference(m)
+    inf.cell_budget = mib << 20
+    d = inf.hyper.d
+    q = _edge_points(1 << 16, d, np.float32, seed=9)
+    xs = torch.from_numpy(q).cuda()
+    plain = decode_device(inf, xs, exact=False, cells=False).cpu().numpy()
+    cached = decode_device(inf, xs, exact=False).cpu().numpy()
+    assert inf.cell_cache_bytes > 0
+    np.testing.assert_array_equal(cached, plain)
+    hx = torch.from_numpy(q).pin_memory()
+    ho = torch.full((q.shape[0], inf.out_dim), float("nan")).pin_memory()
+    HostDecoder(inf, stream=True, stream_chunk=1 << 14)(hx, ho)
+    np.testing.assert_array_equal(ho.numpy(), plain)
+    # the CUDA-core engines (reference order — decode_pixels' default — and FFMA)
+    for kw2 in (dict(exact=True), dict(exact=False, tensor=False)):
+        a = decode_device(inf, xs, cells=False, **kw2).cpu().numpy()
+        np.testing.assert_array_equal(decode_device(inf, xs, **kw2).cpu().numpy(), a)
+    ho2 = torch.full((q.shape[0], inf.out_dim), float("nan")).pin_memory()
+    HostDecoder(inf, exact=True, chunk=1 << 14)(hx, ho2)        # chunked host path, exact engine
+    np.testing.assert_array_equal(ho2.numpy(), decode_device(inf, xs, exact=True, cells=False).cpu().numpy())
