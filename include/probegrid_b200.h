@@ -344,6 +344,19 @@ int pg_train_fused_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
                        float *gfeat, float *gconf, uint8_t *touched,
                        float *gparams, double *loss_sum, float *dy_out,
                        void *stream);
+/* pg_train_fused_f32 with replicated feature-gradient tables: the fused
+ * kernel's CTA b adds its feature gradients into copy b % reps of gfeat_rep
+ * (reps x L x n_f x 2 floats, zero on entry, left zeroed), then one pass adds
+ * the copies into gfeat.  Divides the same-address reduction traffic of
+ * small tables by reps (reference default / C5 shapes); exact-MLP and
+ * reference-order modes ignore it.  reps in [1, 256]. */
+int pg_train_fused_rep_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
+                           const float *targets, int64_t B, const float *feats,
+                           const uint8_t *baked, const float *conf,
+                           const float *params, float scale, unsigned flags,
+                           float *gfeat, float *gconf, uint8_t *touched,
+                           float *gparams, double *loss_sum, float *dy_out,
+                           float *gfeat_rep, int reps, void *stream);
 
 /* Standalone batched MLP, mlp.py:55-85 (mlp_forward / mlp_backward with an
  * arbitrary upstream gradient; ReLU hidden layers, linear output; numpy /

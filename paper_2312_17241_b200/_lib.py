@@ -106,6 +106,8 @@ _SIGS.update({
     "pg_touched_from_f64": [_P, _I64, _P, _P],
     "pg_train_fused_f32": [_G, _M, _P, _P, _I64, _P, _P, _P, _P, _F, ctypes.c_uint, _P, _P, _P,
                            _P, _P, _P, _P],
+    "pg_train_fused_rep_f32": [_G, _M, _P, _P, _I64, _P, _P, _P, _P, _F, ctypes.c_uint, _P, _P, _P,
+                               _P, _P, _P, _P, _I, _P],
     "pg_train_fused_ref_f32": [_G, _M, _P, _P, _I64, _P, _P, _P, _P, _F, ctypes.c_uint, _P, _P,
                                _P, _P, _P, _P],
     "pg_mlp_wgrad_blas_f32": [_M, _P, _I64, _P, _P],

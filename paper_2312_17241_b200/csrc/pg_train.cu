@@ -485,29 +485,58 @@ int train_mma(const pg_grid *g, int od, const float *xs, const float *targets, i
               const uint8_t *baked, const float *conf, const float *params, float scale, int sig, ACC *gfeat,
               ACC *gconf, uint8_t *touched, ACC *gparams, LACC *loss_sum, float *dy_out, cudaStream_t s);
 
+// gfeat += sum of the `reps` replica tables (each n floats), replicas zeroed
+__global__ void reduce_replicas_kernel(float *__restrict__ rep, int reps, int64_t n, float *__restrict__ gfeat) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        float s = 0.0f;
+        for (int r = 0; r < reps; ++r) {
+            s += rep[r * n + i];
+            rep[r * n + i] = 0.0f;
+        }
+        if (s != 0.0f) gfeat[i] += s;
+    }
+}
+
 template <typename ACC, typename LACC>
 int train_fused(const pg_grid *g, const pg_mlp *m, const float *xs, const float *targets, int64_t B,
                 const float *feats, const uint8_t *baked, const float *conf, const float *params,
                 float scale, unsigned flags, ACC *gfeat, ACC *gconf, uint8_t *touched,
-                ACC *gparams, LACC *loss_sum, float *dy_out, float *acts, cudaStream_t s) {
+                ACC *gparams, LACC *loss_sum, float *dy_out, float *acts, cudaStream_t s,
+                float *gfeat_rep = nullptr, int reps = 1) {
     if (int e = validate_grid(g)) return e;
     PG_REQUIRE(train_fast_ok(g, m), "fused training needs F=2, 16 levels, N_p<=16, MLP [32,64,64,<=4]");
     if (B == 0) return PG_OK;
     const int od = m->widths[3];
     const int sig = (flags & PG_SIGMOID) ? 1 : 0;
-    const int touch_all = (flags & PG_TOUCH_ALL) ? 4 : 0;
+    int touch_all = (flags & PG_TOUCH_ALL) ? 4 : 0;
+    // replicated feature-gradient tables (fast fp32 path): the kernel adds
+    // into gfeat_rep copy (CTA % reps), one pass then folds them into gfeat
+    const bool rep = std::is_same<ACC, float>::value && gfeat_rep && reps > 1 && !acts && !(flags & PG_EXACT_MLP);
+    PG_REQUIRE(reps >= 1 && reps <= 256, "reps must be in [1, 256]");
+    ACC *gf = gfeat;
+    if (rep) {
+        touch_all |= (reps - 1) << 8;
+        gf = reinterpret_cast<ACC *>(gfeat_rep);
+    }
+    auto fold = [&](int rc) {
+        if (rc || !rep) return rc;
+        const int64_t n = (int64_t)g->n_levels * g->n_f * 2;
+        reduce_replicas_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(gfeat_rep, reps, n,
+                                                                        reinterpret_cast<float *>(gfeat));
+        return check_launch("reduce_replicas");
+    };
     if (flags & PG_COMPOSITE) {
         // one 64-sample tile = one ray of 64 samples (pg_train_mma.cu)
         PG_REQUIRE(od == 4 && !sig && !(flags & PG_EXACT_MLP) && !acts && B % 64 == 0,
                    "PG_COMPOSITE: out_dim 4, no sigmoid, tensor-core MLP, B a multiple of 64 samples");
-        return train_mma<ACC, LACC>(g, od, xs, targets, B, feats, baked, conf, params, scale, 2 | touch_all, gfeat, gconf,
-                                    touched, gparams, loss_sum, dy_out, s);
+        return fold(train_mma<ACC, LACC>(g, od, xs, targets, B, feats, baked, conf, params, scale, 2 | touch_all, gf, gconf,
+                                    touched, gparams, loss_sum, dy_out, s));
     }
     // fast path: tensor-core MLP (pg_train_mma.cu); this file's FFMA kernel is
     // the OpenBLAS-order path (PG_EXACT_MLP, reference-order mode)
     if (!acts && !(flags & PG_EXACT_MLP))
-        return train_mma<ACC, LACC>(g, od, xs, targets, B, feats, baked, conf, params, scale, sig | touch_all, gfeat, gconf,
-                                    touched, gparams, loss_sum, dy_out, s);
+        return fold(train_mma<ACC, LACC>(g, od, xs, targets, B, feats, baked, conf, params, scale, sig | touch_all, gf, gconf,
+                                    touched, gparams, loss_sum, dy_out, s));
     static DeviceOnce configured[8];
     const int sms = device_sms();
     // tile pipelines per CTA (1 or 2)
@@ -552,6 +581,17 @@ extern "C" int pg_train_fused_f32(const pg_grid *grid, const pg_mlp *mlp, const 
     return pg::train_fused<float, double>(grid, mlp, xs, targets, B, feats, baked, conf, params, scale,
                                           flags, gfeat, gconf, touched, gparams, loss_sum, dy_out,
                                           nullptr, pg::as_stream(stream));
+}
+
+extern "C" int pg_train_fused_rep_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
+                                      const float *targets, int64_t B, const float *feats,
+                                      const uint8_t *baked, const float *conf, const float *params,
+                                      float scale, unsigned flags, float *gfeat, float *gconf,
+                                      uint8_t *touched, float *gparams, double *loss_sum, float *dy_out,
+                                      float *gfeat_rep, int reps, void *stream) {
+    return pg::train_fused<float, double>(grid, mlp, xs, targets, B, feats, baked, conf, params, scale,
+                                          flags, gfeat, gconf, touched, gparams, loss_sum, dy_out,
+                                          nullptr, pg::as_stream(stream), gfeat_rep, reps);
 }
 
 extern "C" int pg_train_fused_ref_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,

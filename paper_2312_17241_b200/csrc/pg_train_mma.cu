@@ -244,12 +244,16 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
                      const uint8_t *__restrict__ baked, const float *__restrict__ conf,
                      const float *__restrict__ params, int od, float scale,
                      int mode_flags,   // bits 0-1: 1 logistic output, 2 volume compositing (one ray
-                                       // per tile); bit 2: flag every probed lookup as touched
+                                       // per tile); bit 2: flag every probed lookup as touched;
+                                       // bits 8-15: feature-gradient replicas - 1 (gfeat then
+                                       // holds that many copies; CTA b adds into copy b % reps)
                      ACC *__restrict__ gfeat, ACC *__restrict__ gconf, uint8_t *__restrict__ touched,
                      ACC *__restrict__ gparams, LACC *__restrict__ loss_sum, float *__restrict__ dy_out) {
     using namespace tm;
     const int sigmoid = mode_flags & 3;
     const bool touch_all = (mode_flags & 4) != 0;
+    const int reps = ((mode_flags >> 8) & 255) + 1;
+    ACC *const gfeat_cta = gfeat + (int64_t)(blockIdx.x % reps) * g.n_levels * g.n_f * 2;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SmemT<NG> &S = *reinterpret_cast<SmemT<NG> *>(smem_raw);
     const int gid = NG == 1 ? 0 : (int)(threadIdx.x >> 8);   // tile pipeline
@@ -514,11 +518,11 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
                 // every lane of the warp takes part (the shuffles); lanes past
                 // the batch end contribute nothing
                 encode_level_bwd2<D, NPM, ACC, lazy, true>(g, l, x, GDY[(2 * l) * kS + pl],
-                                                           GDY[(2 * l + 1) * kS + pl], feats, conf, gfeat, gconf,
+                                                           GDY[(2 * l + 1) * kS + pl], feats, conf, gfeat_cta, gconf,
                                                            touched, touch_all, pl < nv);
             } else if (pl < nv) {
                 encode_level_bwd2<D, NPM, ACC, lazy>(g, l, x, GDY[(2 * l) * kS + pl], GDY[(2 * l + 1) * kS + pl],
-                                                     feats, conf, gfeat, gconf, touched, touch_all);
+                                                     feats, conf, gfeat_cta, gconf, touched, touch_all);
             }
         }
 #pragma unroll

@@ -18,6 +18,7 @@ TrainingDiverged, as the reference does.
 from __future__ import annotations
 
 import json
+import os
 import math
 import time
 from dataclasses import dataclass, field
@@ -86,6 +87,23 @@ def adam_update(param: torch.Tensor, grad: torch.Tensor, slot: AdamSlot, t: int,
               float(eps), None, _lib.stream_ptr())
 
 
+def grad_replicas(hyper: HyperParams, dtype) -> int:
+    """Copies of the feature-gradient table the fused fp32 step spreads its
+    reductions over (pg_train_fused_rep_f32): small tables see every lookup
+    land on a few rows, and same-address reductions from all SMs serialise
+    in L2.  PG_TRAIN_REPS overrides."""
+    env = os.environ.get("PG_TRAIN_REPS")
+    if env:
+        return max(1, min(256, int(env)))
+    # probing ranges per level: <= 8 are warp-aggregated in the kernel
+    # (pg_train_mma.cu, AGG); 9..256 gain from 8 copies (measured, 2^18
+    # samples: n_f 2^8 N_p 16 3.66 -> 1.94 ms, n_f 2^10 N_p 16 1.87 -> 1.67,
+    # n_f 2^8 N_p 4 0.665 -> 0.619); C1 (1024 ranges) is faster without
+    # (0.555 vs 0.563 ms)
+    ranges = hyper.n_f // hyper.n_p
+    return 8 if 8 < ranges <= 256 and np.dtype(dtype) == np.float32 else 1
+
+
 class TrainState:
     """Optimizer state bound to one device model; drives individual steps."""
 
@@ -150,6 +168,7 @@ class TrainState:
         self.loss_host = torch.zeros(1, dtype=torch.float64, pin_memory=True)
         self.rank, self.world = 0, 1
         self.touch_all = False
+        self.grad_replicas = grad_replicas(model.hyper, model.dtype)
         self.scale = 2.0 / (B * h.out_dim)   # trainer.py:134, cast to the model dtype
 
     def shard(self, rank: int, world: int) -> "TrainState":
@@ -287,6 +306,16 @@ class TrainState:
                       _lib.ptr(m.gmlp), s)
             return
         if self.fused:
+            reps = 1 if self.exact_mlp else self.grad_replicas
+            if reps > 1:
+                if getattr(self, "_gfeat_rep", None) is None:
+                    self._gfeat_rep = torch.zeros(reps * m.n_feat, dtype=torch.float32, device=m.device)
+                _lib.call("pg_train_fused_rep_f32", m.grid, m.mlp_desc, _lib.ptr(xs), _lib.ptr(targets),
+                          xs.shape[0], _lib.ptr(m.feats), _lib.ptr(m.baked), _lib.ptr(m.conf),
+                          _lib.ptr(m.mlp_params), scale, flags, _lib.ptr(m.gfeats), _lib.ptr(m.gconf),
+                          _lib.ptr(m.touched), _lib.ptr(m.gmlp), _lib.ptr(self.loss_sum),
+                          _lib.ptr(dy_out), _lib.ptr(self._gfeat_rep), reps, s)
+                return
             _lib.call("pg_train_fused_f32", m.grid, m.mlp_desc, _lib.ptr(xs), _lib.ptr(targets),
                       xs.shape[0], _lib.ptr(m.feats), _lib.ptr(m.baked), _lib.ptr(m.conf),
                       _lib.ptr(m.mlp_params), scale, flags, _lib.ptr(m.gfeats), _lib.ptr(m.gconf),
