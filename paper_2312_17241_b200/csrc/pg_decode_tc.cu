@@ -70,6 +70,7 @@ struct TabPlan {
     int32_t bytes;
     const uint4 *cells;          // decode cell cache (pg_cells), or null
     int32_t cell[PG_MAX_LEVELS]; // level's record offset in uint4 units, -1: not cached
+    int32_t l2_hints;            // evict_last tables/cells, evict_first inputs/outputs
 };
 using Stream = DecodeStream;
 using pg::wait_flag;
@@ -107,7 +108,8 @@ __device__ __forceinline__ float2 encode_level_fwd2_tab(const pg_grid &g, int l,
                                                         const FT *__restrict__ feats,
                                                         const uint8_t *__restrict__ baked,
                                                         const unsigned char *tabs, int off, int pbits,
-                                                        const uint4 *__restrict__ cellrec = nullptr) {
+                                                        const uint4 *__restrict__ cellrec = nullptr,
+                                                        uint64_t pol = 0) {
     constexpr int C = 1 << D;
     const uint32_t nf_mask = (uint32_t)g.n_f - 1u, nc_mask = (uint32_t)g.n_c - 1u;
     const int res = g.res[l], kind = g.kind[l];
@@ -118,7 +120,7 @@ __device__ __forceinline__ float2 encode_level_fwd2_tab(const pg_grid &g, int l,
         c[a] = cell_coord(x[a], res, t[a]);
         omt[a] = __fsub_rn(1.0f, t[a]);
     }
-    if (RangeLoad<FT>::ok && cellrec != nullptr) return encode_level_fwd2_cell<D>(g, l, x, cellrec);
+    if (RangeLoad<FT>::ok && cellrec != nullptr) return encode_level_fwd2_cell<D>(g, l, x, cellrec, pol);
     int idx[C];
     float w[C];
 #pragma unroll
@@ -204,6 +206,8 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
     Smem<NG> &S = *reinterpret_cast<Smem<NG> *>(smem_raw);
     unsigned char *tabs = smem_raw + tab_offset<NG>();
     const int tid = threadIdx.x, lane = tid & 31;
+    const uint64_t pol_last = plan.l2_hints ? l2_policy_evict_last() : 0;
+    const uint64_t pol_first = plan.l2_hints && MODE == 0 ? l2_policy_evict_first() : 0;
 
     // ---- weights: B operands (K-major W^T) + epilogue constants ----
     {
@@ -344,7 +348,9 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
             // from pinned host memory for a group whose flag never came
             const float *src = STREAM && G.host ? st.host_xs : xs;
             for (int i = gt; i < kTP * D; i += kGT)
-                G.xs[i] = i < nv * D ? (STREAM ? __ldcg(src + p0 * D + i) : xs[p0 * D + i]) : 0.5f;
+                G.xs[i] = i < nv * D ? (STREAM ? __ldcg(src + p0 * D + i)
+                                               : pol_first ? ld_nc_hint(xs + p0 * D + i, pol_first) : xs[p0 * D + i])
+                                     : 0.5f;
         }
         group_sync(grp);
         // ---------------- encode -> layer-1 A operand (hi | lo) ----------------
@@ -359,10 +365,10 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
                 const int ca = plan.cell[2 * P], cb = plan.cell[2 * P + 1];
                 const float2 ya = encode_level_fwd2_tab<FT, D>(g, 2 * P, x, feats, baked, tabs,
                                                                plan.off[2 * P], plan.pbits,
-                                                               ca >= 0 ? plan.cells + ca : nullptr);
+                                                               ca >= 0 ? plan.cells + ca : nullptr, pol_last);
                 const float2 yb = encode_level_fwd2_tab<FT, D>(g, 2 * P + 1, x, feats, baked, tabs,
                                                                plan.off[2 * P + 1], plan.pbits,
-                                                               cb >= 0 ? plan.cells + cb : nullptr);
+                                                               cb >= 0 ? plan.cells + cb : nullptr, pol_last);
                 float h[4], lo[4];
                 umma::split_tf32(ya.x, h[0], lo[0]);
                 umma::split_tf32(ya.y, h[1], lo[1]);
@@ -465,7 +471,8 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
                 const int q = i / od, j = i - q * od;
                 float o = S.bias2[j] + G.opA[q * kOutMax + j] + G.opA[(kTP + q) * kOutMax + j];
                 if (sigmoid) o = (float)(1.0 / (1.0 + exp(-(double)o)));
-                dst[i] = o;
+                if (pol_first) st_hint(dst + i, o, pol_first);
+                else dst[i] = o;
             }
         }
         if (STREAM && gt == 0) ++G.pending;
@@ -486,6 +493,8 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
 static tc::TabPlan plan_tables(const pg_grid *g, size_t feat_bytes, int budget, int kinds, const pg_cells *cells) {
     tc::TabPlan p;
     p.cells = nullptr;
+    static const bool hints = !(getenv("PG_DECODE_L2_HINTS") && atoi(getenv("PG_DECODE_L2_HINTS")) == 0);
+    p.l2_hints = hints ? 1 : 0;
     for (int l = 0; l < PG_MAX_LEVELS; ++l) {
         p.off[l] = -1;
         p.cell[l] = -1;

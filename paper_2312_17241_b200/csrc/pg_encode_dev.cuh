@@ -26,9 +26,38 @@ struct CellMap {
 // Forward of a cached level: ONE 16 B (2-D) / 32 B (3-D) record load instead
 // of 2^d index + row gathers; same weights, values and blend order as
 // encode_level_fwd2, so bit-identical.
+// L2 eviction-priority policies (createpolicy): the decode keeps its tables
+// and cell records L2-resident (evict_last) while its 20 B/query of inputs
+// and outputs stream through (evict_first)
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint4 ld_nc_v4_hint(const uint4 *p, uint64_t pol) {
+    uint4 v;
+    asm("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+        : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ld_nc_hint(const float *p, uint64_t pol) {
+    float v;
+    asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_hint(float *p, float v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+
 template <int D>
 __device__ __forceinline__ float2 encode_level_fwd2_cell(const pg_grid &g, int l, const float (&x)[D],
-                                                         const uint4 *__restrict__ rec) {
+                                                         const uint4 *__restrict__ rec, uint64_t pol = 0) {
     constexpr int C = 1 << D;
     const int res = g.res[l];
     int c[D];
@@ -43,7 +72,7 @@ __device__ __forceinline__ float2 encode_level_fwd2_cell(const pg_grid &g, int l
     for (int a = D - 2; a >= 0; --a) cell = cell * res + c[a];
     uint32_t r[C];
     if constexpr (D == 2) {
-        const uint4 v = __ldg(rec + cell);
+        const uint4 v = pol ? ld_nc_v4_hint(rec + cell, pol) : __ldg(rec + cell);
         r[0] = v.x; r[1 % C] = v.y; r[2 % C] = v.z; r[3 % C] = v.w;
     } else {
         float v8[8];

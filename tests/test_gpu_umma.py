@@ -64,3 +64,28 @@ def test_umma_kmajor_m64_layout():
     ref = A.astype(np.float64) @ B.astype(np.float64).T
     lanes = [(i // 16) * 32 + i % 16 for i in range(64)]
     np.testing.assert_allclose(D[lanes], ref, rtol=1e-5, atol=1e-4)
+
+
+def test_umma_mn_major_operands():
+    """MN-major shared-memory operands (the layout a weight-gradient GEMM
+    with K = samples would read an activation tile in).  kind::f16 with an
+    MN-major A (canonical no-swizzle layout: core matrix 8 K-rows x 16 B,
+    LBO = K-group stride, SBO = MN-group stride, instruction-descriptor
+    major bit) computes the product: the descriptor convention is right.
+    kind::tf32 with the A or B major bit set writes zeros on this sm_100a
+    for every layout tried (no-swizzle with both stride conventions, the
+    128-byte-swizzled canonical atom): tf32 operands must be K-major, which
+    is why the training kernel's weight-gradient GEMMs stay on mma.sync
+    (DESIGN.md 4).  The test pins both behaviours."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    rng = np.random.default_rng(0)
+    A = rng.standard_normal((128, 32)).astype(np.float16).astype(np.float32)
+    B = rng.standard_normal((64, 32)).astype(np.float16).astype(np.float32)
+    ref = A.astype(np.float64) @ B.astype(np.float64).T
+    np.testing.assert_allclose(_run(A, B, 10 << 4), ref, rtol=1e-5, atol=1e-4)      # f16, A MN-major
+    for code in (6 << 4, (6 << 4) | (1 << 1), (6 << 4) | (3 << 1), 8 << 4, (8 << 4) | (1 << 1)):
+        D = _run(A, B, code)                                                        # tf32, MN-major
+        ok = np.allclose(D, ref, rtol=1e-5, atol=1e-4)
+        assert ok or not D.any(), f"code {code}: neither the product nor all-zero"
+        print(f"tf32 MN-major variant code {code}: {'correct' if ok else 'all zeros'}")
