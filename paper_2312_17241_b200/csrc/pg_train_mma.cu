@@ -106,16 +106,22 @@ __device__ __forceinline__ void warp_gemm(float (&acc)[NT][4], const float *pa, 
         split(pa[(m0 + g + 8) * am + (k0 + c) * ak], ah[1], al[1]);
         split(pa[(m0 + g) * am + (k0 + c + 4) * ak], ah[2], al[2]);
         split(pa[(m0 + g + 8) * am + (k0 + c + 4) * ak], ah[3], al[3]);
+        // term-major issue: NT independent HMMAs between dependent ones
+        // (0.5545 -> 0.5521 ms per C1 step vs the three terms of one tile
+        // back to back)
+        uint32_t bh[NT][2], bl[NT][2];
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
             const int n = n0 + 8 * t + g;
-            uint32_t bh0, bl0, bh1, bl1;
-            split(pb[(k0 + c) * bk + n * bn], bh0, bl0);
-            split(pb[(k0 + c + 4) * bk + n * bn], bh1, bl1);
-            hmma(acc[t], al, bh0, bh1);  // small terms first
-            hmma(acc[t], ah, bl0, bl1);
-            hmma(acc[t], ah, bh0, bh1);
+            split(pb[(k0 + c) * bk + n * bn], bh[t][0], bl[t][0]);
+            split(pb[(k0 + c + 4) * bk + n * bn], bh[t][1], bl[t][1]);
         }
+#pragma unroll
+        for (int t = 0; t < NT; ++t) hmma(acc[t], al, bh[t][0], bh[t][1]);  // small terms first
+#pragma unroll
+        for (int t = 0; t < NT; ++t) hmma(acc[t], ah, bl[t][0], bl[t][1]);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) hmma(acc[t], ah, bh[t][0], bh[t][1]);
     }
 }
 
