@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(kNT *NG, 2 / NG)
 #pragma unroll 2
         for (int it = 0; it < 4; ++it) {
             const int l = lsub + 4 * it;
-            const float2 yv = encode_level_fwd2<FT, D>(g, l, x, feats_fwd, baked);
+            const float2 yv = encode_level_fwd2_rng<FT, D>(g, l, x, feats_fwd, baked);
             G.yT[sw(2 * l, pl)] = yv.x;
             G.yT[sw(2 * l + 1, pl)] = yv.y;
         }
