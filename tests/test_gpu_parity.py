@@ -1030,6 +1030,17 @@ def test_empty_inputs():
     assert o.shape == (0, 2) and base.shape == (0, 4)
     rows_u, inv = cuda.dedup_rows(np.zeros((0, 4), np.int32), 32)
     assert rows_u.shape == (0,) and inv.shape == (0, 4)
+    # round-2 entry points: standalone MLP, cached decode, host decoders, PNG of an empty rect
+    from paper_2312_17241_b200.decode import HostDecoder
+    from paper_2312_17241_b200.mlp import mlp_backward, mlp_forward
+    out, cache = mlp_forward(m.mlp, torch.zeros((0, 32), device="cuda"))
+    assert out.shape == (0, 3)
+    assert mlp_backward(m.mlp, cache, torch.zeros((0, 3), device="cuda")).shape == (0, 32)
+    assert decode_device(inf, torch.zeros((0, 2), device="cuda"), exact=True).shape == (0, 3)
+    hx = torch.zeros((0, 2)).pin_memory()
+    ho = torch.zeros((0, 3)).pin_memory()
+    HostDecoder(inf)(hx, ho)
+    HostDecoder(inf, exact=True)(hx, ho)
 
 
 @pytest.mark.parametrize("n_p", [32, 256])
