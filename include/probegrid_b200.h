@@ -432,14 +432,18 @@ int pg_raster_coords_f32(int x0, int y0, int w, int h, int width, int height,
  * sample, every layer's input and output delta to acts, laid out as
  * [a_0 | a_1 | .. | a_{n-1} | delta_0 | .. | delta_{n-1}], each block B rows
  * of its width (a_0 = y, a_l = relu activations, delta_l = dL/d(pre-activation
- * of layer l)); pg_mlp_acts_floats(B, mlp) floats (which include the
- * scratch pg_mlp_wgrad_blas_f32 uses after them).  pg_mlp_wgrad_blas_f32
+ * of layer l)), followed by the deltas again column-major (one contiguous
+ * B-float column per output, for the in-order bias chains);
+ * pg_mlp_acts_floats(B, mlp) floats (which include the scratch
+ * pg_mlp_wgrad_blas_f32 uses after them).  pg_mlp_wgrad_blas_f32
  * then forms gparams += every weight and bias gradient in numpy/OpenBLAS
  * order (mlp.py:80-84): the sgemm K loop over samples is blocked by 448 (the
  * last two blocks balanced), each block one sequential FMA chain from 0,
  * blocks added in order; bias sums sequential over samples.  With the forward
  * already in OpenBLAS order this makes the MLP gradients bit-identical to the
- * reference's for out_dim >= 2 (out_dim 1 goes through sgemv there). */
+ * reference's for out_dim >= 2 (out_dim 1 goes through sgemv there) and even
+ * B >= 8192 (odd K and small products take other OpenBLAS paths:
+ * rounding-level agreement only). */
 int64_t pg_mlp_acts_floats(int64_t B, const pg_mlp *mlp);
 int pg_train_fused_ref_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
                            const float *targets, int64_t B, const float *feats,

@@ -756,62 +756,7 @@ __device__ inline void blas_block(int64_t B, int64_t blk, int64_t &start, int64_
     }
 }
 
-// pass 1: every (block, element) chain in parallel -- each block's FMA chain
-// starts from 0 in OpenBLAS, so the chains are independent
-__global__ void wgrad_blas_partial_kernel(const float *__restrict__ a, int fin, const float *__restrict__ d,
-                                          int fout, int64_t B, int64_t nblk, float *__restrict__ part) {
-    const int64_t E = (int64_t)fin * fout;
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= nblk * E) return;
-    const int64_t blk = t / E;
-    const int e = (int)(t - blk * E);
-    const int i = e / fout, j = e - i * fout;
-    int64_t ls, ml;
-    blas_block(B, blk, ls, ml);
-    float acc = 0.0f;
-#pragma unroll 8
-    for (int64_t k = ls; k < ls + ml; ++k) acc = __fmaf_rn(__ldg(a + k * fin + i), __ldg(d + k * fout + j), acc);
-    part[t] = acc;
-}
-
-// pass 1, register-tiled (fin, fout multiples of 4, 16-byte aligned rows):
-// each thread runs the 4x4 chains (i0..i0+3) x (j0..j0+3) of one block --
-// every chain still starts from 0 and adds k in ascending order, so the
-// partials are bit-identical to the one-chain kernel above with 8x fewer
-// loads per FMA (two float4 per 16 FMAs instead of two floats per FMA)
-__global__ void wgrad_blas_partial4_kernel(const float *__restrict__ a, int fin, const float *__restrict__ d,
-                                           int fout, int64_t B, int64_t nblk, float *__restrict__ part) {
-    const int tj = fout >> 2;
-    const int64_t T = (int64_t)(fin >> 2) * tj, E = (int64_t)fin * fout;
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= nblk * T) return;
-    const int64_t blk = t / T;
-    const int e = (int)(t - blk * T);
-    const int i0 = (e / tj) * 4, j0 = (e - (e / tj) * tj) * 4;
-    int64_t ls, ml;
-    blas_block(B, blk, ls, ml);
-    float acc[4][4] = {};
-#pragma unroll 4
-    for (int64_t k = ls; k < ls + ml; ++k) {
-        const float4 av = __ldg(reinterpret_cast<const float4 *>(a + k * fin + i0));
-        const float4 dv = __ldg(reinterpret_cast<const float4 *>(d + k * fout + j0));
-        const float au[4] = {av.x, av.y, av.z, av.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            acc[u][0] = __fmaf_rn(au[u], dv.x, acc[u][0]);
-            acc[u][1] = __fmaf_rn(au[u], dv.y, acc[u][1]);
-            acc[u][2] = __fmaf_rn(au[u], dv.z, acc[u][2]);
-            acc[u][3] = __fmaf_rn(au[u], dv.w, acc[u][3]);
-        }
-    }
-    float *p = part + blk * E + (int64_t)i0 * fout + j0;
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-        *reinterpret_cast<float4 *>(p + (int64_t)u * fout) = make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
-}
-
 // pass 2: C = 0; C += block partial, blocks in order; then gW += C.
-// Bias: delta.sum(axis=0) adds the rows in order (sequential over samples).
 __global__ void wgrad_blas_reduce_kernel(const float *__restrict__ part, int64_t nblk, int fin, int fout,
                                          const float *__restrict__ d, int64_t B, float *__restrict__ gW,
                                          float *__restrict__ gb) {
@@ -824,65 +769,142 @@ __global__ void wgrad_blas_reduce_kernel(const float *__restrict__ part, int64_t
     }
 }
 
-// Bias: delta.sum(axis=0) adds the rows in order -- one dependent add chain
-// per output over all B samples (~4 cycles per row: 0.53 ms for 2^18 rows,
-// the floor).  The chains are independent, so the columns are split across
-// CTAs (kBC per CTA, grid = column groups x layers) and each CTA streams only
-// its columns' 16-byte row slices through an NS-stage cp.async ring of
-// shared memory; thread j < kBC runs column c0 + j's chain in row order while
-// the next NS-1 chunks are in flight (the previous one-CTA-per-layer kernel
-// waited for every 128-row chunk: 6.0 ms per C1 reference_order step; column
-// groups of 8 / 4 / 2 measured 4.2 / 3.6 / 3.3 ms per step).
-constexpr int kBC = 2, kBR = 1024, kBNS = 5, kBT = 256;   // 40 KB ring
-__device__ __forceinline__ void cp_async4(float *dst, const float *src) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
-}
-__global__ void __launch_bounds__(kBT) bias_blas_kernel(const float *__restrict__ d0, const float *__restrict__ d1,
-                                                        const float *__restrict__ d2, int f0, int f1, int f2,
-                                                        int64_t B, float *__restrict__ g0, float *__restrict__ g1,
-                                                        float *__restrict__ g2) {
-    __shared__ float ring[kBNS][kBR * kBC];
-    const int layer = blockIdx.y;
-    const float *d = layer == 0 ? d0 : layer == 1 ? d1 : d2;
-    const int fout = layer == 0 ? f0 : layer == 1 ? f1 : f2;
-    float *gb = layer == 0 ? g0 : layer == 1 ? g1 : g2;
-    const int c0 = blockIdx.x * kBC;
-    if (!d || c0 >= fout) return;
-    const int nc = fout - c0 < kBC ? fout - c0 : kBC;
-    const int t = threadIdx.x;
-    const int64_t nchunk = (B + kBR - 1) / kBR;
-    auto issue = [&](int64_t c) {   // thread t copies rows c*kBR + t + i*kBT, nc columns each
-        if (c < nchunk) {
+// Bias chains, warp edition: ONE warp per output column runs the column's
+// in-order add chain over all B rows.  The 32 lanes load 32 consecutive rows
+// of the column per instruction, 8 such loads in flight per lane (256 rows
+// ahead of the chain, > the L2 latency at ~4 cycles per add); each round's
+// 256 rows go through a 1 KB shared-memory stage and the chain reads them
+// in row order with broadcast 16-byte loads (a shuffle per row measured
+// ~14 cycles per add: the shuffles' latency sat on the chain); every lane
+// carries the same chain (no divergence), lane 0 stores it.  Same additions in the same order
+// as numpy's delta.sum(axis=0) (rows in order): bit-identical.  Round 1 ran
+// the chains from a cp.async ring in shared memory, 2 columns per CTA (~2 ms
+// of a 3.3 ms reference-order C1 step).
+constexpr int kChainDepth = 8;   // float4 loads in flight per lane (1024 rows ahead)
+constexpr int kWT = 128;         // threads per CTA of wgrad_bias_kernel
+__device__ __forceinline__ void bias_chain_warp(const float *__restrict__ dT, int64_t B,
+                                                float *__restrict__ gbj, float *__restrict__ stage) {
+    // dT: this column's B values, contiguous (column-major copy written by
+    // the training kernel); 16-byte aligned when B % 4 == 0
+    const int lane = threadIdx.x & 31;
+    constexpr int kRows = kChainDepth * 128;   // rows staged per round
+    float acc = 0.0f;
+    if ((B & 3) == 0 && ((uintptr_t)dT & 15) == 0) {
+        const float4 *d4 = reinterpret_cast<const float4 *>(dT);
+        const int64_t n4 = B >> 2;
+        float4 cur[kChainDepth];
 #pragma unroll
-            for (int i = 0; i < kBR / kBT; ++i) {
-                const int64_t row = c * kBR + t + i * kBT;
-                if (row < B) {
-                    float *dst = ring[c % kBNS] + (t + i * kBT) * kBC;
-                    const float *src = d + row * fout + c0;
-                    for (int q = 0; q < nc; ++q) cp_async4(dst + q, src + q);
+        for (int k = 0; k < kChainDepth; ++k) {
+            const int64_t r4 = (int64_t)k * 32 + lane;
+            cur[k] = r4 < n4 ? __ldg(d4 + r4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        float4 *s4 = reinterpret_cast<float4 *>(stage);
+        for (int64_t b0 = 0; b0 < B; b0 += kRows) {
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < kChainDepth; ++k) s4[k * 32 + lane] = cur[k];
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < kChainDepth; ++k) {
+                const int64_t r4 = (b0 + kRows) / 4 + (int64_t)k * 32 + lane;
+                cur[k] = r4 < n4 ? __ldg(d4 + r4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            const int nr = (int)(B - b0 < kRows ? B - b0 : kRows);
+            if (nr == kRows) {
+#pragma unroll 16
+                for (int q = 0; q < kRows / 4; ++q) {
+                    const float4 v = s4[q];
+                    acc = __fadd_rn(acc, v.x);
+                    acc = __fadd_rn(acc, v.y);
+                    acc = __fadd_rn(acc, v.z);
+                    acc = __fadd_rn(acc, v.w);
                 }
+            } else {
+                for (int r = 0; r < nr; ++r) acc = __fadd_rn(acc, stage[r]);
             }
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-#pragma unroll 1
-    for (int c = 0; c < kBNS - 1; ++c) issue(c);
-    float acc = 0.0f;
-#pragma unroll 1
-    for (int64_t c = 0; c < nchunk; ++c) {
-        issue(c + kBNS - 1);
-        asm volatile("cp.async.wait_group %0;" ::"n"(kBNS - 1) : "memory");
-        __syncthreads();   // chunk c landed (every thread's part)
-        if (t < nc) {
-            const float *buf = ring[c % kBNS] + t;
-            const int nr = (int)(B - c * kBR < kBR ? B - c * kBR : kBR);
-#pragma unroll 8
-            for (int r = 0; r < nr; ++r) acc = __fadd_rn(acc, buf[r * kBC]);
+    } else {   // ragged batch: scalar loads, same order
+        for (int64_t b0 = 0; b0 < B; b0 += 32) {
+            const float v = b0 + lane < B ? __ldg(dT + b0 + lane) : 0.0f;
+            const int n = (int)(B - b0 < 32 ? B - b0 : 32);
+            for (int i = 0; i < n; ++i) acc = __fadd_rn(acc, __shfl_sync(0xffffffffu, v, i));
         }
-        __syncthreads();   // slot c % kBNS free before the next issue rewrites it
     }
-    if (t < nc) gb[c0 + t] = __fadd_rn(gb[c0 + t], acc);
+    if (lane == 0) *gbj = __fadd_rn(*gbj, acc);
+}
+
+// Pass 1 of the reference-order weight gradients and the bias chains in ONE
+// launch (no side stream, no allocation): CTAs [0, nbias) run one bias chain
+// per warp (all columns of all layers), the rest run the per-layer K-block
+// partials (every (block, element) FMA chain of OpenBLAS's K-blocking starts
+// from 0, so they are independent; tiled 4 x 4 per thread where the widths
+// allow), so the serial chains (~0.5 ms) overlap the parallel partial sums.
+struct WgradJob {
+    const float *a[3], *d[3], *dT[3];
+    float *gb[3], *part[3];
+    int fin[3], fout[3], tiled[3];
+    int64_t first_cta[4];   // CTA ranges of the partial-sum work per layer
+    int n_layers, n_cols, nbias_ctas;
+};
+__global__ void __launch_bounds__(kWT) wgrad_bias_kernel(const WgradJob job, int64_t B, int64_t nblk) {
+    __shared__ __align__(16) float stage[kWT / 32][kChainDepth * 128];
+    if ((int64_t)blockIdx.x < job.nbias_ctas) {
+        const int w = blockIdx.x * (kWT / 32) + (threadIdx.x >> 5);
+        if (w >= job.n_cols) return;
+        int l = 0, j = w;
+        while (l < job.n_layers - 1 && j >= job.fout[l]) {
+            j -= job.fout[l];
+            ++l;
+        }
+        bias_chain_warp(job.dT[l] + (int64_t)j * B, B, job.gb[l] + j, stage[threadIdx.x >> 5]);
+        return;
+    }
+    int l = 0;
+    while (l < job.n_layers - 1 && (int64_t)blockIdx.x >= job.first_cta[l + 1]) ++l;
+    const int64_t t = ((int64_t)blockIdx.x - job.first_cta[l]) * kWT + threadIdx.x;
+    const int fin = job.fin[l], fout = job.fout[l];
+    const float *a = job.a[l], *d = job.d[l];
+    const int64_t E = (int64_t)fin * fout;
+    if (job.tiled[l]) {   // 4 x 4 chains per thread, two float4 loads per 16 FMAs
+        const int tj = fout >> 2;
+        const int64_t T = (int64_t)(fin >> 2) * tj;
+        if (t >= nblk * T) return;
+        const int64_t blk = t / T;
+        const int e = (int)(t - blk * T);
+        const int i0 = (e / tj) * 4, j0 = (e - (e / tj) * tj) * 4;
+        int64_t ls, ml;
+        blas_block(B, blk, ls, ml);
+        float acc[4][4] = {};
+#pragma unroll 4
+        for (int64_t k = ls; k < ls + ml; ++k) {
+            const float4 av = __ldg(reinterpret_cast<const float4 *>(a + k * fin + i0));
+            const float4 dv = __ldg(reinterpret_cast<const float4 *>(d + k * fout + j0));
+            const float au[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                acc[u][0] = __fmaf_rn(au[u], dv.x, acc[u][0]);
+                acc[u][1] = __fmaf_rn(au[u], dv.y, acc[u][1]);
+                acc[u][2] = __fmaf_rn(au[u], dv.z, acc[u][2]);
+                acc[u][3] = __fmaf_rn(au[u], dv.w, acc[u][3]);
+            }
+        }
+        float *p = job.part[l] + blk * E + (int64_t)i0 * fout + j0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            *reinterpret_cast<float4 *>(p + (int64_t)u * fout) =
+                make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
+    } else {              // one chain per thread
+        if (t >= nblk * E) return;
+        const int64_t blk = t / E;
+        const int e = (int)(t - blk * E);
+        const int i = e / fout, j = e - i * fout;
+        int64_t ls, ml;
+        blas_block(B, blk, ls, ml);
+        float acc = 0.0f;
+#pragma unroll 8
+        for (int64_t k = ls; k < ls + ml; ++k) acc = __fmaf_rn(__ldg(a + k * fin + i), __ldg(d + k * fout + j), acc);
+        job.part[l][t] = acc;
+    }
 }
 
 int64_t mlp_acts_floats(int64_t B, const pg_mlp *m) {
@@ -892,52 +914,70 @@ int64_t mlp_acts_floats(int64_t B, const pg_mlp *m) {
         const int64_t el = (int64_t)m->widths[l] * m->widths[l + 1];
         e = el > e ? el : e;
     }
-    return B * w + blas_nblocks(B) * e;   // + the per-block partial sums of pass 1
+    int64_t cols = 0;
+    for (int l = 0; l < m->n_layers; ++l) cols += m->widths[l + 1];
+    // + the deltas again, column-major (bias chains) + the per-block partial
+    // sums of pass 1, one region per layer
+    return B * w + B * cols + (int64_t)m->n_layers * blas_nblocks(B) * e;
 }
 
 int mlp_wgrad_blas(const pg_mlp *m, const float *acts, int64_t B, float *gparams, cudaStream_t s) {
     if (int e = validate_mlp(m)) return e;
     if (B == 0) return PG_OK;
-    // acts = [a_0 | .. | a_{n-1} | delta_0 | .. | delta_{n-1}]
-    int64_t a_off = 0, d_off = 0;
-    for (int l = 0; l < m->n_layers; ++l) d_off += B * m->widths[l];
-    int64_t w = 0;
-    for (int l = 0; l < m->n_layers; ++l) w += m->widths[l] + m->widths[l + 1];
-    float *part = const_cast<float *>(acts) + B * w;   // scratch after the activations
-    const int64_t nblk = blas_nblocks(B);
     PG_REQUIRE(m->n_layers <= 3, "reference-order weight gradients: at most 3 layers");
-    const float *dl[3] = {nullptr, nullptr, nullptr};
-    float *gbl[3] = {nullptr, nullptr, nullptr};
-    int fo[3] = {0, 0, 0};
+    // acts = [a_0 .. a_{n-1} | delta_0 .. delta_{n-1} | delta_l^T (column-major) | partials per layer]
+    int64_t a_off = 0, d_off = 0, w = 0, emax = 0;
+    for (int l = 0; l < m->n_layers; ++l) {
+        d_off += B * m->widths[l];
+        w += m->widths[l] + m->widths[l + 1];
+        const int64_t el = (int64_t)m->widths[l] * m->widths[l + 1];
+        emax = el > emax ? el : emax;
+    }
+    const int64_t nblk = blas_nblocks(B);
+    int64_t cols = 0;
+    for (int l = 0; l < m->n_layers; ++l) cols += m->widths[l + 1];
+    const float *dT0 = acts + B * w;                              // [delta_l^T ...] column-major
+    float *part0 = const_cast<float *>(acts) + B * w + B * cols;
+    WgradJob job{};
+    job.n_layers = m->n_layers;
+    job.n_cols = 0;
+    int64_t cta = 0;
     float *g = gparams;
+    float *gW[3] = {nullptr, nullptr, nullptr};
+    for (int l = 0; l < m->n_layers; ++l) job.n_cols += m->widths[l + 1];
+    job.nbias_ctas = (job.n_cols + kWT / 32 - 1) / (kWT / 32);
+    cta = job.nbias_ctas;
     for (int l = 0; l < m->n_layers; ++l) {
         const int fin = m->widths[l], fout = m->widths[l + 1];
-        PG_REQUIRE(fout <= 64, "reference-order bias sums: width <= 64");
-        const int64_t E = (int64_t)fin * fout, n1 = nblk * E;
+        const int64_t E = (int64_t)fin * fout;
         const float *av = acts + a_off, *dv = acts + d_off;
+        float *part = part0 + (int64_t)l * nblk * emax;
         const bool tiled = fin % 4 == 0 && fout % 4 == 0 && ((uintptr_t)av & 15) == 0 &&
                            ((uintptr_t)dv & 15) == 0 && ((uintptr_t)part & 15) == 0;
-        if (tiled) {
-            const int64_t n4 = n1 / 16;
-            wgrad_blas_partial4_kernel<<<(unsigned)((n4 + 127) / 128), 128, 0, s>>>(av, fin, dv, fout, B, nblk,
-                                                                                    part);
-        } else {
-            wgrad_blas_partial_kernel<<<(unsigned)((n1 + 255) / 256), 256, 0, s>>>(av, fin, dv, fout, B, nblk,
-                                                                                   part);
-        }
-        wgrad_blas_reduce_kernel<<<(unsigned)((E + 127) / 128), 128, 0, s>>>(part, nblk, fin, fout, acts + d_off,
-                                                                             B, g, g + E);
-        dl[l] = acts + d_off;
-        gbl[l] = g + E;
-        fo[l] = fout;
+        job.a[l] = av;
+        job.d[l] = dv;
+        job.dT[l] = dT0;
+        dT0 += B * fout;
+        job.part[l] = part;
+        job.fin[l] = fin;
+        job.fout[l] = fout;
+        job.tiled[l] = tiled ? 1 : 0;
+        job.first_cta[l] = cta;
+        const int64_t work = tiled ? nblk * E / 16 : nblk * E;
+        cta += (work + kWT - 1) / kWT;
+        gW[l] = g;
+        job.gb[l] = g + E;
         a_off += B * fin;
         d_off += B * fout;
         g += E + fout;
     }
-    {
-        const int fmax = fo[0] > fo[1] ? (fo[0] > fo[2] ? fo[0] : fo[2]) : (fo[1] > fo[2] ? fo[1] : fo[2]);
-        const dim3 grid((unsigned)((fmax + kBC - 1) / kBC), (unsigned)m->n_layers);
-        bias_blas_kernel<<<grid, kBT, 0, s>>>(dl[0], dl[1], dl[2], fo[0], fo[1], fo[2], B, gbl[0], gbl[1], gbl[2]);
+    job.first_cta[m->n_layers] = cta;
+    wgrad_bias_kernel<<<(unsigned)cta, kWT, 0, s>>>(job, B, nblk);
+    for (int l = 0; l < m->n_layers; ++l) {
+        const int64_t E = (int64_t)job.fin[l] * job.fout[l];
+        wgrad_blas_reduce_kernel<<<(unsigned)((E + 127) / 128), 128, 0, s>>>(job.part[l], nblk, job.fin[l],
+                                                                             job.fout[l], job.d[l], B, gW[l],
+                                                                             job.gb[l]);
     }
     return check_launch("mlp_wgrad_blas");
 }

@@ -63,6 +63,14 @@ __device__ __forceinline__ void dump_tile(const float *srcT, int width, int nv, 
         dst[(int64_t)q * width + c] = srcT[sw(c, q)];
     }
 }
+// ... and column-major ([feature][sample], stride B) for the in-order bias
+// chains, which then read each column as one contiguous stream
+__device__ __forceinline__ void dump_tile_T(const float *srcT, int width, int nv, float *dstT, int64_t B, int tid) {
+    for (int i = tid; i < nv * width; i += kNT) {
+        const int c = i / nv, q = i - c * nv;
+        dstT[(int64_t)c * B + q] = srcT[sw(c, q)];
+    }
+}
 __device__ __forceinline__ float relu_np(float z) { return z < 0.0f ? 0.0f : z; }  // np.maximum(z, 0)
 __device__ __forceinline__ float mask_np(float z) { return z > 0.0f ? 1.0f : 0.0f; }  // (pre > 0)
 
@@ -246,9 +254,16 @@ __global__ void __launch_bounds__(kNT *NG, 2 / NG)
         }
         gsync();
         PG_PH(4);
-        if (acts)
+        if (acts) {
             for (int i = tid; i < nv * od; i += kNT)
                 acts[B * (kI + 4 * kH) + p0 * od + i] = G.d3[(i / od) * kO + i % od];
+            // column-major copy for the bias chains: [d0^T | d1^T | d2^T] after the activations
+            float *d2T = acts + B * (kI + 4 * kH + od) + 2 * B * kH + p0;
+            for (int i = tid; i < nv * od; i += kNT) {
+                const int j = i / nv, q = i - j * nv;
+                d2T[(int64_t)j * B + q] = G.d3[q * kO + j];
+            }
+        }
         // ---- dW2 += h2^T d3, db2 += sum d3 (4 samples per shared load) ----
         {
             const int k = tid & 63, j = tid >> 6;
@@ -298,7 +313,10 @@ __global__ void __launch_bounds__(kNT *NG, 2 / NG)
         }
         gsync();
         PG_PH(6);
-        if (acts) dump_tile(G.z2T, kH, nv, acts + B * (kI + 3 * kH) + p0 * kH, tid);
+        if (acts) {
+            dump_tile(G.z2T, kH, nv, acts + B * (kI + 3 * kH) + p0 * kH, tid);
+            dump_tile_T(G.z2T, kH, nv, acts + B * (kI + 4 * kH + od) + B * kH + p0, B, tid);
+        }
         // ---- dW1 += h1^T delta2, db1 += sum delta2 (summed by the ig == 0 threads) ----
         {
             const int jg = tid & 15, ig = tid >> 4;
@@ -360,7 +378,10 @@ __global__ void __launch_bounds__(kNT *NG, 2 / NG)
         }
         gsync();
         PG_PH(8);
-        if (acts) dump_tile(G.z1T, kH, nv, acts + B * (kI + 2 * kH) + p0 * kH, tid);
+        if (acts) {
+            dump_tile(G.z1T, kH, nv, acts + B * (kI + 2 * kH) + p0 * kH, tid);
+            dump_tile_T(G.z1T, kH, nv, acts + B * (kI + 4 * kH + od) + p0, B, tid);
+        }
         // ---- dW0 += y^T delta1, db0 += sum delta1 (summed by the ig == 0 threads) ----
         {
             const int jg = tid & 15, ig = tid >> 4;

@@ -536,20 +536,27 @@ def test_exchange_touched_union_any_dtype(dtype):
         assert float(st.loss_sum[0]) == 4.0
 
 
-@pytest.mark.parametrize("od", [3, 2, 4])
-def test_reference_order_mlp_grads_bit_exact(od):
+@pytest.mark.parametrize("od,B", [(3, 8192), (2, 8192), (4, 8192), (3, 8194), (3, 9002)])
+def test_reference_order_mlp_grads_bit_exact(od, B):
     """reference_order=True: every MLP weight and bias gradient of a batch is
     bit-identical to numpy/OpenBLAS's (mlp.py:80-84); with the forward and
-    dL/dy already in OpenBLAS order the whole MLP backward is exact."""
+    dL/dy already in OpenBLAS order the whole MLP backward is exact.  Ragged
+    batches (B % 4 != 0) take the scalar bias-chain path and the balanced
+    last two OpenBLAS K-blocks.  Pinned for even batches of >= 8192 samples
+    (the reference's default 8192 included; test_openblas_wgrad_order pins
+    the block-chain model on the CPU): for odd K, and for small products
+    (e.g. K = 1000 into the 3-wide output layer) OpenBLAS 0.3.30 takes other
+    sgemm paths whose order the model does not reproduce — those batches
+    agree to rounding, not bit for bit."""
     import paper_2312_17241_b200 as pg
     img = np.random.default_rng(od).random((64, 64, od)).astype(np.float32)
     kw = dict(C1, out_dim=od)
     m, om = _models(kw, perturb=True)
-    st = pg.TrainState(m, img, pg.TrainConfig(batch_size=8192, seed=0), reference_order=True)
+    st = pg.TrainState(m, img, pg.TrainConfig(batch_size=B, seed=0), reference_order=True)
     xs, targets = st.sample_batch()
     st.loss_sum.zero_()
     st.compute_grads(xs, targets)
-    ost = O.TrainState(om, img, O.TrainCfg(batch_size=8192, seed=0))
+    ost = O.TrainState(om, img, O.TrainCfg(batch_size=B, seed=0))
     oxs, otg = ost.sample_batch()
     y, traces = O.encode_forward(om, oxs)
     out, cache = O.mlp_forward(om.W, om.b, y)
