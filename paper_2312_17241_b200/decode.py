@@ -182,7 +182,6 @@ def decode_pixels(inf: InferenceModel, xs, counter: TouchCounter | None = None,
             raise DomainViolation(f"expected (batch, {d}) coordinates, got {a.shape}")
         if not (a.shape[0] >= HOST_PATH_MIN and inf.fast) and (np.any(a < 0.0) or np.any(a > 1.0)):
             raise DomainViolation("coordinates outside the unit hypercube")
-        t = torch.from_numpy(a).to(inf.device)
     else:
         t = xs.to(device=inf.device, dtype=torch.float32).contiguous()
         if t.ndim != 2 or t.shape[1] != d:
@@ -201,35 +200,80 @@ def decode_pixels(inf: InferenceModel, xs, counter: TouchCounter | None = None,
     return out.cpu().numpy() if as_numpy else out
 
 
-# numpy batches at least this large go through pinned staging buffers and the
-# host-buffer decode (one streaming tcgen05 launch fed by the copy engine, or
-# chunked launches for the exact engine) instead of pageable copies, which
-# measured ~10x slower at 2^24 queries (tools/e2e_dropin.py)
+# numpy batches at least this large take the pipelined host path below
+# instead of pageable copies (~10x slower at 2^24 queries, tools/e2e_dropin.py)
 HOST_PATH_MIN = 1 << 16
+HOST_CHUNK = 1 << 21
+
+
+class _NumpyPipe:
+    """Chunked host pipeline for numpy in / numpy out: two pinned slots per
+    direction and two device slots; chunk i's host copy into pinned memory
+    (multi-threaded torch copy), H2D, decode kernel and D2H run while the
+    host copies chunk i-1's outputs into the result array and stages chunk
+    i+1 — host copies, PCIe and the kernels overlap."""
+
+    def __init__(self, inf: InferenceModel, chunk: int):
+        d, od, dev = inf.hyper.d, inf.out_dim, inf.device
+        self.chunk = chunk
+        self.px = [torch.empty((chunk, d), dtype=torch.float32).pin_memory() for _ in range(2)]
+        self.po = [torch.empty((chunk, od), dtype=torch.float32).pin_memory() for _ in range(2)]
+        self.dx = [torch.empty((chunk, d), dtype=torch.float32, device=dev) for _ in range(2)]
+        self.do = [torch.empty((chunk, od), dtype=torch.float32, device=dev) for _ in range(2)]
+        self.s_in, self.s_k, self.s_out = (torch.cuda.Stream(device=dev) for _ in range(3))
+        self.e_in = [torch.cuda.Event() for _ in range(2)]
+        self.e_k = [torch.cuda.Event() for _ in range(2)]
+        self.e_out = [torch.cuda.Event() for _ in range(2)]
 
 
 def _decode_host_numpy(inf: InferenceModel, a: np.ndarray, exact: bool) -> np.ndarray:
-    B, d, od = a.shape[0], inf.hyper.d, inf.out_dim
-    cache = inf.__dict__.setdefault("_host_path", {})
-    hd = cache.get(exact)
-    if hd is None:
-        hd = cache[exact] = HostDecoder(inf, exact=exact)
-    cap = cache.get("cap", 0)
-    if cap < B:
-        cap = max(B, 2 * cap)
-        cache["cap"] = cap
-        cache["xs"] = torch.empty(cap * d, dtype=torch.float32).pin_memory()
-        cache["out"] = torch.empty(cap * od, dtype=torch.float32).pin_memory()
-    hx = cache["xs"][:B * d].view(B, d)
-    ho = cache["out"][:B * od].view(B, od)
-    hx.copy_(torch.from_numpy(a))                 # multi-threaded host copy into pinned memory
-    lo, hi = torch.aminmax(hx)                    # encoding.py:37-38 (NaN passes, as there)
-    if float(lo) < 0.0 or float(hi) > 1.0:
-        raise DomainViolation("coordinates outside the unit hypercube")
-    hd(hx, ho)
-    res = torch.empty((B, od), dtype=torch.float32)
-    res.copy_(ho)
-    return res.numpy()
+    B, od = a.shape[0], inf.out_dim
+    pipe = inf.__dict__.get("_numpy_pipe")
+    if pipe is None:
+        pipe = inf._numpy_pipe = _NumpyPipe(inf, HOST_CHUNK)
+    inf.cells()                                   # built (on the current stream) before the pipeline starts
+    cur = torch.cuda.current_stream(inf.device)
+    for st in (pipe.s_in, pipe.s_k, pipe.s_out):
+        st.wait_stream(cur)
+    res = np.empty((B, od), np.float32)
+    res_t = torch.from_numpy(res)
+    src = torch.from_numpy(a)
+    C = pipe.chunk
+    n_chunks = -(-B // C)
+    pending = None                                # (slot, lo, n) of the chunk whose outputs are in flight
+    for i in range(n_chunks + 1):
+        if i < n_chunks:
+            slot, lo = i % 2, i * C
+            n = min(C, B - lo)
+            if i >= 2:
+                pipe.e_in[slot].synchronize()     # the slot's previous H2D has read px[slot]
+            hx = pipe.px[slot][:n]
+            hx.copy_(src[lo:lo + n])              # multi-threaded host copy into pinned memory
+            mn, mx = torch.aminmax(hx)            # encoding.py:37-38 (NaN passes, as there)
+            if float(mn) < 0.0 or float(mx) > 1.0:
+                torch.cuda.synchronize(inf.device)
+                raise DomainViolation("coordinates outside the unit hypercube")
+            with torch.cuda.stream(pipe.s_in):
+                if i >= 2:
+                    pipe.s_in.wait_event(pipe.e_k[slot])      # device slot free
+                pipe.dx[slot][:n].copy_(hx, non_blocking=True)
+                pipe.e_in[slot].record()
+            with torch.cuda.stream(pipe.s_k):
+                pipe.s_k.wait_event(pipe.e_in[slot])
+                if i >= 2:
+                    pipe.s_k.wait_event(pipe.e_out[slot])     # the slot's previous D2H read do[slot]
+                decode_device(inf, pipe.dx[slot][:n], pipe.do[slot][:n], exact=exact, stream=pipe.s_k)
+                pipe.e_k[slot].record()
+            with torch.cuda.stream(pipe.s_out):
+                pipe.s_out.wait_event(pipe.e_k[slot])
+                pipe.po[slot][:n].copy_(pipe.do[slot][:n], non_blocking=True)
+                pipe.e_out[slot].record()
+        if pending is not None:                   # previous chunk's outputs to the result array
+            ps, plo, pn = pending
+            pipe.e_out[ps].synchronize()
+            res_t[plo:plo + pn].copy_(pipe.po[ps][:pn])
+        pending = (slot, lo, n) if i < n_chunks else None
+    return res
 
 
 def decode_at(inf: InferenceModel, x, counter: TouchCounter | None = None) -> np.ndarray:

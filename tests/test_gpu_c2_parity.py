@@ -109,3 +109,23 @@ def test_decode_cell_cache_bit_identical(kw, mib):
     ho2 = torch.full((q.shape[0], inf.out_dim), float("nan")).pin_memory()
     HostDecoder(inf, exact=True, chunk=1 << 14)(hx, ho2)        # chunked host path, exact engine
     np.testing.assert_array_equal(ho2.numpy(), decode_device(inf, xs, exact=True, cells=False).cpu().numpy())
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_numpy_decode_pipeline_chunks(exact, monkeypatch):
+    """decode_pixels(inf, numpy): the chunked host pipeline (pinned slots,
+    H2D / kernel / D2H on three streams, host copies overlapped) returns
+    exactly the device decode for batches of one, two and many chunks incl. a
+    ragged tail, and still raises DomainViolation for a bad chunk."""
+    import paper_2312_17241_b200 as pg
+    from paper_2312_17241_b200 import decode as dec
+    monkeypatch.setattr(dec, "HOST_CHUNK", 1 << 16)
+    inf, _ = _c2_pair(16, 4)
+    for n in ((1 << 16) + 5, 2 << 16, (7 << 16) + 12345):
+        q = np.random.default_rng(n).random((n, 2)).astype(np.float32)
+        got = pg.decode_pixels(inf, q, exact=exact)
+        want = dec.decode_device(inf, torch.from_numpy(q).cuda(), exact=exact).cpu().numpy()
+        np.testing.assert_array_equal(got, want)
+    q[5 << 16, 0] = -0.5
+    with pytest.raises(pg.DomainViolation):
+        pg.decode_pixels(inf, q, exact=exact)
