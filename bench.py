@@ -174,6 +174,20 @@ def gathers_per_query(hyper, inf):
     return sum(1 if c else C for c in cached) + C * (len(probed_unc) - smem)
 
 
+def train_l2_ops_per_sample(hyper, n_probed):
+    """Random L2 operations (gathers + reductions) one training sample issues
+    in the fused step: forward 1 per dense/hashed corner, 2 per probed corner
+    (baked byte + row or whole range); backward 1 reduction per dense/hashed
+    corner, per probed corner the confidence row and probing range loads plus
+    ceil(2 N_p / 4) feature and ceil(N_p / 4) confidence 16-byte reductions."""
+    C, L, n_p = 1 << hyper.d, hyper.n_levels, hyper.n_p
+    plain = L - n_probed
+    fwd = C * (plain + 2 * n_probed)
+    reds = -(-2 * n_p // 4) + -(-n_p // 4)
+    bwd = C * (plain + n_probed * (2 + reds))
+    return fwd + bwd
+
+
 def train_bytes_per_sample(hyper, n_probed):
     """encode fwd + recompute-bwd bytes per training sample."""
     C, L, F, d, n_p = 1 << hyper.d, hyper.n_levels, hyper.feature_dim, hyper.d, hyper.n_p
@@ -411,7 +425,8 @@ def run_gpu(args, rank, world, local_rank):
         dropin[name] = world * B_INFER * n_rep / max_over_ranks(time.perf_counter() - t0)
 
     # ---------------- training (C1, data parallel) ----------------
-    train = run_train(args, pg, torch, dist, rank, world, dev, barrier, max_over_ranks, l2_stream)
+    train = run_train(args, pg, torch, dist, rank, world, dev, barrier, max_over_ranks, l2_stream,
+                      l2_gather * 1e9 / 8)
     extra = {}
     if not args.quick:
         extra["train_c3"] = run_train_field(args, pg, torch, dist, rank, world, barrier, max_over_ranks, "c3",
@@ -478,7 +493,8 @@ def run_gpu(args, rank, world, local_rank):
     return line, e2e_launches
 
 
-def run_train(args, pg, torch, dist, rank, world, dev, barrier, max_over_ranks, l2_stream=None):
+def run_train(args, pg, torch, dist, rank, world, dev, barrier, max_over_ranks, l2_stream=None,
+              l2_gather_rate=None):
     from tests.golden_util import smooth_image
     hyper = pg.HyperParams(**C1)
     model = pg.init_model(hyper, seed=0)
@@ -513,6 +529,11 @@ def run_train(args, pg, torch, dist, rank, world, dev, barrier, max_over_ranks, 
             "encode_bytes_per_sample": bps,
             "encode_algorithmic_gbs": B_TRAIN * bps / (ms * 1e-3) / 1e9,
             "encode_frac_of_l2_stream": (B_TRAIN * bps / (ms * 1e-3) / 1e9 / l2_stream) if l2_stream else None,
+            "l2_random_ops_per_sample": train_l2_ops_per_sample(hyper, n_probed),
+            "random_op_floor_ms": (train_l2_ops_per_sample(hyper, n_probed) * B_TRAIN / l2_gather_rate * 1e3
+                                   if l2_gather_rate else None),
+            "frac_of_random_op_floor": (train_l2_ops_per_sample(hyper, n_probed) * B_TRAIN / l2_gather_rate * 1e3 / ms
+                                        if l2_gather_rate else None),
             "kernel": "train_mma_kernel (3xTF32 mma.sync MLP; exact_mlp=True selects the OpenBLAS-order FFMA kernel)",
             "traffic": ncu_traffic("train_mma_kernel", B_TRAIN),
             "last_loss": loss, "scaling": "weak"}
