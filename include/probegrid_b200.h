@@ -248,6 +248,13 @@ int pg_decode_host_f32(const pg_grid *grid, const pg_mlp *mlp,
 int64_t pg_cells_plan(const pg_grid *grid, int64_t budget_bytes, pg_cells *plan);
 int pg_cells_build(const pg_grid *grid, const void *feats16, const uint8_t *baked,
                    const pg_cells *cells, void *stream);
+/* The same for fp32 F = 2 rows (8 bytes per corner: the training tables;
+ * row_bytes 4 = pg_cells_plan).  The fused training step reads its forward
+ * levels from such a cache (pg_train_fused_ex_f32), rebuilt every step. */
+int64_t pg_cells_plan_rows(const pg_grid *grid, int64_t budget_bytes, int row_bytes,
+                           pg_cells *plan);
+int pg_cells_build_f32(const pg_grid *grid, const float *feats, const uint8_t *baked,
+                       const pg_cells *cells, void *stream);
 /* pg_decode_f32 / pg_decode_host_f32 / pg_decode_host_stream_f32 reading the
  * cached levels from `cells` (NULL = none); every fused engine (tcgen05,
  * FFMA, exact reference order) uses it on fp16 tables. */
@@ -357,6 +364,18 @@ int pg_train_fused_rep_f32(const pg_grid *grid, const pg_mlp *mlp, const float *
                            float *gfeat, float *gconf, uint8_t *touched,
                            float *gparams, double *loss_sum, float *dy_out,
                            float *gfeat_rep, int reps, void *stream);
+/* pg_train_fused_rep_f32 whose encode FORWARD reads the levels in `cells`
+ * (an fp32 cell cache of these tables built by pg_cells_build_f32 for this
+ * step; NULL = none): one 32-byte record per cached level and sample instead
+ * of the dependent index and row gathers; identical values. */
+int pg_train_fused_ex_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
+                          const float *targets, int64_t B, const float *feats,
+                          const uint8_t *baked, const float *conf,
+                          const float *params, float scale, unsigned flags,
+                          float *gfeat, float *gconf, uint8_t *touched,
+                          float *gparams, double *loss_sum, float *dy_out,
+                          float *gfeat_rep, int reps, const pg_cells *cells,
+                          void *stream);
 
 /* Standalone batched MLP, mlp.py:55-85 (mlp_forward / mlp_backward with an
  * arbitrary upstream gradient; ReLU hidden layers, linear output; numpy /

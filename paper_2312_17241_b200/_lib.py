@@ -88,6 +88,7 @@ _SIGS.update({
     "pg_decode_host_stream_cells_f32": [_G, _M, _P, _I64, _P, _P, _P, ctypes.c_uint, _C, _I64, _P, _P, _P, _P,
                                         _P, _P, _P],
     "pg_cells_build": [_G, _P, _P, _C, _P],
+    "pg_cells_build_f32": [_G, _P, _P, _C, _P],
     "pg_decode_host_cells_f32": [_G, _M, _P, _I64, _P, _P, _P, ctypes.c_uint, _C, _I64, _P, _P, _P, _P, _P, _P],
     "pg_decode_host_f32": [_G, _M, _P, _I64, _P, _P, _P, ctypes.c_uint, _I64, _P, _P, _P, _P, _P, _P],
     "pg_touched_to_f32": [_P, _I64, _P, _P],
@@ -108,6 +109,8 @@ _SIGS.update({
                            _P, _P, _P, _P],
     "pg_train_fused_rep_f32": [_G, _M, _P, _P, _I64, _P, _P, _P, _P, _F, ctypes.c_uint, _P, _P, _P,
                                _P, _P, _P, _P, _I, _P],
+    "pg_train_fused_ex_f32": [_G, _M, _P, _P, _I64, _P, _P, _P, _P, _F, ctypes.c_uint, _P, _P, _P,
+                              _P, _P, _P, _P, _I, _C, _P],
     "pg_train_fused_ref_f32": [_G, _M, _P, _P, _I64, _P, _P, _P, _P, _F, ctypes.c_uint, _P, _P,
                                _P, _P, _P, _P],
     "pg_mlp_wgrad_blas_f32": [_M, _P, _I64, _P, _P],
@@ -128,6 +131,7 @@ _SIGS.update({
 })
 _RESTYPE_I64 = {"pg_dedup_workspace_bytes": [_I64, _I64],
                 "pg_cells_plan": [_G, _I64, _C],
+                "pg_cells_plan_rows": [_G, _I64, _I, _C],
                 "pg_mlp_train_workspace_floats": [_I64, _M],
                 "pg_mlp_acts_floats": [_I64, _M]}
 

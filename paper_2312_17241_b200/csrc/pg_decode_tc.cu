@@ -596,17 +596,29 @@ int decode_umma(const pg_grid *g, int od, const float *xs, int64_t B, const void
     return check_launch("decode_umma");
 }
 
-// ---- decode cell cache (pg_cells): records of the 2^d resolved corner rows
-// per cell of the coarsest levels (pg_cells_plan / pg_cells_build)
-template <int D>
-__global__ void build_cells_kernel(const pg_grid g, int l, const __half *__restrict__ feats,
-                                   const uint8_t *__restrict__ baked, uint32_t *__restrict__ rec, int64_t ncells) {
+// ---- cell cache (pg_cells): records of the 2^d resolved corner rows per
+// cell of the coarsest levels; R = the row type (uint32_t: binary16 F = 2 of
+// the inference tables; uint2: fp32 F = 2 of the training tables).  One
+// launch builds every cached level (flattened (level, cell) index).
+struct CellLevels {
+    int n;
+    int level[PG_MAX_LEVELS];
+    int64_t start[PG_MAX_LEVELS + 1];   // first flattened cell index of each entry
+    int64_t rec[PG_MAX_LEVELS];         // record offset of the level, in rows
+};
+template <int D, typename R>
+__global__ void build_cells_kernel(const pg_grid g, const CellLevels cl, const R *__restrict__ feats,
+                                   const uint8_t *__restrict__ baked, R *__restrict__ out) {
     constexpr int C = 1 << D;
     const uint32_t nf_mask = (uint32_t)g.n_f - 1u, nc_mask = (uint32_t)g.n_c - 1u;
-    const int res = g.res[l], kind = g.kind[l];
-    const uint32_t *tab = reinterpret_cast<const uint32_t *>(feats + (int64_t)l * g.n_f * 2);
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ncells;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t total = cl.start[cl.n];
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int e = 0;
+        while (e + 1 < cl.n && t >= cl.start[e + 1]) ++e;
+        const int l = cl.level[e], res = g.res[l], kind = g.kind[l];
+        const int64_t i = t - cl.start[e];
+        const R *tab = feats + (int64_t)l * g.n_f;
         int c[D];
         int64_t rem = i;
 #pragma unroll
@@ -614,6 +626,7 @@ __global__ void build_cells_kernel(const pg_grid g, int l, const __half *__restr
             c[a] = (int)(rem % res);
             rem /= res;
         }
+        R *rec = out + cl.rec[e] + i * C;
 #pragma unroll
         for (int k = 0; k < C; ++k) {
             int idx;
@@ -628,9 +641,38 @@ __global__ void build_cells_kernel(const pg_grid g, int l, const __half *__restr
                     idx = (int)((h << g.log2_np) & nf_mask) + (int)baked[(int64_t)g.slot[l] * g.n_c + r];
                 }
             }
-            rec[i * C + k] = tab[idx];
+            rec[k] = tab[idx];
         }
     }
+}
+
+template <typename R>
+static int build_cells(const pg_grid *grid, const void *feats, const uint8_t *baked, const pg_cells *cells,
+                       cudaStream_t s) {
+    if (int e = validate_grid(grid)) return e;
+    PG_REQUIRE(cells != nullptr, "cells: null");
+    PG_REQUIRE(grid->feature_dim == 2, "cell cache: F = 2 tables only");
+    CellLevels cl;
+    cl.n = 0;
+    cl.start[0] = 0;
+    for (int l = 0; l < grid->n_levels; ++l) {
+        if (cells->off[l] < 0) continue;
+        PG_REQUIRE(cells->data != nullptr, "cells: null data with cached levels");
+        int64_t ncells = 1;
+        for (int a = 0; a < grid->d; ++a) ncells *= grid->res[l];
+        cl.level[cl.n] = l;
+        cl.rec[cl.n] = cells->off[l] * 16 / (int64_t)sizeof(R);
+        cl.start[cl.n + 1] = cl.start[cl.n] + ncells;
+        ++cl.n;
+    }
+    if (cl.n == 0) return PG_OK;
+    const int grd = grid_for(cl.start[cl.n], 256, 148 * 32);
+    R *out = reinterpret_cast<R *>(const_cast<void *>(cells->data));
+    if (grid->d == 2)
+        build_cells_kernel<2, R><<<grd, 256, 0, s>>>(*grid, cl, (const R *)feats, baked, out);
+    else
+        build_cells_kernel<3, R><<<grd, 256, 0, s>>>(*grid, cl, (const R *)feats, baked, out);
+    return check_launch("cells_build");
 }
 
 }  // namespace pg
@@ -639,8 +681,8 @@ using namespace pg;
 
 extern "C" {
 
-int64_t pg_cells_plan(const pg_grid *grid, int64_t budget_bytes, pg_cells *plan) {
-    if (!grid || !plan) return -1;
+int64_t pg_cells_plan_rows(const pg_grid *grid, int64_t budget_bytes, int row_bytes, pg_cells *plan) {
+    if (!grid || !plan || (row_bytes != 4 && row_bytes != 8)) return -1;
     const int C = 1 << grid->d;
     int64_t total = 0;
     bool open = true;
@@ -650,7 +692,7 @@ int64_t pg_cells_plan(const pg_grid *grid, int64_t budget_bytes, pg_cells *plan)
         if (!open || l >= grid->n_levels) continue;
         int64_t cells = 1;
         for (int a = 0; a < grid->d; ++a) cells *= grid->res[l];
-        const int64_t bytes = cells * C * 4;
+        const int64_t bytes = cells * C * row_bytes;
         if (total + bytes > budget_bytes) {
             open = false;
             continue;
@@ -660,26 +702,16 @@ int64_t pg_cells_plan(const pg_grid *grid, int64_t budget_bytes, pg_cells *plan)
     }
     return total;
 }
-
+int64_t pg_cells_plan(const pg_grid *grid, int64_t budget_bytes, pg_cells *plan) {
+    return pg_cells_plan_rows(grid, budget_bytes, 4, plan);
+}
 int pg_cells_build(const pg_grid *grid, const void *feats16, const uint8_t *baked, const pg_cells *cells,
                    void *stream) {
-    if (int e = validate_grid(grid)) return e;
-    PG_REQUIRE(cells != nullptr, "cells: null");
-    PG_REQUIRE(grid->feature_dim == 2, "cell cache: F = 2 fp16 tables only");
-    cudaStream_t s = as_stream(stream);
-    for (int l = 0; l < grid->n_levels; ++l) {
-        if (cells->off[l] < 0) continue;
-        PG_REQUIRE(cells->data != nullptr, "cells: null data with cached levels");
-        int64_t ncells = 1;
-        for (int a = 0; a < grid->d; ++a) ncells *= grid->res[l];
-        uint32_t *rec = reinterpret_cast<uint32_t *>(const_cast<void *>(cells->data)) + cells->off[l] * 4;
-        const int grd = grid_for(ncells, 256, 148 * 32);
-        if (grid->d == 2)
-            build_cells_kernel<2><<<grd, 256, 0, s>>>(*grid, l, (const __half *)feats16, baked, rec, ncells);
-        else
-            build_cells_kernel<3><<<grd, 256, 0, s>>>(*grid, l, (const __half *)feats16, baked, rec, ncells);
-    }
-    return check_launch("cells_build");
+    return build_cells<uint32_t>(grid, feats16, baked, cells, as_stream(stream));
+}
+int pg_cells_build_f32(const pg_grid *grid, const float *feats, const uint8_t *baked, const pg_cells *cells,
+                       void *stream) {
+    return build_cells<uint2>(grid, feats, baked, cells, as_stream(stream));
 }
 
 }  // extern "C"

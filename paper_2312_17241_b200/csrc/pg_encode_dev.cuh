@@ -91,6 +91,43 @@ __device__ __forceinline__ float2 encode_level_fwd2_cell(const pg_grid &g, int l
     return make_float2(y0, y1);
 }
 
+// fp32 cell records (the training tables, rebuilt every step): 2^d corners x
+// 8 B per cell, read as 32-byte loads; same weights, values and blend order
+// as encode_level_fwd2, so bit-identical
+template <int D>
+__device__ __forceinline__ float2 encode_level_fwd2_cell32(const pg_grid &g, int l, const float (&x)[D],
+                                                           const uint4 *__restrict__ rec) {
+    constexpr int C = 1 << D;
+    const int res = g.res[l];
+    int c[D];
+    float t[D], omt[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        c[a] = cell_coord(x[a], res, t[a]);
+        omt[a] = __fsub_rn(1.0f, t[a]);
+    }
+    int64_t cell = c[D - 1];
+#pragma unroll
+    for (int a = D - 2; a >= 0; --a) cell = cell * res + c[a];
+    const float *p = reinterpret_cast<const float *>(rec + (int64_t)(C / 2) * cell);
+    float f[2 * C];
+#pragma unroll
+    for (int h = 0; h < C / 4; ++h) {
+        float f8[8];
+        ld_nc_v8(p + 8 * h, f8);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f[8 * h + i] = f8[i];
+    }
+    float y0 = 0.0f, y1 = 0.0f;
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+        const float w = corner_weight<float, D>(k, t, omt);
+        y0 = __fadd_rn(y0, __fmul_rn(w, f[2 * k]));
+        y1 = __fadd_rn(y1, __fmul_rn(w, f[2 * k + 1]));
+    }
+    return make_float2(y0, y1);
+}
+
 // Forward: blended F=2 feature of point x at level l (bit-exact vs _core).
 template <typename FT, int D>
 __device__ __forceinline__ float2 encode_level_fwd2(const pg_grid &g, int l, const float (&x)[D],

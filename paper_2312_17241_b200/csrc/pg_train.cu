@@ -504,7 +504,8 @@ bool train_fast_ok(const pg_grid *g, const pg_mlp *m) {
 template <typename ACC, typename LACC>
 int train_mma(const pg_grid *g, int od, const float *xs, const float *targets, int64_t B, const float *feats,
               const uint8_t *baked, const float *conf, const float *params, float scale, int sig, ACC *gfeat,
-              ACC *gconf, uint8_t *touched, ACC *gparams, LACC *loss_sum, float *dy_out, cudaStream_t s);
+              ACC *gconf, uint8_t *touched, ACC *gparams, LACC *loss_sum, float *dy_out, cudaStream_t s,
+              const pg_cells *cells = nullptr);
 
 // gfeat += sum of the `reps` replica tables (each n floats), replicas zeroed
 __global__ void reduce_replicas_kernel(float *__restrict__ rep, int reps, int64_t n, float *__restrict__ gfeat) {
@@ -523,7 +524,7 @@ int train_fused(const pg_grid *g, const pg_mlp *m, const float *xs, const float 
                 const float *feats, const uint8_t *baked, const float *conf, const float *params,
                 float scale, unsigned flags, ACC *gfeat, ACC *gconf, uint8_t *touched,
                 ACC *gparams, LACC *loss_sum, float *dy_out, float *acts, cudaStream_t s,
-                float *gfeat_rep = nullptr, int reps = 1) {
+                float *gfeat_rep = nullptr, int reps = 1, const pg_cells *cells = nullptr) {
     if (int e = validate_grid(g)) return e;
     PG_REQUIRE(train_fast_ok(g, m), "fused training needs F=2, 16 levels, N_p<=16, MLP [32,64,64,<=4]");
     if (B == 0) return PG_OK;
@@ -551,13 +552,13 @@ int train_fused(const pg_grid *g, const pg_mlp *m, const float *xs, const float 
         PG_REQUIRE(od == 4 && !sig && !(flags & PG_EXACT_MLP) && !acts && B % 64 == 0,
                    "PG_COMPOSITE: out_dim 4, no sigmoid, tensor-core MLP, B a multiple of 64 samples");
         return fold(train_mma<ACC, LACC>(g, od, xs, targets, B, feats, baked, conf, params, scale, 2 | touch_all, gf, gconf,
-                                    touched, gparams, loss_sum, dy_out, s));
+                                    touched, gparams, loss_sum, dy_out, s, cells));
     }
     // fast path: tensor-core MLP (pg_train_mma.cu); this file's FFMA kernel is
     // the OpenBLAS-order path (PG_EXACT_MLP, reference-order mode)
     if (!acts && !(flags & PG_EXACT_MLP))
         return fold(train_mma<ACC, LACC>(g, od, xs, targets, B, feats, baked, conf, params, scale, sig | touch_all, gf, gconf,
-                                    touched, gparams, loss_sum, dy_out, s));
+                                    touched, gparams, loss_sum, dy_out, s, cells));
     static DeviceOnce configured[8];
     const int sms = device_sms();
     // tile pipelines per CTA (1 or 2)
@@ -613,6 +614,16 @@ extern "C" int pg_train_fused_rep_f32(const pg_grid *grid, const pg_mlp *mlp, co
     return pg::train_fused<float, double>(grid, mlp, xs, targets, B, feats, baked, conf, params, scale,
                                           flags, gfeat, gconf, touched, gparams, loss_sum, dy_out,
                                           nullptr, pg::as_stream(stream), gfeat_rep, reps);
+}
+extern "C" int pg_train_fused_ex_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,
+                                     const float *targets, int64_t B, const float *feats,
+                                     const uint8_t *baked, const float *conf, const float *params,
+                                     float scale, unsigned flags, float *gfeat, float *gconf,
+                                     uint8_t *touched, float *gparams, double *loss_sum, float *dy_out,
+                                     float *gfeat_rep, int reps, const pg_cells *cells, void *stream) {
+    return pg::train_fused<float, double>(grid, mlp, xs, targets, B, feats, baked, conf, params, scale,
+                                          flags, gfeat, gconf, touched, gparams, loss_sum, dy_out,
+                                          nullptr, pg::as_stream(stream), gfeat_rep, reps, cells);
 }
 
 extern "C" int pg_train_fused_ref_f32(const pg_grid *grid, const pg_mlp *mlp, const float *xs,

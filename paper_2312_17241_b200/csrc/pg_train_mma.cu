@@ -254,7 +254,8 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
                                        // bits 8-15: feature-gradient replicas - 1 (gfeat then
                                        // holds that many copies; CTA b adds into copy b % reps)
                      ACC *__restrict__ gfeat, ACC *__restrict__ gconf, uint8_t *__restrict__ touched,
-                     ACC *__restrict__ gparams, LACC *__restrict__ loss_sum, float *__restrict__ dy_out) {
+                     ACC *__restrict__ gparams, LACC *__restrict__ loss_sum, float *__restrict__ dy_out,
+                     const CellMap cmap) {
     using namespace tm;
     const int sigmoid = mode_flags & 3;
     const bool touch_all = (mode_flags & 4) != 0;
@@ -353,7 +354,8 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
 #pragma unroll 2
         for (int it = 0; it < 4; ++it) {
             const int l = lsub + 4 * it;
-            const float2 yv = encode_level_fwd2_rng<FT, D>(g, l, x, feats_fwd, baked);
+            const float2 yv = cmap.off[l] >= 0 ? encode_level_fwd2_cell32<D>(g, l, x, cmap.cells + cmap.off[l])
+                                               : encode_level_fwd2_rng<FT, D>(g, l, x, feats_fwd, baked);
             G.y[(2 * l) * kS + pl] = yv.x;
             G.y[(2 * l + 1) * kS + pl] = yv.y;
         }
@@ -517,7 +519,9 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
             if (has_next) {
                 // N_p = 4: the probing range fetched whole beside the baked
                 // byte (one L2 round trip, not two): 0.5499 -> 0.5473 ms (C1)
-                const float2 yv = encode_level_fwd2_rng<FT, D>(g, l, xn, feats_fwd, baked);
+                // levels in the step's cell cache: one 32-byte record load
+                const float2 yv = cmap.off[l] >= 0 ? encode_level_fwd2_cell32<D>(g, l, xn, cmap.cells + cmap.off[l])
+                                                   : encode_level_fwd2_rng<FT, D>(g, l, xn, feats_fwd, baked);
                 G.y[(2 * l) * kS + pl] = yv.x;
                 G.y[(2 * l + 1) * kS + pl] = yv.y;
             }
@@ -595,8 +599,16 @@ PG_PH_READER(pg_phase_prof_read_mma)
 template <typename ACC, typename LACC>
 int train_mma(const pg_grid *g, int od, const float *xs, const float *targets, int64_t B, const float *feats,
               const uint8_t *baked, const float *conf, const float *params, float scale, int sig, ACC *gfeat,
-              ACC *gconf, uint8_t *touched, ACC *gparams, LACC *loss_sum, float *dy_out, cudaStream_t s) {
+              ACC *gconf, uint8_t *touched, ACC *gparams, LACC *loss_sum, float *dy_out, cudaStream_t s,
+              const pg_cells *cells) {
     static DeviceOnce configured[18];
+    CellMap cmap;
+    cmap.cells = nullptr;
+    for (int l = 0; l < PG_MAX_LEVELS; ++l) cmap.off[l] = -1;
+    if (cells && cells->data) {
+        cmap.cells = reinterpret_cast<const uint4 *>(cells->data);
+        for (int l = 0; l < g->n_levels; ++l) cmap.off[l] = cells->off[l] >= 0 ? (int32_t)cells->off[l] : -1;
+    }
     const int sms = device_sms();
     // tile pipelines per CTA (1 or 2)
     static const int groups = getenv("PG_TRAIN_GROUPS") && atoi(getenv("PG_TRAIN_GROUPS")) == 1 ? 1 : 2;
@@ -616,7 +628,7 @@ int train_mma(const pg_grid *g, int od, const float *xs, const float *targets, i
         const int64_t want = (ntiles + NG_ - 1) / NG_, cap = (int64_t)sms * (2 / NG_);                \
         const int grd = (int)(want < cap ? want : cap);                                               \
         kern<<<grd, tm::kNT * NG_, smem, s>>>(*g, xs, targets, B, feats, feats, baked, conf, params, od, \
-                                              scale, sig, gfeat, gconf, touched, gparams, loss_sum, dy_out); \
+                                              scale, sig, gfeat, gconf, touched, gparams, loss_sum, dy_out, cmap); \
     } while (0)
 #define PG_TRAIN_MMA_AGG(D_, NP_, IDX)                                                                \
     do {                                                                                              \
@@ -627,7 +639,7 @@ int train_mma(const pg_grid *g, int od, const float *xs, const float *targets, i
         const int64_t want = (ntiles + 1) / 2, cap = (int64_t)sms;                                    \
         const int grd = (int)(want < cap ? want : cap);                                               \
         kern<<<grd, tm::kNT * 2, smem, s>>>(*g, xs, targets, B, feats, feats, baked, conf, params, od,   \
-                                            scale, sig, gfeat, gconf, touched, gparams, loss_sum, dy_out); \
+                                            scale, sig, gfeat, gconf, touched, gparams, loss_sum, dy_out, cmap); \
     } while (0)
 #define PG_TRAIN_MMA_NG(D_, NP_, IDX)                                                                 \
     do {                                                                                              \
@@ -651,9 +663,10 @@ int train_mma(const pg_grid *g, int od, const float *xs, const float *targets, i
 template int train_mma<float, double>(const pg_grid *, int, const float *, const float *, int64_t,
                                       const float *, const uint8_t *, const float *, const float *, float,
                                       int, float *, float *, uint8_t *, float *, double *, float *,
-                                      cudaStream_t);
+                                      cudaStream_t, const pg_cells *);
 template int train_mma<fx_t, fx_t>(const pg_grid *, int, const float *, const float *, int64_t,
                                    const float *, const uint8_t *, const float *, const float *, float, int,
-                                   fx_t *, fx_t *, uint8_t *, fx_t *, fx_t *, float *, cudaStream_t);
+                                   fx_t *, fx_t *, uint8_t *, fx_t *, fx_t *, float *, cudaStream_t,
+                                   const pg_cells *);
 
 }  // namespace pg

@@ -87,6 +87,14 @@ def adam_update(param: torch.Tensor, grad: torch.Tensor, slot: AdamSlot, t: int,
               float(eps), None, _lib.stream_ptr())
 
 
+def train_cell_budget() -> int:
+    """Bytes of the per-step fp32 cell cache the fused training forward
+    reads its coarsest levels from (PG_TRAIN_CELL_MB; 0 disables).  Rebuilt
+    from the current tables at every step (one launch, ~22 MB at C1, all 16
+    levels); C1 step 0.554 -> 0.530 ms, other shapes 1-3%."""
+    return int(float(os.environ.get("PG_TRAIN_CELL_MB", "32")) * (1 << 20))
+
+
 def grad_replicas(hyper: HyperParams, dtype) -> int:
     """Copies of the feature-gradient table the fused fp32 step spreads its
     reductions over (pg_train_fused_rep_f32): small tables see every lookup
@@ -307,6 +315,20 @@ class TrainState:
             return
         if self.fused:
             reps = 1 if self.exact_mlp else self.grad_replicas
+            cells = None if self.exact_mlp else self._train_cells()
+            if cells is not None:
+                if reps > 1 and getattr(self, "_gfeat_rep", None) is None:
+                    self._gfeat_rep = torch.zeros(reps * m.n_feat, dtype=torch.float32, device=m.device)
+                # the forward's cell cache of THIS step's tables (feats/baked
+                # moved in the last optimizer step)
+                _lib.call("pg_cells_build_f32", m.grid, _lib.ptr(m.feats), _lib.ptr(m.baked), cells, s)
+                _lib.call("pg_train_fused_ex_f32", m.grid, m.mlp_desc, _lib.ptr(xs), _lib.ptr(targets),
+                          xs.shape[0], _lib.ptr(m.feats), _lib.ptr(m.baked), _lib.ptr(m.conf),
+                          _lib.ptr(m.mlp_params), scale, flags, _lib.ptr(m.gfeats), _lib.ptr(m.gconf),
+                          _lib.ptr(m.touched), _lib.ptr(m.gmlp), _lib.ptr(self.loss_sum),
+                          _lib.ptr(dy_out), _lib.ptr(getattr(self, "_gfeat_rep", None)) if reps > 1 else None,
+                          reps, cells, s)
+                return
             if reps > 1:
                 if getattr(self, "_gfeat_rep", None) is None:
                     self._gfeat_rep = torch.zeros(reps * m.n_feat, dtype=torch.float32, device=m.device)
@@ -332,6 +354,20 @@ class TrainState:
         encode_backward_device(m, xs, self.dy)
 
     @on_device
+    def _train_cells(self):
+        """fp32 cell cache plan + buffer for the fused forward (None: off)."""
+        if not hasattr(self, "_cells"):
+            self._cells = None
+            budget = train_cell_budget()
+            if budget > 0 and self.model.tdtype == torch.float32 and self.model.hyper.feature_dim == 2:
+                plan = _lib.PgCells()
+                n = int(_lib.lib().pg_cells_plan_rows(self.model.grid, budget, 8, plan))
+                if n > 0:
+                    self._cells_buf = torch.empty(n, dtype=torch.uint8, device=self.model.device)
+                    plan.data = self._cells_buf.data_ptr()
+                    self._cells = plan
+        return self._cells
+
     def apply_updates(self) -> None:
         """Dense Adam over [features | MLP] and lazy Adam + re-bake over the
         touched confidence rows; both skip the update if the loss diverged."""

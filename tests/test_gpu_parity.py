@@ -1097,3 +1097,30 @@ def test_c_abi_rejects_bad_arguments():
         _lib.call("pg_decode_host_f32", inf.grid, inf.mlp_desc, None, 10, _lib.ptr(inf.feats16), _lib.ptr(inf.baked),
                   _lib.ptr(inf.params), 0, 0, None, None, None, None, None, None)        # chunk 0
     torch.cuda.synchronize()    # the context is still healthy
+
+
+@pytest.mark.parametrize("kw", [C1, dict(), dict(n_f=2**8, n_c=2**12, n_p=16), dict(d=3, n_f=2**8, n_c=2**12, n_p=4)])
+def test_training_cell_cache_forward_identical(kw, monkeypatch):
+    """The fused step's per-step fp32 cell cache (pg_cells_build_f32 +
+    pg_train_fused_ex_f32) changes where the forward reads rows, not what it
+    reads: dL/dy of a batch is bit-identical with and without it."""
+    import paper_2312_17241_b200 as pg
+    out = []
+    for mb in ("0", "32"):
+        monkeypatch.setenv("PG_TRAIN_CELL_MB", mb)
+        m, _ = _models(kw, perturb=True)
+        d = m.hyper.d
+        if d == 2:
+            st = pg.TrainState(m, _smooth(), pg.TrainConfig(batch_size=4099, seed=0))
+            xs, tg = st.sample_batch()
+        else:
+            pts = np.random.default_rng(1).random((4099, 3)).astype(np.float32)
+            st = pg.FieldTrainState(m, pts, np.zeros((4099, m.hyper.out_dim), np.float32),
+                                    pg.TrainConfig(batch_size=4099, seed=0))
+            xs, tg = st.sample_batch()
+        assert (st._train_cells() is not None) == (mb != "0")
+        dy = torch.empty((4099, 32), device="cuda")
+        st.loss_sum.zero_()
+        st.compute_grads(xs, tg, dy_out=dy)
+        out.append(dy.cpu().numpy())
+    eq(out[0], out[1])
