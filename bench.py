@@ -455,7 +455,7 @@ def run_gpu(args, rank, world, local_rank):
                 "d2h_bytes_per_step": B_INFER * hyper.out_dim * 4,
                 "host_fallback_pipelines": fallbacks,
                 "dropin_decode_pixels_numpy_qps": dropin,
-                "path": ("pg_decode_host_stream_f32 (pinned host in/out; ONE decode launch fed 2^18-query "
+                "path": ("pg_decode_host_stream_cells_f32 (pinned host in/out; ONE decode launch fed 2^19-query "
                          "pieces by the copy engine through device flags, D2H of each piece on a stream wait "
                          "for its tile counter; 3 streams)" if hd.streaming else
                          "pg_decode_host_f32 (pinned host in/out; H2D, kernel, D2H on 3 event-ordered streams; "

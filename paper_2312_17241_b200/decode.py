@@ -332,7 +332,7 @@ class HostDecoder:
 
     @on_device
     def __init__(self, inf: InferenceModel, chunk: int = 1 << 21, exact: bool = False,
-                 stream: bool | None = None, stream_chunk: int = 1 << 18, cells: bool = True):
+                 stream: bool | None = None, stream_chunk: int = 1 << 19, cells: bool = True):
         if not inf.fast:
             raise ValueError("host decode needs the fused [32,64,64,<=4] shape")
         if stream_chunk < 128 or stream_chunk & (stream_chunk - 1):
