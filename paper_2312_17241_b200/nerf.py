@@ -182,11 +182,8 @@ class NerfTrainState(TrainState):
                 t4 = self.tgt4[:R * S].view(R, S, 4)
                 t4[:, :, 0] = deltas.view(R, S)
                 t4[:, :, 1:] = rgb[:, None, :]
-            _lib.call("pg_train_fused_f32", m.grid, m.mlp_desc, _lib.ptr(xs), _lib.ptr(t4), R * S,
-                      _lib.ptr(m.feats), _lib.ptr(m.baked), _lib.ptr(m.conf), _lib.ptr(m.mlp_params),
-                      float(np.float32(self.scale)),
-                      _lib.PG_COMPOSITE | (_lib.PG_TOUCH_ALL if self.touch_all else 0), _lib.ptr(m.gfeats), _lib.ptr(m.gconf),
-                      _lib.ptr(m.touched), _lib.ptr(m.gmlp), _lib.ptr(self.loss_sum), _lib.ptr(dy_out), s)
+            self._fused_step(xs, t4, R * S, float(np.float32(self.scale)),
+                             _lib.PG_COMPOSITE | (_lib.PG_TOUCH_ALL if self.touch_all else 0), dy_out)
             return
         encode_forward_device(m, xs, self.y)
         _lib.call("pg_nerf_train_f32", m.mlp_desc, _lib.ptr(self.y), _lib.ptr(deltas), _lib.ptr(rgb), R,

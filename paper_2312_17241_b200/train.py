@@ -314,35 +314,7 @@ class TrainState:
                       _lib.ptr(m.gmlp), s)
             return
         if self.fused:
-            reps = 1 if self.exact_mlp else self.grad_replicas
-            cells = None if self.exact_mlp else self._train_cells()
-            if cells is not None:
-                if reps > 1 and getattr(self, "_gfeat_rep", None) is None:
-                    self._gfeat_rep = torch.zeros(reps * m.n_feat, dtype=torch.float32, device=m.device)
-                # the forward's cell cache of THIS step's tables (feats/baked
-                # moved in the last optimizer step)
-                _lib.call("pg_cells_build_f32", m.grid, _lib.ptr(m.feats), _lib.ptr(m.baked), cells, s)
-                _lib.call("pg_train_fused_ex_f32", m.grid, m.mlp_desc, _lib.ptr(xs), _lib.ptr(targets),
-                          xs.shape[0], _lib.ptr(m.feats), _lib.ptr(m.baked), _lib.ptr(m.conf),
-                          _lib.ptr(m.mlp_params), scale, flags, _lib.ptr(m.gfeats), _lib.ptr(m.gconf),
-                          _lib.ptr(m.touched), _lib.ptr(m.gmlp), _lib.ptr(self.loss_sum),
-                          _lib.ptr(dy_out), _lib.ptr(getattr(self, "_gfeat_rep", None)) if reps > 1 else None,
-                          reps, cells, s)
-                return
-            if reps > 1:
-                if getattr(self, "_gfeat_rep", None) is None:
-                    self._gfeat_rep = torch.zeros(reps * m.n_feat, dtype=torch.float32, device=m.device)
-                _lib.call("pg_train_fused_rep_f32", m.grid, m.mlp_desc, _lib.ptr(xs), _lib.ptr(targets),
-                          xs.shape[0], _lib.ptr(m.feats), _lib.ptr(m.baked), _lib.ptr(m.conf),
-                          _lib.ptr(m.mlp_params), scale, flags, _lib.ptr(m.gfeats), _lib.ptr(m.gconf),
-                          _lib.ptr(m.touched), _lib.ptr(m.gmlp), _lib.ptr(self.loss_sum),
-                          _lib.ptr(dy_out), _lib.ptr(self._gfeat_rep), reps, s)
-                return
-            _lib.call("pg_train_fused_f32", m.grid, m.mlp_desc, _lib.ptr(xs), _lib.ptr(targets),
-                      xs.shape[0], _lib.ptr(m.feats), _lib.ptr(m.baked), _lib.ptr(m.conf),
-                      _lib.ptr(m.mlp_params), scale, flags, _lib.ptr(m.gfeats), _lib.ptr(m.gconf),
-                      _lib.ptr(m.touched), _lib.ptr(m.gmlp), _lib.ptr(self.loss_sum),
-                      _lib.ptr(dy_out), s)
+            self._fused_step(xs, targets, xs.shape[0], scale, flags, dy_out)
             return
         sfx = "f64" if m.tdtype == torch.float64 else "f32"
         encode_forward_device(m, xs, self.y)
@@ -354,6 +326,25 @@ class TrainState:
         encode_backward_device(m, xs, self.dy)
 
     @on_device
+    def _fused_step(self, xs, targets, n, scale, flags, dy_out) -> None:
+        """One fused fp32 training pass (pg_train_fused_ex_f32): the forward
+        reads this step's cell cache (rebuilt here from the current tables),
+        feature gradients go through the replica buffer for small tables;
+        the OpenBLAS-order MLP (exact_mlp) takes neither."""
+        m, s = self.model, _lib.stream_ptr()
+        exact = bool(flags & _lib.PG_EXACT_MLP)
+        reps = 1 if exact else self.grad_replicas
+        cells = None if exact else self._train_cells()
+        if reps > 1 and getattr(self, "_gfeat_rep", None) is None:
+            self._gfeat_rep = torch.zeros(reps * m.n_feat, dtype=torch.float32, device=m.device)
+        if cells is not None:
+            _lib.call("pg_cells_build_f32", m.grid, _lib.ptr(m.feats), _lib.ptr(m.baked), cells, s)
+        _lib.call("pg_train_fused_ex_f32", m.grid, m.mlp_desc, _lib.ptr(xs), _lib.ptr(targets), n,
+                  _lib.ptr(m.feats), _lib.ptr(m.baked), _lib.ptr(m.conf), _lib.ptr(m.mlp_params), scale, flags,
+                  _lib.ptr(m.gfeats), _lib.ptr(m.gconf), _lib.ptr(m.touched), _lib.ptr(m.gmlp),
+                  _lib.ptr(self.loss_sum), _lib.ptr(dy_out),
+                  _lib.ptr(self._gfeat_rep) if reps > 1 else None, reps, cells, s)
+
     def _train_cells(self):
         """fp32 cell cache plan + buffer for the fused forward (None: off)."""
         if not hasattr(self, "_cells"):
