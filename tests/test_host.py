@@ -107,3 +107,31 @@ def test_product_does_not_import_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in text.replace("oracle (", ""), f
+
+
+def test_round2_host_rules():
+    """Host-side rules of the round-2 paths: feature-gradient replicas by
+    probing ranges per level, the cell-cache budgets, the bench's operation
+    and byte counts."""
+    import os
+    import bench
+    import paper_2312_17241_b200 as pg
+    from paper_2312_17241_b200 import train
+    f32 = np.float32
+    assert train.grad_replicas(pg.HyperParams(n_f=2**12, n_c=2**14, n_p=4), f32) == 1      # 1024 ranges
+    assert train.grad_replicas(pg.HyperParams(n_f=2**8, n_c=2**12, n_p=16), f32) == 8      # 16 ranges
+    assert train.grad_replicas(pg.HyperParams(), f32) == 1                                 # 4 ranges: warp-aggregated
+    assert train.grad_replicas(pg.HyperParams(n_f=2**8, n_c=2**12, n_p=4), np.float64) == 1
+    os.environ["PG_TRAIN_REPS"] = "3"
+    try:
+        assert train.grad_replicas(pg.HyperParams(), f32) == 3
+    finally:
+        del os.environ["PG_TRAIN_REPS"]
+    assert train.train_cell_budget() == 32 << 20
+    h = pg.HyperParams(**bench.C1)
+    assert bench.train_l2_ops_per_sample(h, 10) == 328
+    assert bench.train_bytes_per_sample(h, 10) == 6840          # SURVEY 8(d): C1 6,840 B/sample
+    assert bench.infer_bytes_per_query(pg.HyperParams(**bench.C2), 9, 4) == 312
+    from paper_2312_17241_b200 import decode
+    if "PG_DECODE_CELL_MB" not in os.environ:
+        assert decode.CELL_BUDGET == 96 << 20
