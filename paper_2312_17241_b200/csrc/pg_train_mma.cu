@@ -35,8 +35,12 @@ constexpr int kS = 72;    // row stride (floats) of [feature][sample] tiles and 
                           // feature-indexed GEMMs bank-conflict free
 
 struct SmemW {            // weights: shared by the tile pipelines of a CTA
-    float w0[kI * kS];    // W0 [in f][out i]
-    float w1[kH * kS];    // W1 [in i][out j]
+    // W0 / W1 as their 3xTF32 hi and lo terms (tf32 bit patterns), split once
+    // per CTA instead of at every fragment load: the serialised MLP phases
+    // bound the ping-pong step, so 28 KB less L1 for the encode costs less
+    // than the conversions (C1 0.5247 -> 0.5175 ms)
+    float w0[kI * kS], w0l[kI * kS];
+    float w1[kH * kS], w1l[kH * kS];
     float w2[kH * 8];     // W2 [in k][out j], columns >= od zero
     float b0[kH], b1[kH], b2[8];
 };
@@ -118,6 +122,38 @@ __device__ __forceinline__ void warp_gemm(float (&acc)[NT][4], const float *pa, 
         }
 #pragma unroll
         for (int t = 0; t < NT; ++t) hmma(acc[t], al, bh[t][0], bh[t][1]);  // small terms first
+#pragma unroll
+        for (int t = 0; t < NT; ++t) hmma(acc[t], ah, bl[t][0], bl[t][1]);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) hmma(acc[t], ah, bh[t][0], bh[t][1]);
+    }
+}
+
+// warp_gemm with B given as its pre-split tf32 hi / lo terms (same products,
+// same accumulation order: bit-identical to splitting at the load)
+template <int NT, int K>
+__device__ __forceinline__ void warp_gemm_bs(float (&acc)[NT][4], const float *pa, int am, int ak, int m0,
+                                             const float *pbh, const float *pbl, int bk, int bn, int n0) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
+#pragma unroll 2
+    for (int k0 = 0; k0 < K; k0 += 8) {
+        uint32_t ah[4], al[4];
+        split(pa[(m0 + g) * am + (k0 + c) * ak], ah[0], al[0]);
+        split(pa[(m0 + g + 8) * am + (k0 + c) * ak], ah[1], al[1]);
+        split(pa[(m0 + g) * am + (k0 + c + 4) * ak], ah[2], al[2]);
+        split(pa[(m0 + g + 8) * am + (k0 + c + 4) * ak], ah[3], al[3]);
+        uint32_t bh[NT][2], bl[NT][2];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            const int n = n0 + 8 * t + g;
+            const int o0 = (k0 + c) * bk + n * bn, o1 = (k0 + c + 4) * bk + n * bn;
+            bh[t][0] = __float_as_uint(pbh[o0]);
+            bl[t][0] = __float_as_uint(pbl[o0]);
+            bh[t][1] = __float_as_uint(pbh[o1]);
+            bl[t][1] = __float_as_uint(pbl[o1]);
+        }
+#pragma unroll
+        for (int t = 0; t < NT; ++t) hmma(acc[t], al, bh[t][0], bh[t][1]);
 #pragma unroll
         for (int t = 0; t < NT; ++t) hmma(acc[t], ah, bl[t][0], bl[t][1]);
 #pragma unroll
@@ -287,11 +323,21 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
     {
         const float *p = params;
         const int nt = kNT * NG, t0 = threadIdx.x;
-        for (int i = t0; i < kI * kH; i += nt) W.w0[(i / kH) * kS + i % kH] = p[i];
+        for (int i = t0; i < kI * kH; i += nt) {
+            uint32_t h, l;
+            split(p[i], h, l);
+            W.w0[(i / kH) * kS + i % kH] = __uint_as_float(h);
+            W.w0l[(i / kH) * kS + i % kH] = __uint_as_float(l);
+        }
         p += kI * kH;
         for (int i = t0; i < kH; i += nt) W.b0[i] = p[i];
         p += kH;
-        for (int i = t0; i < kH * kH; i += nt) W.w1[(i / kH) * kS + i % kH] = p[i];
+        for (int i = t0; i < kH * kH; i += nt) {
+            uint32_t h, l;
+            split(p[i], h, l);
+            W.w1[(i / kH) * kS + i % kH] = __uint_as_float(h);
+            W.w1l[(i / kH) * kS + i % kH] = __uint_as_float(l);
+        }
         p += kH * kH;
         for (int i = t0; i < kH; i += nt) W.b1[i] = p[i];
         p += kH;
@@ -377,7 +423,7 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
         // ---- layer 1: h1 = relu(y W0 + b0) ----
         {
             float acc[4][4] = {};
-            warp_gemm<4, kI>(acc, G.y, 1, kS, 16 * mt, W.w0, kS, 1, 32 * (warp >> 2));
+            warp_gemm_bs<4, kI>(acc, G.y, 1, kS, 16 * mt, W.w0, W.w0l, kS, 1, 32 * (warp >> 2));
             store_frags_T<4>(G.h1, acc, 16 * mt, 32 * (warp >> 2), [&](float v, int n, int) {
                 const float z = v + W.b0[n];
                 return z > 0.0f ? z : 0.0f;
@@ -388,7 +434,7 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
         // ---- layer 2: h2 = relu(h1 W1 + b1) ----
         {
             float acc[4][4] = {};
-            warp_gemm<4, kH>(acc, G.h1, 1, kS, 16 * mt, W.w1, kS, 1, 32 * (warp >> 2));
+            warp_gemm_bs<4, kH>(acc, G.h1, 1, kS, 16 * mt, W.w1, W.w1l, kS, 1, 32 * (warp >> 2));
             store_frags_T<4>(G.h2, acc, 16 * mt, 32 * (warp >> 2), [&](float v, int n, int) {
                 const float z = v + W.b1[n];
                 return z > 0.0f ? z : 0.0f;
@@ -465,7 +511,7 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
             warp_gemm<4, kT>(t1, G.h1, kS, 1, 16 * (warp & 3), G.h2, 1, kS, 32 * (warp >> 2));
             tmem_accumulate<16>(tm, &t1[0][0]);
         }
-        warp_gemm<4, kH>(dacc, G.h2, 1, kS, 16 * mt, W.w1, 1, kS, 32 * (warp >> 2));
+        warp_gemm_bs<4, kH>(dacc, G.h2, 1, kS, 16 * mt, W.w1, W.w1l, 1, kS, 32 * (warp >> 2));
         gsync();
         PG_PH(7);
         // delta1 = delta1' * (h1 > 0), in place over h1
@@ -486,7 +532,7 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
                 warp_gemm<2, kT>(t0, G.y, kS, 1, 16 * (warp & 1), G.h1, 1, kS, 16 * (warp >> 1));
                 tmem_accumulate<8>(tm + 16, &t0[0][0]);
             }
-            warp_gemm<2, kH>(yacc, G.h1, 1, kS, 16 * mt, W.w0, 1, kS, 16 * (warp >> 2));
+            warp_gemm_bs<2, kH>(yacc, G.h1, 1, kS, 16 * mt, W.w0, W.w0l, 1, kS, 16 * (warp >> 2));
             PG_PH(9);
             store_frags_T<2>(GDY, yacc, 16 * mt, 16 * (warp >> 2), [](float v, int, int) { return v; });
         }
