@@ -463,8 +463,8 @@ def run_gpu(args, rank, world, local_rank):
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak,
-                     "binding_unit": "L1TEX/LSU random-gather issue (ncu: L1TEX ~80% busy, L2 ~46%, "
-                                     "DRAM ~1%; profiles/r02_*)",
+                     "binding_unit": "L1TEX/LSU random-gather issue and latency (ncu: issue 61%, L1TEX 66%, L2 34%, "
+                                     "DRAM 3%, long-scoreboard stalls on the gathers; profiles/r02_*)",
                      "frac_by_unit": {"hbm": achieved / hbm_peak,
                                       "l2_stream": achieved / l2_stream,
                                       "random_gather_rate": qps / world * gpq / (l2_gather * 1e9 / 8)},
