@@ -31,8 +31,20 @@ constexpr int kH = 64;    // hidden width
 constexpr int kO = 4;     // max output width
 constexpr int kAggRanges = 8;   // warp-aggregate feature reductions up to this many ranges per level
 constexpr int kS = 72;    // row stride (floats) of [feature][sample] tiles and weights:
-                          // 72 = 8 mod 32 makes the A/B fragment loads of the
-                          // feature-indexed GEMMs bank-conflict free
+                          // 72 = 8 mod 32 makes the fragment loads that walk
+                          // rows 4 at a time (c) and columns 8 at a time (g)
+                          // bank-conflict free ...
+// ... and the XOR swizzle (column ^ (row & 4)) makes the transposed walk
+// (rows 8 at a time, columns 4 at a time: the weight-gradient GEMMs, whose K
+// is the sample index, and the W^T data-gradient GEMMs) conflict free too;
+// every access to a [row][column] tile goes through sw()
+__device__ __forceinline__ int sw(int row, int col) {
+#ifdef PG_NO_SWIZZLE
+    return row * kS + col;
+#else
+    return row * kS + (col ^ (row & 4));
+#endif
+}
 
 struct SmemW {            // weights: shared by the tile pipelines of a CTA
     // W0 / W1 as their 3xTF32 hi and lo terms (tf32 bit patterns), split once
@@ -99,17 +111,24 @@ __device__ __forceinline__ void hmma(float (&d)[4], const uint32_t (&a)[4], uint
 // Fragment layouts (PTX mma.m16n8k8 .tf32): g = lane/4, c = lane%4;
 // A: (g, c) (g+8, c) (g, c+4) (g+8, c+4); B: (c, g) (c+4, g);
 // C: (g, 2c) (g, 2c+1) (g+8, 2c) (g+8, 2c+1).
-template <int NT, int K>
+// element (i, j) of an operand with strides (si, sj): a swizzled kS tile
+// (one stride is 1, the other kS) or, SW = false, a plain array
+template <bool SW>
+__device__ __forceinline__ int opnd(int i, int j, int si, int sj) {
+    if constexpr (!SW) return i * si + j * sj;
+    else return si == 1 ? sw(j, i) : sw(i, j);
+}
+template <int NT, int K, bool SWB = true>
 __device__ __forceinline__ void warp_gemm(float (&acc)[NT][4], const float *pa, int am, int ak, int m0,
                                           const float *pb, int bk, int bn, int n0) {
     const int lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
 #pragma unroll 2
     for (int k0 = 0; k0 < K; k0 += 8) {
         uint32_t ah[4], al[4];
-        split(pa[(m0 + g) * am + (k0 + c) * ak], ah[0], al[0]);
-        split(pa[(m0 + g + 8) * am + (k0 + c) * ak], ah[1], al[1]);
-        split(pa[(m0 + g) * am + (k0 + c + 4) * ak], ah[2], al[2]);
-        split(pa[(m0 + g + 8) * am + (k0 + c + 4) * ak], ah[3], al[3]);
+        split(pa[opnd<true>(m0 + g, k0 + c, am, ak)], ah[0], al[0]);
+        split(pa[opnd<true>(m0 + g + 8, k0 + c, am, ak)], ah[1], al[1]);
+        split(pa[opnd<true>(m0 + g, k0 + c + 4, am, ak)], ah[2], al[2]);
+        split(pa[opnd<true>(m0 + g + 8, k0 + c + 4, am, ak)], ah[3], al[3]);
         // term-major issue: NT independent HMMAs between dependent ones
         // (0.5545 -> 0.5521 ms per C1 step vs the three terms of one tile
         // back to back)
@@ -117,8 +136,8 @@ __device__ __forceinline__ void warp_gemm(float (&acc)[NT][4], const float *pa, 
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
             const int n = n0 + 8 * t + g;
-            split(pb[(k0 + c) * bk + n * bn], bh[t][0], bl[t][0]);
-            split(pb[(k0 + c + 4) * bk + n * bn], bh[t][1], bl[t][1]);
+            split(pb[opnd<SWB>(k0 + c, n, bk, bn)], bh[t][0], bl[t][0]);
+            split(pb[opnd<SWB>(k0 + c + 4, n, bk, bn)], bh[t][1], bl[t][1]);
         }
 #pragma unroll
         for (int t = 0; t < NT; ++t) hmma(acc[t], al, bh[t][0], bh[t][1]);  // small terms first
@@ -138,15 +157,15 @@ __device__ __forceinline__ void warp_gemm_bs(float (&acc)[NT][4], const float *p
 #pragma unroll 2
     for (int k0 = 0; k0 < K; k0 += 8) {
         uint32_t ah[4], al[4];
-        split(pa[(m0 + g) * am + (k0 + c) * ak], ah[0], al[0]);
-        split(pa[(m0 + g + 8) * am + (k0 + c) * ak], ah[1], al[1]);
-        split(pa[(m0 + g) * am + (k0 + c + 4) * ak], ah[2], al[2]);
-        split(pa[(m0 + g + 8) * am + (k0 + c + 4) * ak], ah[3], al[3]);
+        split(pa[opnd<true>(m0 + g, k0 + c, am, ak)], ah[0], al[0]);
+        split(pa[opnd<true>(m0 + g + 8, k0 + c, am, ak)], ah[1], al[1]);
+        split(pa[opnd<true>(m0 + g, k0 + c + 4, am, ak)], ah[2], al[2]);
+        split(pa[opnd<true>(m0 + g + 8, k0 + c + 4, am, ak)], ah[3], al[3]);
         uint32_t bh[NT][2], bl[NT][2];
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
             const int n = n0 + 8 * t + g;
-            const int o0 = (k0 + c) * bk + n * bn, o1 = (k0 + c + 4) * bk + n * bn;
+            const int o0 = opnd<true>(k0 + c, n, bk, bn), o1 = opnd<true>(k0 + c + 4, n, bk, bn);
             bh[t][0] = __float_as_uint(pbh[o0]);
             bl[t][0] = __float_as_uint(pbl[o0]);
             bh[t][1] = __float_as_uint(pbh[o1]);
@@ -169,10 +188,10 @@ __device__ __forceinline__ void store_frags_T(float *dstT, const float (&acc)[NT
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
         const int n = n0 + 8 * t + 2 * c;
-        dstT[n * kS + m0 + g] = f(acc[t][0], n, m0 + g);
-        dstT[(n + 1) * kS + m0 + g] = f(acc[t][1], n + 1, m0 + g);
-        dstT[n * kS + m0 + g + 8] = f(acc[t][2], n, m0 + g + 8);
-        dstT[(n + 1) * kS + m0 + g + 8] = f(acc[t][3], n + 1, m0 + g + 8);
+        dstT[sw(n, m0 + g)] = f(acc[t][0], n, m0 + g);
+        dstT[sw(n + 1, m0 + g)] = f(acc[t][1], n + 1, m0 + g);
+        dstT[sw(n, m0 + g + 8)] = f(acc[t][2], n, m0 + g + 8);
+        dstT[sw(n + 1, m0 + g + 8)] = f(acc[t][3], n + 1, m0 + g + 8);
     }
 }
 
@@ -181,7 +200,7 @@ __device__ __forceinline__ void store_frags_T(float *dstT, const float (&acc)[NT
 __device__ __forceinline__ float row_sum4(const float *srcT, int r, int qq) {
     float s = 0.0f;
 #pragma unroll
-    for (int i = 0; i < kT / 4; ++i) s += srcT[r * kS + qq + 4 * i];
+    for (int i = 0; i < kT / 4; ++i) s += srcT[sw(r, qq + 4 * i)];
     s += __shfl_xor_sync(0xffffffffu, s, 1);
     s += __shfl_xor_sync(0xffffffffu, s, 2);
     return s;
@@ -326,8 +345,8 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
         for (int i = t0; i < kI * kH; i += nt) {
             uint32_t h, l;
             split(p[i], h, l);
-            W.w0[(i / kH) * kS + i % kH] = __uint_as_float(h);
-            W.w0l[(i / kH) * kS + i % kH] = __uint_as_float(l);
+            W.w0[sw(i / kH, i % kH)] = __uint_as_float(h);
+            W.w0l[sw(i / kH, i % kH)] = __uint_as_float(l);
         }
         p += kI * kH;
         for (int i = t0; i < kH; i += nt) W.b0[i] = p[i];
@@ -335,8 +354,8 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
         for (int i = t0; i < kH * kH; i += nt) {
             uint32_t h, l;
             split(p[i], h, l);
-            W.w1[(i / kH) * kS + i % kH] = __uint_as_float(h);
-            W.w1l[(i / kH) * kS + i % kH] = __uint_as_float(l);
+            W.w1[sw(i / kH, i % kH)] = __uint_as_float(h);
+            W.w1l[sw(i / kH, i % kH)] = __uint_as_float(l);
         }
         p += kH * kH;
         for (int i = t0; i < kH; i += nt) W.b1[i] = p[i];
@@ -402,8 +421,8 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
             const int l = lsub + 4 * it;
             const float2 yv = cmap.off[l] >= 0 ? encode_level_fwd2_cell32<D>(g, l, x, cmap.cells + cmap.off[l])
                                                : encode_level_fwd2_rng<FT, D>(g, l, x, feats_fwd, baked);
-            G.y[(2 * l) * kS + pl] = yv.x;
-            G.y[(2 * l + 1) * kS + pl] = yv.y;
+            G.y[sw(2 * l, pl)] = yv.x;
+            G.y[sw(2 * l + 1, pl)] = yv.y;
         }
     }
     for (int64_t iter = 0; iter < n_iter; ++iter) {
@@ -445,7 +464,7 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
         // ---- output layer, loss, dL/dout (warps 0-3: one 16-sample tile each) ----
         if (warp < 4) {
             float acc[1][4] = {};
-            warp_gemm<1, kH>(acc, G.h2, 1, kS, 16 * warp, W.w2, 8, 1, 0);
+            warp_gemm<1, kH, false>(acc, G.h2, 1, kS, 16 * warp, W.w2, 8, 1, 0);
             const int gq = lane >> 2, c = lane & 3;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -473,7 +492,7 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
         // ---- dW2 += h2^T d3 (warps 0-3), db2; delta2 = (d3 W2^T) * (h2 > 0) ----
         if (warp < 4) {
             float t2[1][4] = {};
-            warp_gemm<1, kT>(t2, G.h2, kS, 1, 16 * warp, G.d3, 8, 1, 0);
+            warp_gemm<1, kT, false>(t2, G.h2, kS, 1, 16 * warp, G.d3, 8, 1, 0);
             tmem_accumulate<4>(tm + 24, &t2[0][0]);
         }
         if (tid < 8) {
@@ -491,12 +510,12 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
                 const int k = k0 + u;
                 const float4 w = *reinterpret_cast<const float4 *>(W.w2 + k * 8);
                 const float s = dq.x * w.x + dq.y * w.y + dq.z * w.z + dq.w * w.w;
-                dl[u] = G.h2[k * kS + q] > 0.0f ? s : 0.0f;
+                dl[u] = G.h2[sw(k, q)] > 0.0f ? s : 0.0f;
             }
             gsync();  // dW2 reads h2 above
             PG_PH(5);
 #pragma unroll
-            for (int u = 0; u < 16; ++u) G.h2[(k0 + u) * kS + q] = dl[u];
+            for (int u = 0; u < 16; ++u) G.h2[sw(k0 + u, q)] = dl[u];
         }
         gsync();
         PG_PH(6);
@@ -516,7 +535,7 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
         PG_PH(7);
         // delta1 = delta1' * (h1 > 0), in place over h1
         store_frags_T<4>(G.h1, dacc, 16 * mt, 32 * (warp >> 2), [&](float v, int n, int m) {
-            return G.h1[n * kS + m] > 0.0f ? v : 0.0f;
+            return G.h1[sw(n, m)] > 0.0f ? v : 0.0f;
         });
         gsync();
         PG_PH(8);
@@ -541,7 +560,7 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
         if (dy_out) {
             for (int i = tid; i < nv * kI; i += kNT) {
                 const int q = i / kI, c = i % kI;
-                dy_out[(p0 + q) * kI + c] = GDY[c * kS + q];
+                dy_out[(p0 + q) * kI + c] = GDY[sw(c, q)];
             }
         }
         // ---- stage the next tile's inputs (prefetched into registers) ----
@@ -568,18 +587,18 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
                 // levels in the step's cell cache: one 32-byte record load
                 const float2 yv = cmap.off[l] >= 0 ? encode_level_fwd2_cell32<D>(g, l, xn, cmap.cells + cmap.off[l])
                                                    : encode_level_fwd2_rng<FT, D>(g, l, xn, feats_fwd, baked);
-                G.y[(2 * l) * kS + pl] = yv.x;
-                G.y[(2 * l + 1) * kS + pl] = yv.y;
+                G.y[sw(2 * l, pl)] = yv.x;
+                G.y[sw(2 * l + 1, pl)] = yv.y;
             }
             constexpr bool lazy = std::is_same<ACC, float>::value;
             if constexpr (AGG) {
                 // every lane of the warp takes part (the shuffles); lanes past
                 // the batch end contribute nothing
-                encode_level_bwd2<D, NPM, ACC, lazy, true>(g, l, x, GDY[(2 * l) * kS + pl],
-                                                           GDY[(2 * l + 1) * kS + pl], feats, conf, gfeat_cta, gconf,
+                encode_level_bwd2<D, NPM, ACC, lazy, true>(g, l, x, GDY[sw(2 * l, pl)],
+                                                           GDY[sw(2 * l + 1, pl)], feats, conf, gfeat_cta, gconf,
                                                            touched, touch_all, pl < nv);
             } else if (pl < nv) {
-                encode_level_bwd2<D, NPM, ACC, lazy>(g, l, x, GDY[(2 * l) * kS + pl], GDY[(2 * l + 1) * kS + pl],
+                encode_level_bwd2<D, NPM, ACC, lazy>(g, l, x, GDY[sw(2 * l, pl)], GDY[sw(2 * l + 1, pl)],
                                                      feats, conf, gfeat_cta, gconf, touched, touch_all);
             }
         }
