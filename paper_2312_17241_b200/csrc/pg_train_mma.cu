@@ -89,14 +89,29 @@ __device__ __forceinline__ void tmem_accumulate(uint32_t taddr, const float *acc
     else umma::tmem_st4(taddr, v);
 }
 
+// cvt.rn.tf32.f32 is one F2FP.TF32 instruction on sm_100a; cvt.rna (ties
+// away) is a three-instruction software sequence (FSETP, IADD, LOP3), and
+// the 3xTF32 splits are most of the MLP phase's non-MMA instructions
+// (tools/micro/tf32_cvt_check.cu checks the .rn result is a clean,
+// round-to-nearest-even tf32): C1 step 0.510 -> 0.483 ms
 __device__ __forceinline__ uint32_t to_tf32(float x) {
     uint32_t r;
+#ifdef PG_TF32_RNA
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+#else
+    asm("cvt.rn.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+#endif
     return r;
 }
 __device__ __forceinline__ void split(float x, uint32_t &hi, uint32_t &lo) {
     hi = to_tf32(x);
+#ifndef PG_TF32_LO_RND
+    // lo unrounded: the MMA reads its upper 19 bits (truncation: <= 2^-21
+    // relative to x, as the decode's split); C1 0.483 -> 0.479 ms
+    lo = __float_as_uint(__fsub_rn(x, __uint_as_float(hi)));
+#else
     lo = to_tf32(__fsub_rn(x, __uint_as_float(hi)));
+#endif
 }
 __device__ __forceinline__ void hmma(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
     asm volatile(

@@ -156,11 +156,15 @@ PG_TMEM_LDST(16, PG_O16, PG_I16, "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13
 #undef PG_TMEM_LDST
 
 // fp32 -> (hi, lo) with hi exactly representable in tf32 (round to nearest
-// on the 10-bit mantissa) and lo = x - hi (exact), itself rounded to tf32 by
+// even on the 10-bit mantissa) and lo = x - hi (exact), itself rounded to tf32 by
 // the MMA: hi*w + lo*w carries ~22 significand bits of x.
 __device__ __forceinline__ void split_tf32(float x, float &hi, float &lo) {
     uint32_t h;
+#ifdef PG_TF32_RNA
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+#else
+    asm("cvt.rn.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));   // one F2FP.TF32 (.rna: three instructions)
+#endif
     hi = __uint_as_float(h);
     lo = __fsub_rn(x, hi);
 }
