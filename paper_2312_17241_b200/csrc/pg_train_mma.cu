@@ -38,13 +38,7 @@ constexpr int kS = 72;    // row stride (floats) of [feature][sample] tiles and 
 // (rows 8 at a time, columns 4 at a time: the weight-gradient GEMMs, whose K
 // is the sample index, and the W^T data-gradient GEMMs) conflict free too;
 // every access to a [row][column] tile goes through sw()
-__device__ __forceinline__ int sw(int row, int col) {
-#ifdef PG_NO_SWIZZLE
-    return row * kS + col;
-#else
-    return row * kS + (col ^ (row & 4));
-#endif
-}
+__device__ __forceinline__ int sw(int row, int col) { return row * kS + (col ^ (row & 4)); }
 
 struct SmemW {            // weights: shared by the tile pipelines of a CTA
     // W0 / W1 as their 3xTF32 hi and lo terms (tf32 bit patterns), split once
@@ -126,33 +120,72 @@ __device__ __forceinline__ void hmma(float (&d)[4], const uint32_t (&a)[4], uint
 // Fragment layouts (PTX mma.m16n8k8 .tf32): g = lane/4, c = lane%4;
 // A: (g, c) (g+8, c) (g, c+4) (g+8, c+4); B: (c, g) (c+4, g);
 // C: (g, 2c) (g, 2c+1) (g+8, 2c) (g+8, 2c+1).
-// element (i, j) of an operand with strides (si, sj): a swizzled kS tile
-// (one stride is 1, the other kS) or, SW = false, a plain array
+// Per-lane fragment offsets, hoisted out of the K loop: element k0 + ... of
+// the fragment sits at o[i] + k0 * ks (+ t * ts for B's n-tile t).  Operands
+// are swizzled kS tiles (one stride 1, the other kS; m0, n0, k0 multiples of
+// 8, so the swizzle reduces to lane-constant XORs) or, SW = false, plain
+// arrays.  Same addresses as sw() element by element.
+struct FragA { int o[4], ks; };
+__device__ __forceinline__ FragA frag_a(int am, int m0, int g, int c) {
+    FragA f;
+    if (am == 1) {          // [k][m] tile: rows k0+c, k0+c+4; columns m0+g, m0+g+8
+        f.o[0] = c * kS + m0 + g;
+        f.o[2] = (c + 4) * kS + m0 + (g ^ 4);
+        f.o[1] = f.o[0] + 8;
+        f.o[3] = f.o[2] + 8;
+        f.ks = kS;
+    } else {                // [m][k] tile: rows m0+g, m0+g+8; columns k0+c, k0+c+4
+        const int s = g & 4;
+        f.o[0] = (m0 + g) * kS + (c ^ s);
+        f.o[2] = (m0 + g) * kS + ((c + 4) ^ s);
+        f.o[1] = f.o[0] + 8 * kS;
+        f.o[3] = f.o[2] + 8 * kS;
+        f.ks = 1;
+    }
+    return f;
+}
+struct FragB { int o[2], ks, ts; };
 template <bool SW>
-__device__ __forceinline__ int opnd(int i, int j, int si, int sj) {
-    if constexpr (!SW) return i * si + j * sj;
-    else return si == 1 ? sw(j, i) : sw(i, j);
+__device__ __forceinline__ FragB frag_b(int bk, int bn, int n0, int g, int c) {
+    FragB f;
+    if constexpr (!SW) {
+        f.o[0] = c * bk + (n0 + g) * bn;
+        f.o[1] = (c + 4) * bk + (n0 + g) * bn;
+        f.ks = bk;
+        f.ts = 8 * bn;
+    } else if (bn == 1) {   // [k][n] tile
+        f.o[0] = c * kS + n0 + g;
+        f.o[1] = (c + 4) * kS + n0 + (g ^ 4);
+        f.ks = kS;
+        f.ts = 8;
+    } else {                // [n][k] tile
+        const int s = g & 4;
+        f.o[0] = (n0 + g) * kS + (c ^ s);
+        f.o[1] = (n0 + g) * kS + ((c + 4) ^ s);
+        f.ks = 1;
+        f.ts = 8 * kS;
+    }
+    return f;
 }
 template <int NT, int K, bool SWB = true>
 __device__ __forceinline__ void warp_gemm(float (&acc)[NT][4], const float *pa, int am, int ak, int m0,
                                           const float *pb, int bk, int bn, int n0) {
     const int lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
+    const FragA fa = frag_a(am, m0, g, c);
+    const FragB fb = frag_b<SWB>(bk, bn, n0, g, c);
 #pragma unroll 2
     for (int k0 = 0; k0 < K; k0 += 8) {
         uint32_t ah[4], al[4];
-        split(pa[opnd<true>(m0 + g, k0 + c, am, ak)], ah[0], al[0]);
-        split(pa[opnd<true>(m0 + g + 8, k0 + c, am, ak)], ah[1], al[1]);
-        split(pa[opnd<true>(m0 + g, k0 + c + 4, am, ak)], ah[2], al[2]);
-        split(pa[opnd<true>(m0 + g + 8, k0 + c + 4, am, ak)], ah[3], al[3]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) split(pa[fa.o[i] + k0 * fa.ks], ah[i], al[i]);
         // term-major issue: NT independent HMMAs between dependent ones
         // (0.5545 -> 0.5521 ms per C1 step vs the three terms of one tile
         // back to back)
         uint32_t bh[NT][2], bl[NT][2];
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
-            const int n = n0 + 8 * t + g;
-            split(pb[opnd<SWB>(k0 + c, n, bk, bn)], bh[t][0], bl[t][0]);
-            split(pb[opnd<SWB>(k0 + c + 4, n, bk, bn)], bh[t][1], bl[t][1]);
+            split(pb[fb.o[0] + k0 * fb.ks + t * fb.ts], bh[t][0], bl[t][0]);
+            split(pb[fb.o[1] + k0 * fb.ks + t * fb.ts], bh[t][1], bl[t][1]);
         }
 #pragma unroll
         for (int t = 0; t < NT; ++t) hmma(acc[t], al, bh[t][0], bh[t][1]);  // small terms first
@@ -169,18 +202,17 @@ template <int NT, int K>
 __device__ __forceinline__ void warp_gemm_bs(float (&acc)[NT][4], const float *pa, int am, int ak, int m0,
                                              const float *pbh, const float *pbl, int bk, int bn, int n0) {
     const int lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
+    const FragA fa = frag_a(am, m0, g, c);
+    const FragB fb = frag_b<true>(bk, bn, n0, g, c);
 #pragma unroll 2
     for (int k0 = 0; k0 < K; k0 += 8) {
         uint32_t ah[4], al[4];
-        split(pa[opnd<true>(m0 + g, k0 + c, am, ak)], ah[0], al[0]);
-        split(pa[opnd<true>(m0 + g + 8, k0 + c, am, ak)], ah[1], al[1]);
-        split(pa[opnd<true>(m0 + g, k0 + c + 4, am, ak)], ah[2], al[2]);
-        split(pa[opnd<true>(m0 + g + 8, k0 + c + 4, am, ak)], ah[3], al[3]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) split(pa[fa.o[i] + k0 * fa.ks], ah[i], al[i]);
         uint32_t bh[NT][2], bl[NT][2];
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
-            const int n = n0 + 8 * t + g;
-            const int o0 = opnd<true>(k0 + c, n, bk, bn), o1 = opnd<true>(k0 + c + 4, n, bk, bn);
+            const int o0 = fb.o[0] + k0 * fb.ks + t * fb.ts, o1 = fb.o[1] + k0 * fb.ks + t * fb.ts;
             bh[t][0] = __float_as_uint(pbh[o0]);
             bl[t][0] = __float_as_uint(pbl[o0]);
             bh[t][1] = __float_as_uint(pbh[o1]);
