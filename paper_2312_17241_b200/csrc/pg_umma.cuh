@@ -75,6 +75,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t parity) {
         : "memory");
 }
 
+// ReLU that propagates NaN like numpy's maximum(x, 0): one FMNMX.NAN
+// (the x < 0 ? 0 : x select is two instructions)
+__device__ __forceinline__ float relu_nan(float x) {
+    float r;
+    asm("max.NaN.f32 %0, %1, 0f00000000;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // generic-proxy smem writes -> visible to the tensor core (async proxy)
 __device__ __forceinline__ void fence_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
