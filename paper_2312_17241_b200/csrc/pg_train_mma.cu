@@ -584,9 +584,9 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
         {
             float t1[4][4] = {};
             warp_gemm<4, kT>(t1, G.h1, kS, 1, 16 * (warp & 3), G.h2, 1, kS, 32 * (warp >> 2));
-            tmem_accumulate<16>(tm, &t1[0][0]);
+            warp_gemm_bs<4, kH>(dacc, G.h2, 1, kS, 16 * mt, W.w1, W.w1l, 1, kS, 32 * (warp >> 2));
+            tmem_accumulate<16>(tm, &t1[0][0]);   // after the independent GEMM: they interleave
         }
-        warp_gemm_bs<4, kH>(dacc, G.h2, 1, kS, 16 * mt, W.w1, W.w1l, 1, kS, 32 * (warp >> 2));
         gsync();
         PG_PH(7);
         // delta1 = delta1' * (h1 > 0), in place over h1
@@ -605,9 +605,9 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
             {
                 float t0[2][4] = {};
                 warp_gemm<2, kT>(t0, G.y, kS, 1, 16 * (warp & 1), G.h1, 1, kS, 16 * (warp >> 1));
+                warp_gemm_bs<2, kH>(yacc, G.h1, 1, kS, 16 * mt, W.w0, W.w0l, 1, kS, 16 * (warp >> 2));
                 tmem_accumulate<8>(tm + 16, &t0[0][0]);
             }
-            warp_gemm_bs<2, kH>(yacc, G.h1, 1, kS, 16 * mt, W.w0, W.w0l, 1, kS, 16 * (warp >> 2));
             PG_PH(9);
             store_frags_T<2>(GDY, yacc, 16 * mt, 16 * (warp >> 2), [](float v, int, int) { return v; });
         }
