@@ -7,6 +7,12 @@
 #include "pg_common.cuh"
 
 namespace pg {
+// 2^x by the SFU (MUFU.EX2; x <= 0 here, so no overflow handling needed)
+__device__ __forceinline__ float exp2f_approx(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 
 // 256-bit read-only global load (sm_100: LDG.E.ENL2.256); p 32-byte aligned
 __device__ __forceinline__ void ld_nc_v8(const float *p, float (&v)[8]) {
@@ -395,20 +401,32 @@ __device__ __forceinline__ void encode_level_bwd2(const pg_grid &g, int l, const
 #pragma unroll
             for (int j = 1; j < NPMAX; ++j)
                 if (j < n_p) mx = fmaxf(mx, cv[u][j]);
+            // AGG (the fast fp32 step): exp as one ex2.approx of a scaled
+            // argument and one reciprocal instead of n_p IEEE divisions
+            // (relative error ~1e-6 on the probe weights, inside the 1e-5
+            // gradient bars; the parity-mode kernels keep the reference's
+            // expf and division)
+#ifndef PG_SM_EXACT
+            constexpr bool kFastSm = AGG;
+#else
+            constexpr bool kFastSm = false;
+#endif
             float sum = 0.0f;
 #pragma unroll
             for (int j = 0; j < NPMAX; ++j)
                 if (j < n_p) {
-                    sg[j] = expf(cv[u][j] - mx);
+                    sg[j] = kFastSm ? exp2f_approx(__fmul_rn(cv[u][j] - mx, 1.4426950408889634f))
+                                    : expf(cv[u][j] - mx);
                     sum += sg[j];
                 }
+            const float inv = kFastSm ? __frcp_rn(sum) : 0.0f;
             // the reference's rounding: z /= sums (numpy_backend.py:128-130);
             // dot = f0*g0 + f1*g1 and s += sj*dot without FMA (_core.pyx:196-201)
             float s = 0.0f;
 #pragma unroll
             for (int j = 0; j < NPMAX; ++j)
                 if (j < n_p) {
-                    sg[j] = __fdiv_rn(sg[j], sum);
+                    sg[j] = kFastSm ? __fmul_rn(sg[j], inv) : __fdiv_rn(sg[j], sum);
                     dots[j] = __fadd_rn(__fmul_rn(fv[u][j][0], g0), __fmul_rn(fv[u][j][1], g1));
                     s = __fadd_rn(s, __fmul_rn(sg[j], dots[j]));
                 }

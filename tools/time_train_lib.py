@@ -16,7 +16,9 @@ _lib._LIB = _lib.load(sys.argv[1])
 import paper_2312_17241_b200 as pg  # noqa: E402
 from tests.golden_util import smooth_image  # noqa: E402
 
-st = pg.TrainState(pg.init_model(pg.HyperParams(n_f=2**12, n_c=2**14, n_p=4), seed=0),
+import json  # noqa: E402
+KW = json.loads(os.environ.get("CFG", '{"n_f": 4096, "n_c": 16384, "n_p": 4}'))   # default: C1
+st = pg.TrainState(pg.init_model(pg.HyperParams(**KW), seed=0),
                    smooth_image(256, 256), pg.TrainConfig(batch_size=1 << 18, seed=0), sampler="device")
 for _ in range(5):
     st.launch_step()
