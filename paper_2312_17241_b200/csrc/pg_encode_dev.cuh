@@ -401,13 +401,13 @@ __device__ __forceinline__ void encode_level_bwd2(const pg_grid &g, int l, const
 #pragma unroll
             for (int j = 1; j < NPMAX; ++j)
                 if (j < n_p) mx = fmaxf(mx, cv[u][j]);
-            // AGG (the fast fp32 step): exp as one ex2.approx of a scaled
+            // LAZY (the fast fp32 step): exp as one ex2.approx of a scaled
             // argument and one reciprocal instead of n_p IEEE divisions
             // (relative error ~1e-6 on the probe weights, inside the 1e-5
             // gradient bars; the parity-mode kernels keep the reference's
             // expf and division)
 #ifndef PG_SM_EXACT
-            constexpr bool kFastSm = AGG;
+            constexpr bool kFastSm = LAZY;
 #else
             constexpr bool kFastSm = false;
 #endif

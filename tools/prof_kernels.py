@@ -8,6 +8,7 @@ launches so `ncu --set full` replays stay short.  Numbers printed here are
 never bench values (they may run under a profiler)."""
 
 import argparse
+import json
 import os
 import sys
 
@@ -28,6 +29,7 @@ def main():
     ap.add_argument("--n", type=int, default=3)
     ap.add_argument("--exact", action="store_true")
     ap.add_argument("--bq", type=int, default=1 << 24)
+    ap.add_argument("--train-cfg", default=None, help="HyperParams kwargs as JSON (default: bench.C1)")
     args = ap.parse_args()
     if args.what in ("decode", "all"):
         _, inf = bench.inference_model(pg, pg.HyperParams(**bench.C2))
@@ -39,7 +41,8 @@ def main():
         print("decode ok", float(out[:4].sum()))
     if args.what in ("train", "all"):
         from tests.golden_util import smooth_image
-        st = pg.TrainState(pg.init_model(pg.HyperParams(**bench.C1)), smooth_image(),
+        kw = json.loads(args.train_cfg) if args.train_cfg else bench.C1
+        st = pg.TrainState(pg.init_model(pg.HyperParams(**kw)), smooth_image(),
                            pg.TrainConfig(batch_size=bench.B_TRAIN, seed=0), sampler="device")
         for _ in range(args.n):
             st.launch_step()
