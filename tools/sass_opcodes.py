@@ -12,7 +12,7 @@ import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KEYS = ["UTCHMMA", "UTCMMA", "UTCBAR", "LDTM", "STTM", "HMMA", "FFMA", "FFMA2", "FMUL", "FADD",
-        "LDG", "STG", "RED", "ATOMG", "LDS", "STS", "SYNCS", "BAR", "UTMALDG", "UBLKCP"]
+        "LDG", "STG", "RED", "ATOMG", "LDS", "STS", "SYNCS", "BAR", "UTMALDG", "UBLKCP", "F2FP", "FMNMX"]
 WATCH = ["decode_umma_kernel", "train_mma_kernel", "train_fused_kernel", "decode_fused_kernel",
          "encode_fwd_kernel", "encode_bwd_kernel", "lazy_adam_rebake_kernel", "adam_kernel",
          "umma_selftest_kernel", "probe_stream_kernel", "probe_gather_kernel"]
