@@ -41,12 +41,18 @@ constexpr int kS = 72;    // row stride (floats) of [feature][sample] tiles and 
 __device__ __forceinline__ int sw(int row, int col) { return row * kS + (col ^ (row & 4)); }
 
 struct SmemW {            // weights: shared by the tile pipelines of a CTA
-    // W0 / W1 as their 3xTF32 hi and lo terms (tf32 bit patterns), split once
-    // per CTA instead of at every fragment load: the serialised MLP phases
-    // bound the ping-pong step, so 28 KB less L1 for the encode costs less
-    // than the conversions (C1 0.5247 -> 0.5175 ms)
+    // W0 / W1 in fp32, split into their 3xTF32 terms at the fragment load.
+    // PG_W_PRESPLIT keeps hi and lo copies instead (split once per CTA): that
+    // won while a split cost three instructions (cvt.rna; C1 0.5247 ->
+    // 0.5175 ms), and loses now that it is one F2FP and L1TEX is the busiest
+    // unit (twice the weight wavefronts, 28 KB less L1: 0.4516 vs 0.4435 ms)
+#ifdef PG_W_PRESPLIT
     float w0[kI * kS], w0l[kI * kS];
     float w1[kH * kS], w1l[kH * kS];
+#else
+    float w0[kI * kS];
+    float w1[kH * kS];
+#endif
     float w2[kH * 8];     // W2 [in k][out j], columns >= od zero
     float b0[kH], b1[kH], b2[8];
 };
@@ -236,6 +242,15 @@ PG_GEMM_UNROLL_PRAGMA
     }
 }
 
+// GEMM with a weight operand: pre-split hi/lo copies (PG_W_PRESPLIT) or
+// one fp32 copy split at the fragment load
+#ifdef PG_W_PRESPLIT
+#define PG_WGEMM(NT, K, acc, pa, am, ak, m0, wh, wl, bk, bn, n0) \
+    warp_gemm_bs<NT, K>(acc, pa, am, ak, m0, wh, wl, bk, bn, n0)
+#else
+#define PG_WGEMM(NT, K, acc, pa, am, ak, m0, wh, wl, bk, bn, n0) warp_gemm<NT, K>(acc, pa, am, ak, m0, wh, bk, bn, n0)
+#endif
+
 // store a warp's C fragments (rows = samples m, columns = features n) into a
 // [feature][sample] tile, optionally through f(value, feature, sample)
 template <int NT, typename F>
@@ -399,19 +414,27 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
         const float *p = params;
         const int nt = kNT * NG, t0 = threadIdx.x;
         for (int i = t0; i < kI * kH; i += nt) {
+#ifdef PG_W_PRESPLIT
             uint32_t h, l;
             split(p[i], h, l);
             W.w0[sw(i / kH, i % kH)] = __uint_as_float(h);
             W.w0l[sw(i / kH, i % kH)] = __uint_as_float(l);
+#else
+            W.w0[sw(i / kH, i % kH)] = p[i];
+#endif
         }
         p += kI * kH;
         for (int i = t0; i < kH; i += nt) W.b0[i] = p[i];
         p += kH;
         for (int i = t0; i < kH * kH; i += nt) {
+#ifdef PG_W_PRESPLIT
             uint32_t h, l;
             split(p[i], h, l);
             W.w1[sw(i / kH, i % kH)] = __uint_as_float(h);
             W.w1l[sw(i / kH, i % kH)] = __uint_as_float(l);
+#else
+            W.w1[sw(i / kH, i % kH)] = p[i];
+#endif
         }
         p += kH * kH;
         for (int i = t0; i < kH; i += nt) W.b1[i] = p[i];
@@ -498,7 +521,7 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
         // ---- layer 1: h1 = relu(y W0 + b0) ----
         {
             float acc[4][4] = {};
-            warp_gemm_bs<4, kI>(acc, G.y, 1, kS, 16 * mt, W.w0, W.w0l, kS, 1, 32 * (warp >> 2));
+            PG_WGEMM(4, kI, acc, G.y, 1, kS, 16 * mt, W.w0, W.w0l, kS, 1, 32 * (warp >> 2));
             store_frags_T<4>(G.h1, acc, 16 * mt, 32 * (warp >> 2), [&](float v, int n, int) {
                 const float z = v + W.b0[n];
                 return z > 0.0f ? z : 0.0f;
@@ -509,7 +532,7 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
         // ---- layer 2: h2 = relu(h1 W1 + b1) ----
         {
             float acc[4][4] = {};
-            warp_gemm_bs<4, kH>(acc, G.h1, 1, kS, 16 * mt, W.w1, W.w1l, kS, 1, 32 * (warp >> 2));
+            PG_WGEMM(4, kH, acc, G.h1, 1, kS, 16 * mt, W.w1, W.w1l, kS, 1, 32 * (warp >> 2));
             store_frags_T<4>(G.h2, acc, 16 * mt, 32 * (warp >> 2), [&](float v, int n, int) {
                 const float z = v + W.b1[n];
                 return z > 0.0f ? z : 0.0f;
@@ -584,7 +607,7 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
         {
             float t1[4][4] = {};
             warp_gemm<4, kT>(t1, G.h1, kS, 1, 16 * (warp & 3), G.h2, 1, kS, 32 * (warp >> 2));
-            warp_gemm_bs<4, kH>(dacc, G.h2, 1, kS, 16 * mt, W.w1, W.w1l, 1, kS, 32 * (warp >> 2));
+            PG_WGEMM(4, kH, dacc, G.h2, 1, kS, 16 * mt, W.w1, W.w1l, 1, kS, 32 * (warp >> 2));
             tmem_accumulate<16>(tm, &t1[0][0]);   // after the independent GEMM: they interleave
         }
         gsync();
@@ -605,7 +628,7 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
             {
                 float t0[2][4] = {};
                 warp_gemm<2, kT>(t0, G.y, kS, 1, 16 * (warp & 1), G.h1, 1, kS, 16 * (warp >> 1));
-                warp_gemm_bs<2, kH>(yacc, G.h1, 1, kS, 16 * mt, W.w0, W.w0l, 1, kS, 16 * (warp >> 2));
+                PG_WGEMM(2, kH, yacc, G.h1, 1, kS, 16 * mt, W.w0, W.w0l, 1, kS, 16 * (warp >> 2));
                 tmem_accumulate<8>(tm + 16, &t0[0][0]);
             }
             PG_PH(9);

@@ -1,3 +1,4 @@
-CFG='{"n_f":256,"n_c":4096,"n_p":16}' bash tools/gpu_ab_vars.sh
-CFG='{"n_f":4096,"n_c":16384,"n_p":4}' bash tools/gpu_ab_vars.sh
-python -m pytest tests/test_gpu_parity.py -q -x -k "train or grad or step or fused" 2>&1 | tail -2
+python tools/train_bitcheck.py tools/_var_presplit/lib.so gpurun_out/bc_base.npz
+python tools/train_bitcheck.py paper_2312_17241_b200/libprobegrid_b200.so gpurun_out/bc_new.npz gpurun_out/bc_base.npz
+bash tools/gpu_ab_vars.sh
+CFG='{}' bash tools/gpu_ab_vars.sh
