@@ -34,11 +34,13 @@ constexpr int kS = 72;    // row stride (floats) of [feature][sample] tiles and 
                           // 72 = 8 mod 32 makes the fragment loads that walk
                           // rows 4 at a time (c) and columns 8 at a time (g)
                           // bank-conflict free ...
-// ... and the XOR swizzle (column ^ (row & 4)) makes the transposed walk
-// (rows 8 at a time, columns 4 at a time: the weight-gradient GEMMs, whose K
-// is the sample index, and the W^T data-gradient GEMMs) conflict free too;
-// every access to a [row][column] tile goes through sw()
-__device__ __forceinline__ int sw(int row, int col) { return row * kS + (col ^ (row & 4)); }
+// ... and the XOR swizzle (column ^ 12 in rows with bit 2 set) makes the
+// transposed walk (rows 8 at a time, columns 4 at a time: the weight-gradient
+// GEMMs, whose K is the sample index, and the W^T data-gradient GEMMs) and
+// the C-fragment stores (rows 2c, columns g) conflict free too (^4 left the
+// stores 2-way conflicted); every access to a [row][column] tile goes
+// through sw()
+__device__ __forceinline__ int sw(int row, int col) { return row * kS + (col ^ ((row & 4) * 3)); }
 
 struct SmemW {            // weights: shared by the tile pipelines of a CTA
     // W0 / W1 in fp32, split into their 3xTF32 terms at the fragment load.
@@ -140,43 +142,69 @@ __device__ __forceinline__ void hmma(float (&d)[4], const uint32_t (&a)[4], uint
 #define PG_STR_(x) #x
 #define PG_UNROLL_(n) _Pragma(PG_STR_(unroll n))
 #define PG_GEMM_UNROLL_PRAGMA PG_UNROLL_(PG_GEMM_UNROLL)
-struct FragA { int o[4], ks; };
+// o[kp][i]: element i at k0 = kp * 8 (k0 & 8 selects kp; the rest of k0
+// adds (k0 & ~15) * ks: the swizzle flips column bits 2-3, so offsets are
+// lane-constant per 16-column group)
+struct FragA { int o[2][4], ks; };
 __device__ __forceinline__ FragA frag_a(int am, int m0, int g, int c) {
     FragA f;
-    if (am == 1) {          // [k][m] tile: rows k0+c, k0+c+4; columns m0+g, m0+g+8
-        f.o[0] = c * kS + m0 + g;
-        f.o[2] = (c + 4) * kS + m0 + (g ^ 4);
-        f.o[1] = f.o[0] + 8;
-        f.o[3] = f.o[2] + 8;
+    if (am == 1) {          // [k][m] tile: rows k0+c (unswizzled), k0+c+4 (^12); columns m0+g, m0+g+8
+        f.o[0][0] = c * kS + m0 + g;
+        f.o[0][1] = c * kS + m0 + 8 + g;
+        f.o[0][2] = (c + 4) * kS + m0 + (g ^ 12);
+        f.o[0][3] = (c + 4) * kS + m0 + (g ^ 4);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) f.o[1][i] = f.o[0][i] + 8 * kS;
         f.ks = kS;
-    } else {                // [m][k] tile: rows m0+g, m0+g+8; columns k0+c, k0+c+4
-        const int s = g & 4;
-        f.o[0] = (m0 + g) * kS + (c ^ s);
-        f.o[2] = (m0 + g) * kS + ((c + 4) ^ s);
-        f.o[1] = f.o[0] + 8 * kS;
-        f.o[3] = f.o[2] + 8 * kS;
+    } else {                // [m][k] tile: rows m0+g, m0+g+8 (swizzle s); columns k0+c, k0+c+4
+        const int s = (g & 4) * 3, r0 = (m0 + g) * kS, r1 = r0 + 8 * kS;
+        f.o[0][0] = r0 + (c ^ s);
+        f.o[0][1] = r1 + (c ^ s);
+        f.o[0][2] = r0 + ((c + 4) ^ s);
+        f.o[0][3] = r1 + ((c + 4) ^ s);
+        f.o[1][0] = r0 + ((c + 8) ^ s);
+        f.o[1][1] = r1 + ((c + 8) ^ s);
+        f.o[1][2] = r0 + ((c + 12) ^ s);
+        f.o[1][3] = r1 + ((c + 12) ^ s);
         f.ks = 1;
     }
     return f;
 }
-struct FragB { int o[2], ks, ts; };
+// o[kp][tp][j]: element j of n-tile t at k0 = kp * 8, t = tp; add
+// (k0 & ~15) * ks + (t & ~1) * ts
+struct FragB { int o[2][2][2], ks, ts; };
 template <bool SW>
 __device__ __forceinline__ FragB frag_b(int bk, int bn, int n0, int g, int c) {
     FragB f;
     if constexpr (!SW) {
-        f.o[0] = c * bk + (n0 + g) * bn;
-        f.o[1] = (c + 4) * bk + (n0 + g) * bn;
+#pragma unroll
+        for (int kp = 0; kp < 2; ++kp)
+#pragma unroll
+            for (int tp = 0; tp < 2; ++tp) {
+                f.o[kp][tp][0] = (8 * kp + c) * bk + (n0 + 8 * tp + g) * bn;
+                f.o[kp][tp][1] = (8 * kp + c + 4) * bk + (n0 + 8 * tp + g) * bn;
+            }
         f.ks = bk;
         f.ts = 8 * bn;
-    } else if (bn == 1) {   // [k][n] tile
-        f.o[0] = c * kS + n0 + g;
-        f.o[1] = (c + 4) * kS + n0 + (g ^ 4);
+    } else if (bn == 1) {   // [k][n] tile: rows k0+c, k0+c+4 (^12); columns n0+8t+g (n0 % 16 == 0)
+#pragma unroll
+        for (int kp = 0; kp < 2; ++kp) {
+            f.o[kp][0][0] = (8 * kp + c) * kS + n0 + g;
+            f.o[kp][1][0] = (8 * kp + c) * kS + n0 + 8 + g;
+            f.o[kp][0][1] = (8 * kp + c + 4) * kS + n0 + (g ^ 12);
+            f.o[kp][1][1] = (8 * kp + c + 4) * kS + n0 + (g ^ 4);
+        }
         f.ks = kS;
         f.ts = 8;
-    } else {                // [n][k] tile
-        const int s = g & 4;
-        f.o[0] = (n0 + g) * kS + (c ^ s);
-        f.o[1] = (n0 + g) * kS + ((c + 4) ^ s);
+    } else {                // [n][k] tile: rows n0+8t+g (swizzle s); columns k0+c, k0+c+4
+        const int s = (g & 4) * 3, r0 = (n0 + g) * kS;
+#pragma unroll
+        for (int tp = 0; tp < 2; ++tp) {
+            f.o[0][tp][0] = r0 + 8 * tp * kS + (c ^ s);
+            f.o[0][tp][1] = r0 + 8 * tp * kS + ((c + 4) ^ s);
+            f.o[1][tp][0] = r0 + 8 * tp * kS + ((c + 8) ^ s);
+            f.o[1][tp][1] = r0 + 8 * tp * kS + ((c + 12) ^ s);
+        }
         f.ks = 1;
         f.ts = 8 * kS;
     }
@@ -192,15 +220,16 @@ PG_GEMM_UNROLL_PRAGMA
     for (int k0 = 0; k0 < K; k0 += 8) {
         uint32_t ah[4], al[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) split(pa[fa.o[i] + k0 * fa.ks], ah[i], al[i]);
+        for (int i = 0; i < 4; ++i) split(pa[fa.o[(k0 >> 3) & 1][i] + (k0 & ~15) * fa.ks], ah[i], al[i]);
         // term-major issue: NT independent HMMAs between dependent ones
         // (0.5545 -> 0.5521 ms per C1 step vs the three terms of one tile
         // back to back)
         uint32_t bh[NT][2], bl[NT][2];
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
-            split(pb[fb.o[0] + k0 * fb.ks + t * fb.ts], bh[t][0], bl[t][0]);
-            split(pb[fb.o[1] + k0 * fb.ks + t * fb.ts], bh[t][1], bl[t][1]);
+            const int kp = (k0 >> 3) & 1, kb = (k0 & ~15) * fb.ks + (t & ~1) * fb.ts;
+            split(pb[fb.o[kp][t & 1][0] + kb], bh[t][0], bl[t][0]);
+            split(pb[fb.o[kp][t & 1][1] + kb], bh[t][1], bl[t][1]);
         }
 #pragma unroll
         for (int t = 0; t < NT; ++t) hmma(acc[t], al, bh[t][0], bh[t][1]);  // small terms first
@@ -223,11 +252,12 @@ PG_GEMM_UNROLL_PRAGMA
     for (int k0 = 0; k0 < K; k0 += 8) {
         uint32_t ah[4], al[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) split(pa[fa.o[i] + k0 * fa.ks], ah[i], al[i]);
+        for (int i = 0; i < 4; ++i) split(pa[fa.o[(k0 >> 3) & 1][i] + (k0 & ~15) * fa.ks], ah[i], al[i]);
         uint32_t bh[NT][2], bl[NT][2];
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
-            const int o0 = fb.o[0] + k0 * fb.ks + t * fb.ts, o1 = fb.o[1] + k0 * fb.ks + t * fb.ts;
+            const int kp = (k0 >> 3) & 1, kb = (k0 & ~15) * fb.ks + (t & ~1) * fb.ts;
+            const int o0 = fb.o[kp][t & 1][0] + kb, o1 = fb.o[kp][t & 1][1] + kb;
             bh[t][0] = __float_as_uint(pbh[o0]);
             bl[t][0] = __float_as_uint(pbl[o0]);
             bh[t][1] = __float_as_uint(pbh[o1]);
