@@ -560,21 +560,61 @@ __global__ void __launch_bounds__(tm::kNT *NG, 2 / NG)
         gsync();
         PG_PH(2);
         // ---- layer 2: h2 = relu(h1 W1 + b1) ----
+        float po[4] = {};   // this warp's partial output layer (its 32 hidden units)
         {
             float acc[4][4] = {};
             PG_WGEMM(4, kH, acc, G.h1, 1, kS, 16 * mt, W.w1, W.w1l, kS, 1, 32 * (warp >> 2));
+#ifdef PG_OUT_SEPARATE
             store_frags_T<4>(G.h2, acc, 16 * mt, 32 * (warp >> 2), [&](float v, int n, int) {
                 const float z = v + W.b1[n];
                 return z > 0.0f ? z : 0.0f;
             });
+#else
+            // ReLU in registers: the C fragments are also the A fragments of
+            // the output layer over this warp's 32 hidden units (k-slot c ->
+            // unit 2c, c + 4 -> 2c + 1), so each warp of an m-tile pair
+            // computes a K-half of the output from registers; the halves meet
+            // in G.d3 across the barrier (output phase 7.5% of a tile)
+            const int nb = 32 * (warp >> 2), g = lane >> 2, c = lane & 3;
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float z = acc[t][e] + W.b1[nb + 8 * t + 2 * c + (e & 1)];
+                    acc[t][e] = z > 0.0f ? z : 0.0f;
+                }
+            store_frags_T<4>(G.h2, acc, 16 * mt, nb, [](float v, int, int) { return v; });
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                uint32_t ah[4], al[4], bh0, bl0, bh1, bl1;
+                split(acc[t][0], ah[0], al[0]);
+                split(acc[t][2], ah[1], al[1]);
+                split(acc[t][1], ah[2], al[2]);
+                split(acc[t][3], ah[3], al[3]);
+                split(W.w2[(nb + 8 * t + 2 * c) * 8 + g], bh0, bl0);
+                split(W.w2[(nb + 8 * t + 2 * c + 1) * 8 + g], bh1, bl1);
+                hmma(po, al, bh0, bh1);
+                hmma(po, ah, bl0, bl1);
+                hmma(po, ah, bh0, bh1);
+            }
+            if (warp >= 4) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) G.d3[(16 * mt + g + (e >> 1) * 8) * 8 + 2 * c + (e & 1)] = po[e];
+            }
+#endif
         }
         gsync();
         PG_PH(3);
         // ---- output layer, loss, dL/dout (warps 0-3: one 16-sample tile each) ----
         if (warp < 4) {
             float acc[1][4] = {};
-            warp_gemm<1, kH, false>(acc, G.h2, 1, kS, 16 * warp, W.w2, 8, 1, 0);
             const int gq = lane >> 2, c = lane & 3;
+#ifdef PG_OUT_SEPARATE
+            warp_gemm<1, kH, false>(acc, G.h2, 1, kS, 16 * warp, W.w2, 8, 1, 0);
+#else
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[0][e] = po[e] + G.d3[(16 * warp + gq + (e >> 1) * 8) * 8 + 2 * c + (e & 1)];
+#endif
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int q = 16 * warp + gq + (e >> 1) * 8, j = 2 * c + (e & 1);
