@@ -25,6 +25,8 @@
 //   round trip.  Dense-level feature tables can be placed too (ablation
 //   knob); they are not, because every KB of shared memory comes out of the
 //   L1 that caches the coarse levels' rows.
+#include <type_traits>
+
 #include "pg_encode_dev.cuh"
 #include "pg_umma.cuh"
 
@@ -408,9 +410,12 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
         auto load_h1 = [&]() {
             umma::tmem_ld32(tm_d1 + lane_off + ehalf * 32, v);
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-                const float z = v[c] + S.bias0[ehalf * 32 + c];
-                v[c] = umma::relu_nan(z);   // 1.5% of the decode vs a select
+            for (int c = 0; c < 32; c += 4) {
+                const float4 b4 = *reinterpret_cast<const float4 *>(S.bias0 + ehalf * 32 + c);
+                v[c] = umma::relu_nan(v[c] + b4.x);   // one FMNMX (1.5% of the decode vs a select)
+                v[c + 1] = umma::relu_nan(v[c + 1] + b4.y);
+                v[c + 2] = umma::relu_nan(v[c + 2] + b4.z);
+                v[c + 3] = umma::relu_nan(v[c + 3] + b4.w);
             }
         };
         if (NG == 1) load_h1();
@@ -450,17 +455,27 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
         {
             umma::tmem_ld32(tm_d2 + lane_off + ehalf * 32, v);
             float acc[kOutMax] = {0.0f, 0.0f, 0.0f, 0.0f};
+            // biases by float4; the fourth output column only when od > 3
+            // (its weights are zero otherwise)
+            auto out_layer = [&](auto four) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-                const int k = ehalf * 32 + c;
-                float h = v[c] + S.bias1[k];
-                h = umma::relu_nan(h);
-                const float4 w = *reinterpret_cast<const float4 *>(S.w2 + k * kOutMax);
-                acc[0] = fmaf(h, w.x, acc[0]);
-                acc[1] = fmaf(h, w.y, acc[1]);
-                acc[2] = fmaf(h, w.z, acc[2]);
-                acc[3] = fmaf(h, w.w, acc[3]);
-            }
+                for (int c = 0; c < 32; c += 4) {
+                    const float4 b4 = *reinterpret_cast<const float4 *>(S.bias1 + ehalf * 32 + c);
+                    const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int k = ehalf * 32 + c + u;
+                        const float h = umma::relu_nan(v[c + u] + bb[u]);
+                        const float4 w = *reinterpret_cast<const float4 *>(S.w2 + k * kOutMax);
+                        acc[0] = fmaf(h, w.x, acc[0]);
+                        acc[1] = fmaf(h, w.y, acc[1]);
+                        acc[2] = fmaf(h, w.z, acc[2]);
+                        if (decltype(four)::value) acc[3] = fmaf(h, w.w, acc[3]);
+                    }
+                }
+            };
+            if (od > 3) out_layer(std::true_type{});
+            else out_layer(std::false_type{});
             *reinterpret_cast<float4 *>(G.opA + (ehalf * kTP + erow) * kOutMax) =
                 make_float4(acc[0], acc[1], acc[2], acc[3]);
         }
