@@ -710,7 +710,8 @@ int64_t pg_cells_plan_rows(const pg_grid *grid, int64_t budget_bytes, int row_by
         int64_t cells = 1;
         for (int a = 0; a < grid->d; ++a) cells *= grid->res[l];
         const int64_t bytes = cells * C * row_bytes;
-        if (total + bytes > budget_bytes) {
+        // the decode indexes a level's records with 32-bit math
+        if (total + bytes > budget_bytes || cells > ((int64_t)1 << 30)) {
             open = false;
             continue;
         }

@@ -73,7 +73,9 @@ __device__ __forceinline__ float2 encode_level_fwd2_cell(const pg_grid &g, int l
         c[a] = cell_coord(x[a], res, t[a]);
         omt[a] = __fsub_rn(1.0f, t[a]);
     }
-    int64_t cell = c[D - 1];
+    // cached levels hold res^D <= 2^27 cells (the cache budget), so 32-bit
+    // index math suffices
+    int cell = c[D - 1];
 #pragma unroll
     for (int a = D - 2; a >= 0; --a) cell = cell * res + c[a];
     uint32_t r[C];
