@@ -476,8 +476,12 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
             };
             if (od > 3) out_layer(std::true_type{});
             else out_layer(std::false_type{});
-            *reinterpret_cast<float4 *>(G.opA + (ehalf * kTP + erow) * kOutMax) =
-                make_float4(acc[0], acc[1], acc[2], acc[3]);
+            // packed [half][query][od]: the output loop below then reads
+            // consecutive words (a [query][4] float4 layout left its reads
+            // 2-way bank conflicted)
+#pragma unroll
+            for (int j = 0; j < kOutMax; ++j)
+                if (j < od) G.opA[(ehalf * kTP + erow) * od + j] = acc[j];
         }
         umma::fence_before_sync();
         group_sync(grp);
@@ -486,7 +490,7 @@ __global__ void __launch_bounds__(tc::kGT *NG, MINB)
             float *dst = out + p0 * od;
             for (int i = gt; i < nv * od; i += kGT) {
                 const int q = (int)(((uint32_t)i * od_mag) >> 16), j = i - q * od;   // 1.1% vs i / od
-                float o = S.bias2[j] + G.opA[q * kOutMax + j] + G.opA[(kTP + q) * kOutMax + j];
+                float o = S.bias2[j] + G.opA[i] + G.opA[kTP * od + i];
                 if (sigmoid) o = (float)(1.0 / (1.0 + exp(-(double)o)));
                 if (pol_first) st_hint(dst + i, o, pol_first);
                 else dst[i] = o;
