@@ -1,6 +1,5 @@
-for i in 1 2; do
-python tools/time_decode_lib.py paper_2312_17241_b200/libprobegrid_b200.so base
-python tools/time_decode_lib.py tools/_var_prev/lib.so prev
-done
-python -m pytest tests/test_gpu_c2_parity.py tests/test_gpu_cngp.py -q -x 2>&1 | tail -2
-python -m pytest tests/test_gpu_parity.py -q -x -k "decode or umma or infer" 2>&1 | tail -2
+L=paper_2312_17241_b200/libprobegrid_b200.so
+for r in 4 8 16 32; do PG_TRAIN_REPS=$r python tools/time_c3_lib.py $L reps$r; done
+PG_TRAIN_AGG_RANGES=64 python tools/time_c3_lib.py $L agg64
+PG_TRAIN_AGG_RANGES=64 PG_TRAIN_REPS=1 python tools/time_c3_lib.py $L agg64_reps1
+for mb in 0 32 128; do PG_TRAIN_CELL_MB=$mb python tools/time_c3_lib.py $L cells$mb; done
