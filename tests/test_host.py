@@ -135,3 +135,41 @@ def test_round2_host_rules():
     from paper_2312_17241_b200 import decode
     if "PG_DECODE_CELL_MB" not in os.environ:
         assert decode.CELL_BUDGET == 96 << 20
+
+
+def test_training_tile_swizzle_is_bank_conflict_free():
+    """Restates pg_train_mma.cu's tile layout (row stride kS = 72 floats,
+    column ^ 12 in rows with bit 2 set: sw()) and checks the three warp access
+    patterns it is designed for hit 32 distinct banks: fragment walks over 4
+    rows x 8 columns (P1) and 8 rows x 4 columns (P2, the weight-gradient and
+    W^T GEMMs), and the C-fragment stores (rows 2c / 2c+1, columns g)."""
+    kS = 72
+
+    def sw(r, c):
+        return r * kS + (c ^ ((r & 4) * 3))
+
+    def distinct(cells):
+        banks = [sw(r, c) % 32 for r, c in cells]
+        return len(set(banks)) == 32
+
+    for R in range(0, 64, 4):
+        for C in range(0, 64, 8):
+            assert distinct([(R + c, C + g) for c in range(4) for g in range(8)])
+    for R in range(0, 64, 8):
+        for C in range(0, 64, 4):
+            assert distinct([(R + g, C + c) for g in range(8) for c in range(4)])
+        for C in range(0, 64, 8):
+            for e in (0, 1):
+                assert distinct([(R + 2 * c + e, C + g) for c in range(4) for g in range(8)])
+    # the swizzle permutes columns within each row (a bijection on [0, 64))
+    for r in range(64):
+        assert sorted(sw(r, c) - r * kS for c in range(64)) == list(range(64))
+
+
+def test_decode_output_index_reciprocal():
+    """pg_decode_tc.cu splits the output index i into (query, column) with
+    q = (i * ceil(2^16 / od)) >> 16: exact for every i < 128 * od it sees."""
+    for od in range(1, 5):
+        mag = (65536 + od - 1) // od
+        for i in range(128 * od):
+            assert (i * mag) >> 16 == i // od
